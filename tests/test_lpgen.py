@@ -1,0 +1,54 @@
+"""Generator contracts."""
+import numpy as np
+
+import lpgen
+
+
+def test_determinism():
+    a = lpgen.twophase_signed(7, 9, 6, 3)
+    b = lpgen.twophase_signed(7, 9, 6, 3)
+    for x, y in zip(a, b):
+        assert np.array_equal(x, y)
+
+
+def test_g1_feasible_start_bounded():
+    A, b, c = lpgen.signed_bounded(50, 6, 4, 1)
+    assert A.shape == (50, 6, 4) and b.shape == (50, 6) and c.shape == (50, 4)
+    assert np.all(b >= 1.0) and np.all(A[:, 0, :] >= 1.0)
+
+
+def test_g2_cover_rows_negative_and_xstar_feasible():
+    B, m, n = 40, 12, 7
+    A, b, c = lpgen.twophase_signed(B, m, n, 5)
+    kk = int(np.ceil(m / 4))
+    assert np.all((b < 0).sum(axis=1) == kk)
+    assert np.all(b[:, 0] > 0)  # the budget row is never a cover row
+
+
+def test_oct_and_box_counts():
+    assert lpgen.box_directions(3).shape == (6, 3)
+    for n in (2, 5, 28):
+        d = lpgen.oct_directions(n)
+        assert d.shape == (2 * n * n, n)
+        np.testing.assert_allclose(np.linalg.norm(d, axis=1), 1.0, atol=1e-12)
+
+
+def test_g3_box_and_dirs():
+    lo, hi, dirs = lpgen.hyperbox(100, 5, 4)
+    np.testing.assert_allclose(hi - lo, 0.02, atol=1e-15)
+    np.testing.assert_allclose((lo + hi) / 2, [1, 0, 0, 0, 0], atol=1e-15)
+    assert dirs.shape == (100, 5)
+    lo, hi, dirs = lpgen.hyperbox(3000, 28, 5)
+    assert np.all(hi > lo) and dirs.shape == (3000, 28)
+    np.testing.assert_allclose(np.linalg.norm(dirs, axis=1), 1.0, atol=1e-12)
+
+
+def test_status_mix_negated_rows():
+    A, b, c = lpgen.status_mix(30, 8, 5, 2, infeasible_start=True)
+    assert np.all((b < 0).sum(axis=1) == 2)
+
+
+def test_config_table():
+    assert lpgen.CONFIGS["cfg2"]["B"] == 50000 and lpgen.CONFIGS["cfg5"]["B"] == 6003000
+    A, b, c = lpgen.make_config("cfg3", B=3)
+    assert A.shape == (3, 200, 200) and np.all((b < 0).sum(axis=1) == 50)
