@@ -55,7 +55,8 @@ def signed_bounded(B: int, m: int, n: int, seed: int):
 def twophase_signed(B: int, m: int, n: int, seed: int):
     """G2 (type-2 workload).  Feasible by construction (x* is feasible) with
     kk = ceil(m/4) covering rows (SPEC.md:357 count) whose b < 0, so the slack basis is
-    infeasible and phase I is needed.
+    infeasible and phase I is needed.  Non-cover rows get
+    b_i = max(A_i x*, 0) + U[1,100) (>= 1), covering rows b_i = -(Q_i x*) + U[0,1).
 
     Draw order: A U[-10,10)^{BxMxN}; budget U[1,10)^{BxN}; x* U[0,1)^{BxN};
     slack U[1,100)^{BxM}; keys U[0,1)^{Bx(M-1)}; cover U[1,10)^{BxKKxN};
@@ -70,7 +71,9 @@ def twophase_signed(B: int, m: int, n: int, seed: int):
     cover = g.uniform(1.0, 10.0, size=(B, max(kk, 0), n))
     cover_slack = g.uniform(0.0, 1.0, size=(B, max(kk, 0)))
     c = g.uniform(-10.0, 10.0, size=(B, n))
-    b = np.einsum("bij,bj->bi", A, xs) + slack
+    # max(., 0) keeps every non-cover b_i >= 1 (x* stays feasible), so exactly kk rows start
+    # infeasible, as SPEC.md:357 states ("forces ceil(m/4) entries of b negative")
+    b = np.maximum(np.einsum("bij,bj->bi", A, xs), 0.0) + slack
     if kk > 0:
         rows = 1 + np.argsort(keys, axis=1, kind="stable")[:, :kk]
         bi = np.arange(B)[:, None]
