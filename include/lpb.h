@@ -1,0 +1,158 @@
+/*
+ * lpb.h — C ABI of the B200-native batched LP solver (paper_1609_08114_b200/liblpb.so).
+ *
+ * Solves a batch of independent linear programs in standard form
+ *     maximize c.x  subject to  A x <= b,  x >= 0                (Eq. 1-3)
+ * with the dense-tableau simplex method (Dantzig's "Largest Positive Coefficient" entering
+ * rule; ratio test PAPER.md:97,126; pivot PAPER.md:163-172), the two-phase
+ * method when the slack basis is infeasible, and the closed-form hyperbox LP
+ * (Eq. 6).  One LP per CUDA thread block (or thread-block cluster, or
+ * thread), as in PAPER.md:114 ("We assign a CUDA block of threads to solve an LP").
+ *
+ * Conventions
+ *   - Every call returns int: LPB_OK (0) or a negative error code.  No C++ exception crosses
+ *     the ABI.  Per-LP outcomes (optimal / unbounded / infeasible / ...) are DATA returned in
+ *     the status array, never call errors (a pathological LP does not fail the batch).
+ *   - All floating point is IEEE fp64.  Inputs must be finite (caller contract; no NaN scan).
+ *   - One context is used by one host thread at a time.  Contexts are independent (e.g. one
+ *     per GPU / torch.distributed rank).
+ *
+ * Layouts (LP-contiguous, index-aligned: output k belongs to input LP k)
+ *   A    : batch x m x n, row-major        A[(k*m + i)*n + j]
+ *   b    : batch x m                       b[k*m + i]
+ *   c    : batch x n                       c[k*n + j]
+ *   status: int32[batch]   obj: f64[batch]   x: f64[batch*n]   iters: int32[batch*2]
+ *          (iters[2k] = phase-I pivots incl. artificial drive-outs, iters[2k+1] = phase-II)
+ *   Non-optimal LPs report obj = +inf (UNBOUNDED), -inf (INFEASIBLE), NaN (ITER_LIMIT,
+ *   NUMERICAL) and x = NaN.
+ *
+ * Hyperbox kind (LPB_HYPERBOX): the feasible region is the box [lo_1,hi_1] x ... x [lo_n,hi_n]
+ *   encoded literally as A x <= b with A = [I; -I] (implicit: pass A = NULL), m = 2n and
+ *   b = [hi_1..hi_n, -lo_1..-lo_n]; c holds the direction l.  With LPB_SHARED_BOX one box is
+ *   shared by the whole batch (b has 2n entries; the paper's experiment).  NOTE:
+ *   x >= 0 is NOT implied for this kind; the box is the whole feasible region.
+ *   Result: obj = sum_i l_i h_i, h_i = lo_i if l_i < 0 else hi_i, x = h, status OPTIMAL, or
+ *   INFEASIBLE when some lo_i > hi_i.
+ *
+ * Ownership
+ *   The caller owns every array.  Without LPB_ASYNC, lpb_solve_batch has consumed its
+ *   inputs when it returns (the library keeps no caller pointer).  With LPB_ASYNC the work is
+ *   only enqueued on the context's stream: the caller keeps inputs alive until lpb_results /
+ *   lpb_sync returns.  Results live in context-owned device memory until the next solve.
+ */
+#ifndef LPB_H_
+#define LPB_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct lpb_ctx lpb_ctx; /* opaque, owned by the library */
+
+enum { LPB_GENERAL = 0, LPB_HYPERBOX = 1 }; /* problem kind */
+
+enum { /* per-LP status (data, not an error) */
+  LPB_OPTIMAL = 0,    /* no entering variable: reduced costs all <= eps_enter  */
+  LPB_UNBOUNDED = 1,  /* no leaving variable in phase II                       */
+  LPB_INFEASIBLE = 2, /* phase-I optimum w* > eps_phase1*max(1,|b|_inf)         */
+  LPB_ITER_LIMIT = 3, /* phase-I + phase-II pivots reached max_iter                           */
+  LPB_NUMERICAL = 4   /* phase I reported unbounded (impossible in exact arithmetic)          */
+};
+
+enum { /* call errors */
+  LPB_OK = 0,
+  LPB_EINVAL = -1,  /* batch <= 0, m or n <= 0, NULL required pointer, bad kind / options     */
+  LPB_ENOMEM = -2,  /* device or pinned-host allocation failed                                */
+  LPB_ECUDA = -3,   /* a CUDA runtime error (text via lpb_strerror / lpb_last_error)          */
+  LPB_ESTATE = -4,  /* results requested before any solve                                     */
+  LPB_ETOOBIG = -5  /* no compiled size class fits (m, n)                                     */
+};
+
+enum { /* lpb_solve_batch flags */
+  LPB_DEVICE_PTRS = 1u, /* A, b, c are device pointers (e.g. torch CUDA tensors)              */
+  LPB_SHARED_BOX = 2u,  /* hyperbox: one box (2n entries of b) for the whole batch             */
+  LPB_NO_X = 4u,        /* do not produce x (saves 8n bytes per LP of HBM / D2H traffic)       */
+  LPB_ASYNC = 8u        /* enqueue only; do not synchronize before returning                   */
+};
+
+typedef struct {
+  int32_t struct_size; /* = sizeof(lpb_options); ABI versioning                               */
+  double eps_enter;    /* 1e-9: Step 1 candidates have reduced cost d_j > eps_enter          */
+  double eps_piv;      /* 1e-9: Step 2 candidates have pivot-column entry a_ie > eps_piv     */
+  double eps_phase1;   /* 1e-9: infeasible iff w* > eps_phase1 * max(1, |b|_inf)             */
+  int32_t max_iter;    /* 0 -> 50*(n+m) pivots (phase I + phase II), then LPB_ITER_LIMIT     */
+  int32_t bland_after; /* 0 -> n+m consecutive degenerate pivots switch to Bland's rule;
+                          < 0 -> never (pure Dantzig)                                         */
+  int32_t device;      /* CUDA device ordinal; -1 -> the current device                       */
+  void* stream;        /* cudaStream_t to run on; NULL -> a stream owned by the context       */
+  int32_t n_chunks;    /* host-pointer pipeline depth; 0 -> 10 if batch > 100 else 1
+                          (the paper's stream count)                            */
+  int32_t kernel_class;/* 0 auto; 1 S (thread/LP), 2 M (block/LP), 3 L (2-CTA cluster/LP),
+                          4 R (block/LP, register-resident tableau); for tests / benches     */
+  int32_t grid_ctas;   /* 0 auto; persistent grid size override (scheduling-invariance tests) */
+} lpb_options;
+
+/* Fill *o with the defaults above.  Returns LPB_EINVAL if o is NULL. */
+int lpb_default_options(lpb_options* o);
+
+/* Create a context for batches of up to `batch` LPs of size m x n of the given kind.
+ * o may be NULL (defaults).  Allocates device result buffers for `batch` LPs.
+ * Errors: LPB_EINVAL (batch <= 0, m/n <= 0, kind invalid, hyperbox with m != 2n),
+ *         LPB_ETOOBIG (no size class holds m x n), LPB_ENOMEM, LPB_ECUDA. */
+int lpb_create(lpb_ctx** out, int64_t batch, int32_t m, int32_t n, int32_t kind,
+               const lpb_options* o);
+
+/* Solve the context's batch (size given at create).  A must be NULL for LPB_HYPERBOX.
+ * Host pointers (default): inputs are copied host->device through pinned staging in
+ * n_chunks chunks on separate streams, each chunk's kernel overlapping the next chunk's copy
+ * (PAPER.md:185-206).  With LPB_DEVICE_PTRS the kernels read the caller's device arrays.
+ * Errors: LPB_EINVAL (NULL required pointer), LPB_ECUDA, LPB_ENOMEM. */
+int lpb_solve_batch(lpb_ctx* c, const double* A, const double* b, const double* cvec,
+                    uint32_t flags);
+
+/* lpb_solve_batch + results in one call: the result arrays (host or device pointers; any may
+ * be NULL) are filled per chunk, so on the host-pointer path chunk c's D2H overlaps chunk
+ * c+1's kernel (the paper's "D2H-res").  This is the end-to-end entry point.
+ * Errors: as lpb_solve_batch. */
+int lpb_solve_batch_into(lpb_ctx* c, const double* A, const double* b, const double* cvec,
+                         uint32_t flags, int32_t* status, double* obj, double* x,
+                         int32_t* iters);
+
+/* Copy results out (host or device pointers; cudaMemcpyDefault).  Any pointer may be NULL
+ * to skip that output.  Synchronizes the context's stream.  x is not available when the
+ * last solve used LPB_NO_X (x must then be NULL).  Errors: LPB_ESTATE, LPB_EINVAL,
+ * LPB_ECUDA. */
+int lpb_results(lpb_ctx* c, int32_t* status, double* obj, double* x, int32_t* iters);
+
+/* Zero-copy access: device pointers of the context-owned result arrays (valid until the
+ * next solve or destroy).  Any out-pointer may be NULL.  Does not synchronize. */
+int lpb_result_device_ptrs(lpb_ctx* c, int32_t** status, double** obj, double** x,
+                           int32_t** iters);
+
+/* Wait for all work enqueued by this context.  Errors: LPB_ECUDA. */
+int lpb_sync(lpb_ctx* c);
+
+/* Device-event timing of the last solve (synchronizes): solve_ms brackets the kernel
+ * launches only (inputs resident on the device); e2e_ms brackets first H2D copy -> last D2H
+ * copy for host-pointer solves (equal to solve_ms for device-pointer solves). */
+int lpb_last_timing(lpb_ctx* c, double* solve_ms, double* e2e_ms);
+
+/* Number of kernel launches the last solve issued (for the bench's gpu_launches count),
+ * and the size class it dispatched to (1 S, 2 M, 3 L, 4 R, 5 H). */
+int lpb_last_launch_info(lpb_ctx* c, int32_t* launches, int32_t* kernel_class);
+
+/* Release every resource of the context.  NULL is accepted. */
+int lpb_destroy(lpb_ctx* c);
+
+/* Static text for an error code. */
+const char* lpb_strerror(int err);
+
+/* Text of the last CUDA error seen by this context ("" if none). */
+const char* lpb_last_error(lpb_ctx* c);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LPB_H_ */

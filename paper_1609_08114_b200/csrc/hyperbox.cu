@@ -1,0 +1,130 @@
+// hyperbox.cu — H class: the closed-form hyperbox LP (§6, Eq. 6):
+//     max_{x in B} l.x = sum_i l_i h_i,  h_i = lo_i if l_i < 0 else hi_i   (l_i = 0 -> hi_i)
+// One LP per thread (the paper also uses one thread per LP), but the
+// HBM traffic is staged through shared memory so that every global access is coalesced:
+//   1. the CTA's tile of TILE LPs x n directions (a contiguous TILE*n*8-byte run) is read
+//      with consecutive 8-byte loads across the block into a padded SMEM tile (odd row
+//      stride: the per-thread row reads in step 2 are bank-conflict free);
+//   2. each thread evaluates its LP: the sequential chain acc = fma(l_i, h_i, acc),
+//      i = 0..n-1 from acc = 0 (the oracle's order, bit-exact), writes h back in place;
+//   3. obj/status are stored per thread (coalesced) and x = h leaves through the same
+//      coalesced walk.
+// The box (2n fp64) is shared by the batch (LPB_SHARED_BOX, the paper's experiment,
+// PAPER.md:313) and lives in SMEM; a per-LP box is read from global memory.
+// This kernel is HBM-bound: 8n bytes in + (8n + 12) bytes out per LP.
+#include "lpb_internal.cuh"
+
+namespace lpb {
+namespace {
+
+constexpr int HB_NT = 256;  // threads = LPs per tile
+
+__global__ void __launch_bounds__(HB_NT) hyperbox_kernel(HyperboxArgs a) {
+  extern __shared__ __align__(16) double hsm[];
+  const int n = a.n;
+  const int S = n | 1;
+  double* tile = hsm;                      // HB_NT x S
+  double* blo = tile + (size_t)HB_NT * S;  // n
+  double* bhi = blo + n;                   // n
+  const int tid = threadIdx.x;
+  if (a.shared_box) {
+    for (int i = tid; i < n; i += HB_NT) {
+      bhi[i] = a.box[i];
+      blo[i] = -a.box[n + i];
+    }
+  }
+  // incremental divmod of the flat tile index by n
+  const int r0 = tid / n, j0 = tid - r0 * n;
+  const int dq = HB_NT / n, dr = HB_NT - dq * n;
+  const int64_t ntiles = (a.batch + HB_NT - 1) / HB_NT;
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const int64_t lp0 = t * HB_NT;
+    const int64_t left = a.batch - lp0;
+    const int rows = left < HB_NT ? (int)left : HB_NT;
+    const int total = rows * n;
+    const double* __restrict__ src = a.l + lp0 * n;
+    {
+      int r = r0, j = j0;
+      for (int f = tid; f < total; f += HB_NT) {
+        tile[r * S + j] = __ldcs(src + f);  // streamed once: evict-first
+        j += dr;
+        r += dq;
+        if (j >= n) { j -= n; ++r; }
+      }
+    }
+    __syncthreads();
+    if (tid < rows) {
+      const int64_t lp = lp0 + tid;
+      const double* lo = blo;
+      const double* hi = bhi;
+      if (!a.shared_box) {
+        // per-LP box from global memory (b = [hi; -lo] per LP)
+        const double* bx = a.box + lp * 2 * (int64_t)n;
+        double* row = tile + tid * S;
+        bool empty = false;
+        double acc = 0.0;
+        for (int i = 0; i < n; ++i) {
+          const double h_hi = __ldg(bx + i), h_lo = -__ldg(bx + n + i);
+          empty |= (h_lo > h_hi);
+          const double li = row[i];
+          const double h = (li < 0.0) ? h_lo : h_hi;
+          acc = __fma_rn(li, h, acc);
+          row[i] = h;
+        }
+        a.status[lp] = empty ? ST_INFEASIBLE : ST_OPTIMAL;
+        a.obj[lp] = empty ? __longlong_as_double(0xfff0000000000000ll) : acc;
+        if (empty)
+          for (int i = 0; i < n; ++i) row[i] = __longlong_as_double(0x7ff8000000000000ll);
+      } else {
+        double* row = tile + tid * S;
+        bool empty = false;
+        double acc = 0.0;
+        for (int i = 0; i < n; ++i) {
+          const double li = row[i];
+          const double h = (li < 0.0) ? lo[i] : hi[i];
+          empty |= (lo[i] > hi[i]);
+          acc = __fma_rn(li, h, acc);
+          row[i] = h;
+        }
+        __stcs(a.status + lp, empty ? ST_INFEASIBLE : ST_OPTIMAL);
+        __stcs(a.obj + lp, empty ? __longlong_as_double(0xfff0000000000000ll) : acc);
+        if (empty)
+          for (int i = 0; i < n; ++i) row[i] = __longlong_as_double(0x7ff8000000000000ll);
+      }
+    }
+    __syncthreads();
+    if (a.x) {
+      double* __restrict__ dst = a.x + lp0 * n;
+      int r = r0, j = j0;
+      for (int f = tid; f < total; f += HB_NT) {
+        __stcs(dst + f, tile[r * S + j]);
+        j += dr;
+        r += dq;
+        if (j >= n) { j -= n; ++r; }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_hyperbox(const HyperboxArgs& a, cudaStream_t s) {
+  const int S = a.n | 1;
+  const size_t smem = sizeof(double) * ((size_t)HB_NT * S + 2 * (size_t)a.n);
+  if (smem > 227 * 1024) return cudaErrorInvalidValue;
+  cudaError_t e = cudaFuncSetAttribute(hyperbox_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, hyperbox_kernel, HB_NT, smem);
+  if (e != cudaSuccess) return e;
+  const int64_t ntiles = (a.batch + HB_NT - 1) / HB_NT;
+  int64_t grid = (int64_t)per_sm * device_sm_count();
+  if (grid > ntiles) grid = ntiles;
+  if (grid < 1) grid = 1;
+  hyperbox_kernel<<<(unsigned)grid, HB_NT, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace lpb

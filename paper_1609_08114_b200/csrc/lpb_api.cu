@@ -1,0 +1,471 @@
+// lpb_api.cu — the C ABI (include/lpb.h): contexts, size-class dispatch, the host<->device
+// stream pipeline and device-event timing.  No torch types, plain pointers only.
+//
+// Host pipeline (§4.4: H2D-ST -> kernel -> D2H-res on CUDA streams,
+// 10 streams above 100 LPs): the batch is cut into n_chunks contiguous chunks; chunk c
+// runs H2D(A,b,c) -> solve kernel -> D2H(results) on its own stream, so chunk c+1's copy
+// overlaps chunk c's kernel.  Unlike the paper, only the raw A, b, c cross PCIe (the
+// tableau is built on the device), which halves the bytes of a full-tableau H2D.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <vector>
+
+#include "../../include/lpb.h"
+#include "lpb_internal.cuh"
+
+namespace lpb {
+int device_sm_count() {
+  static int cache[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (cache[dev] == 0) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    cache[dev] = v > 0 ? v : 1;
+  }
+  return cache[dev];
+}
+}  // namespace lpb
+
+using namespace lpb;
+
+struct lpb_ctx {
+  int64_t batch = 0;
+  int m = 0, n = 0, kind = 0;
+  lpb_options opt{};
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  // context-owned device results
+  int32_t* d_status = nullptr;
+  double* d_obj = nullptr;
+  double* d_x = nullptr;
+  int32_t* d_iters = nullptr;
+  // device input buffers for host-pointer solves (allocated on first use)
+  double* d_A = nullptr;
+  double* d_b = nullptr;
+  double* d_c = nullptr;
+  int* d_ticket = nullptr;  // one counter per chunk
+  int* d_kmax = nullptr;
+  int* h_kmax = nullptr;    // pinned
+  std::vector<cudaStream_t> chunk_streams;
+  std::vector<cudaEvent_t> chunk_done;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  bool solved = false, last_nox = false, host_path = false;
+  int last_launches = 0, last_class = 0;
+  char err[256] = {0};
+};
+
+static int set_cuda_err(lpb_ctx* c, cudaError_t e, const char* where) {
+  if (c) std::snprintf(c->err, sizeof(c->err), "%s: %s", where, cudaGetErrorString(e));
+  return LPB_ECUDA;
+}
+
+#define LPB_CUDA(ctx, call)                                  \
+  do {                                                       \
+    cudaError_t e_ = (call);                                 \
+    if (e_ != cudaSuccess) return set_cuda_err(ctx, e_, #call); \
+  } while (0)
+
+extern "C" int lpb_default_options(lpb_options* o) {
+  if (!o) return LPB_EINVAL;
+  std::memset(o, 0, sizeof(*o));
+  o->struct_size = (int32_t)sizeof(lpb_options);
+  o->eps_enter = 1e-9;
+  o->eps_piv = 1e-9;
+  o->eps_phase1 = 1e-9;
+  o->max_iter = 0;
+  o->bland_after = 0;
+  o->device = -1;
+  o->stream = nullptr;
+  o->n_chunks = 0;
+  o->kernel_class = 0;
+  o->grid_ctas = 0;
+  return LPB_OK;
+}
+
+extern "C" const char* lpb_strerror(int err) {
+  switch (err) {
+    case LPB_OK: return "ok";
+    case LPB_EINVAL: return "invalid argument";
+    case LPB_ENOMEM: return "out of memory";
+    case LPB_ECUDA: return "CUDA error";
+    case LPB_ESTATE: return "results requested before a solve";
+    case LPB_ETOOBIG: return "no compiled size class fits this LP size";
+    default: return "unknown error";
+  }
+}
+
+extern "C" const char* lpb_last_error(lpb_ctx* c) { return c ? c->err : ""; }
+
+// Size-class capacity check at the best case (no artificial rows).
+static bool general_fits_any(int m, int n) {
+  return thread_fits(m, n) || block_fits(1, m, n, 0) || block_fits(2, m, n, 0) ||
+         block_fits(4, m, n, 0);
+}
+
+extern "C" int lpb_create(lpb_ctx** out, int64_t batch, int32_t m, int32_t n, int32_t kind,
+                          const lpb_options* o) {
+  if (!out) return LPB_EINVAL;
+  *out = nullptr;
+  if (batch <= 0 || m <= 0 || n <= 0) return LPB_EINVAL;
+  if (kind != LPB_GENERAL && kind != LPB_HYPERBOX) return LPB_EINVAL;
+  if (kind == LPB_HYPERBOX && m != 2 * n) return LPB_EINVAL;
+  lpb_options opt;
+  lpb_default_options(&opt);
+  if (o) {
+    if (o->struct_size != (int32_t)sizeof(lpb_options)) return LPB_EINVAL;
+    opt = *o;
+  }
+  if (!(opt.eps_enter >= 0) || !(opt.eps_piv >= 0) || !(opt.eps_phase1 >= 0)) return LPB_EINVAL;
+  if (kind == LPB_GENERAL && !general_fits_any(m, n)) return LPB_ETOOBIG;
+  if (kind == LPB_HYPERBOX && (size_t)(n | 1) * 256 * 8 > 200 * 1024) return LPB_ETOOBIG;
+
+  lpb_ctx* c = new (std::nothrow) lpb_ctx();
+  if (!c) return LPB_ENOMEM;
+  c->batch = batch;
+  c->m = m;
+  c->n = n;
+  c->kind = kind;
+  c->opt = opt;
+  int dev = opt.device;
+  if (dev < 0) {
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) { set_cuda_err(c, e, "cudaGetDevice"); delete c; return LPB_ECUDA; }
+  }
+  c->device = dev;
+  cudaError_t e = cudaSetDevice(dev);
+  if (e == cudaSuccess) {
+    if (opt.stream) {
+      c->stream = (cudaStream_t)opt.stream;
+    } else {
+      e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+      c->own_stream = true;
+    }
+  }
+  if (e == cudaSuccess) e = cudaMalloc(&c->d_status, sizeof(int32_t) * batch);
+  if (e == cudaSuccess) e = cudaMalloc(&c->d_obj, sizeof(double) * batch);
+  if (e == cudaSuccess) e = cudaMalloc(&c->d_x, sizeof(double) * batch * (int64_t)n);
+  if (e == cudaSuccess) e = cudaMalloc(&c->d_iters, sizeof(int32_t) * 2 * batch);
+  if (e == cudaSuccess) e = cudaMalloc(&c->d_ticket, sizeof(int) * 64);
+  if (e == cudaSuccess) e = cudaMalloc(&c->d_kmax, sizeof(int));
+  if (e == cudaSuccess) e = cudaMallocHost(&c->h_kmax, sizeof(int));
+  if (e == cudaSuccess) e = cudaEventCreate(&c->ev0);
+  if (e == cudaSuccess) e = cudaEventCreate(&c->ev1);
+  if (e != cudaSuccess) {
+    const bool oom = (e == cudaErrorMemoryAllocation);
+    set_cuda_err(c, e, "lpb_create");
+    lpb_destroy(c);
+    return oom ? LPB_ENOMEM : LPB_ECUDA;
+  }
+  *out = c;
+  return LPB_OK;
+}
+
+extern "C" int lpb_destroy(lpb_ctx* c) {
+  if (!c) return LPB_OK;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  for (auto s : c->chunk_streams) { cudaStreamSynchronize(s); cudaStreamDestroy(s); }
+  for (auto ev : c->chunk_done) cudaEventDestroy(ev);
+  cudaFree(c->d_status);
+  cudaFree(c->d_obj);
+  cudaFree(c->d_x);
+  cudaFree(c->d_iters);
+  cudaFree(c->d_A);
+  cudaFree(c->d_b);
+  cudaFree(c->d_c);
+  cudaFree(c->d_ticket);
+  cudaFree(c->d_kmax);
+  if (c->h_kmax) cudaFreeHost(c->h_kmax);
+  if (c->ev0) cudaEventDestroy(c->ev0);
+  if (c->ev1) cudaEventDestroy(c->ev1);
+  if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+  return LPB_OK;
+}
+
+// Choose the simplex size class for a known kmax (forced class honoured when it fits).
+static int choose_class(const lpb_ctx* c, int kmax, int* cl) {
+  const int m = c->m, n = c->n;
+  const int forced = c->opt.kernel_class;
+  *cl = 1;
+  if (forced == CLASS_S) return thread_fits(m, n) ? CLASS_S : -1;
+  if (forced == CLASS_R) return reg_fits(m, n, kmax) ? CLASS_R : -1;
+  if (forced == CLASS_M) return block_fits(1, m, n, kmax) ? CLASS_M : -1;
+  if (forced == CLASS_L) {
+    for (int q : {2, 4})
+      if (block_fits(q, m, n, kmax)) { *cl = q; return CLASS_L; }
+    return -1;
+  }
+  if (reg_fits(m, n, kmax)) return CLASS_R;
+  if (block_fits(1, m, n, kmax)) return CLASS_M;
+  for (int q : {2, 4})
+    if (block_fits(q, m, n, kmax)) { *cl = q; return CLASS_L; }
+  return -1;
+}
+
+static void fill_args(const lpb_ctx* c, SimplexArgs& a, int64_t lp0, int64_t cnt,
+                      const double* A, const double* b, const double* cv, bool nox,
+                      int kmax, int* ticket) {
+  const int m = c->m, n = c->n;
+  a.batch = cnt;
+  a.m = m;
+  a.n = n;
+  a.A = A;
+  a.b = b;
+  a.c = cv;
+  a.status = c->d_status + lp0;
+  a.obj = c->d_obj + lp0;
+  a.x = nox ? nullptr : c->d_x + lp0 * n;
+  a.iters = c->d_iters + 2 * lp0;
+  a.eps_enter = c->opt.eps_enter;
+  a.eps_piv = c->opt.eps_piv;
+  a.eps_phase1 = c->opt.eps_phase1;
+  a.max_iter = c->opt.max_iter > 0 ? c->opt.max_iter : 50 * (n + m);
+  a.bland_K = c->opt.bland_after == 0 ? n + m : c->opt.bland_after;
+  a.kmax = kmax;
+  a.ticket = ticket;
+}
+
+// Enqueue the general-LP kernels for one resident chunk on stream s.
+static int run_general(lpb_ctx* c, cudaStream_t s, int64_t lp0, int64_t cnt, const double* A,
+                       const double* b, const double* cv, bool nox, int kmax_known,
+                       int* ticket, int* launches) {
+  int kmax = kmax_known;
+  const bool s_class = (c->opt.kernel_class == CLASS_S) ||
+                       (c->opt.kernel_class == CLASS_AUTO && thread_fits(c->m, c->n));
+  SimplexArgs a;
+  if (s_class) {
+    if (!thread_fits(c->m, c->n)) return LPB_ETOOBIG;
+    fill_args(c, a, lp0, cnt, A, b, cv, nox, c->m, ticket);
+    LPB_CUDA(c, launch_simplex_thread(a, c->opt.grid_ctas, s));
+    *launches += 1;
+    c->last_class = CLASS_S;
+    return LPB_OK;
+  }
+  if (kmax < 0) {  // device prepass: kmax over the chunk (one tiny kernel + 4-byte D2H)
+    LPB_CUDA(c, launch_count_art(b, cnt, c->m, c->d_kmax, s));
+    LPB_CUDA(c, cudaMemcpyAsync(c->h_kmax, c->d_kmax, sizeof(int), cudaMemcpyDeviceToHost, s));
+    LPB_CUDA(c, cudaStreamSynchronize(s));
+    kmax = *c->h_kmax;
+    *launches += 1;
+  }
+  int cl = 1;
+  const int klass = choose_class(c, kmax, &cl);
+  if (klass < 0) return LPB_ETOOBIG;
+  fill_args(c, a, lp0, cnt, A, b, cv, nox, kmax, ticket);
+  LPB_CUDA(c, cudaMemsetAsync(ticket, 0, sizeof(int), s));
+  int ctas = 0;
+  if (klass == CLASS_R) {
+    LPB_CUDA(c, launch_simplex_reg(a, c->opt.grid_ctas, s, &ctas));
+  } else {
+    LPB_CUDA(c, launch_simplex_block(cl, a, c->opt.grid_ctas, s, &ctas));
+  }
+  *launches += 1;
+  c->last_class = klass;
+  return LPB_OK;
+}
+
+static int run_hyperbox(lpb_ctx* c, cudaStream_t s, int64_t lp0, int64_t cnt, const double* l,
+                        const double* box, bool shared, bool nox, int* launches) {
+  HyperboxArgs h;
+  h.batch = cnt;
+  h.n = c->n;
+  h.l = l;
+  h.box = box;
+  h.shared_box = shared ? 1 : 0;
+  h.status = c->d_status + lp0;
+  h.obj = c->d_obj + lp0;
+  h.x = nox ? nullptr : c->d_x + lp0 * c->n;
+  LPB_CUDA(c, launch_hyperbox(h, s));
+  *launches += 1;
+  c->last_class = CLASS_H;
+  return LPB_OK;
+}
+
+static int ensure_host_path(lpb_ctx* c, int nch) {
+  const int64_t B = c->batch;
+  if (c->kind == LPB_GENERAL && !c->d_A) {
+    LPB_CUDA(c, cudaMalloc(&c->d_A, sizeof(double) * B * (int64_t)c->m * c->n));
+    LPB_CUDA(c, cudaMalloc(&c->d_b, sizeof(double) * B * (int64_t)c->m));
+    LPB_CUDA(c, cudaMalloc(&c->d_c, sizeof(double) * B * (int64_t)c->n));
+  }
+  if (c->kind == LPB_HYPERBOX && !c->d_c) {
+    LPB_CUDA(c, cudaMalloc(&c->d_c, sizeof(double) * B * (int64_t)c->n));
+    LPB_CUDA(c, cudaMalloc(&c->d_b, sizeof(double) * B * (int64_t)c->m));
+  }
+  while ((int)c->chunk_streams.size() < nch) {
+    cudaStream_t s;
+    cudaEvent_t ev;
+    LPB_CUDA(c, cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    LPB_CUDA(c, cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    c->chunk_streams.push_back(s);
+    c->chunk_done.push_back(ev);
+  }
+  return LPB_OK;
+}
+
+static int solve_impl(lpb_ctx* c, const double* A, const double* b, const double* cv,
+                      uint32_t flags, int32_t* o_status, double* o_obj, double* o_x,
+                      int32_t* o_iters) {
+  if (!c) return LPB_EINVAL;
+  const bool general = c->kind == LPB_GENERAL;
+  if ((general && (!A || !b || !cv)) || (!general && (A || !b || !cv))) return LPB_EINVAL;
+  const bool nox = (flags & LPB_NO_X) != 0;
+  const bool shared = (flags & LPB_SHARED_BOX) != 0;
+  if (o_x && nox) return LPB_EINVAL;
+  LPB_CUDA(c, cudaSetDevice(c->device));
+  c->solved = false;
+  c->last_launches = 0;
+  c->last_nox = nox;
+  const int64_t B = c->batch;
+  const int m = c->m, n = c->n;
+
+  if (flags & LPB_DEVICE_PTRS) {
+    c->host_path = false;
+    LPB_CUDA(c, cudaEventRecord(c->ev0, c->stream));
+    int rc = general ? run_general(c, c->stream, 0, B, A, b, cv, nox, -1, c->d_ticket,
+                                   &c->last_launches)
+                     : run_hyperbox(c, c->stream, 0, B, cv, b, shared, nox, &c->last_launches);
+    if (rc != LPB_OK) return rc;
+    LPB_CUDA(c, cudaEventRecord(c->ev1, c->stream));
+    if (o_status) LPB_CUDA(c, cudaMemcpyAsync(o_status, c->d_status, 4 * B, cudaMemcpyDefault, c->stream));
+    if (o_obj) LPB_CUDA(c, cudaMemcpyAsync(o_obj, c->d_obj, 8 * B, cudaMemcpyDefault, c->stream));
+    if (o_x) LPB_CUDA(c, cudaMemcpyAsync(o_x, c->d_x, 8 * B * (int64_t)n, cudaMemcpyDefault, c->stream));
+    if (o_iters) LPB_CUDA(c, cudaMemcpyAsync(o_iters, c->d_iters, 8 * B, cudaMemcpyDefault, c->stream));
+    c->solved = true;
+    if (!(flags & LPB_ASYNC)) LPB_CUDA(c, cudaStreamSynchronize(c->stream));
+    return LPB_OK;
+  }
+
+  // ---- host pointers: chunked H2D -> kernel -> D2H pipeline on n_chunks streams ----
+  c->host_path = true;
+  int nch = c->opt.n_chunks > 0 ? c->opt.n_chunks : (B > 100 ? 10 : 1);
+  if (nch > 64) nch = 64;
+  if (nch > B) nch = (int)B;
+  int rc = ensure_host_path(c, nch);
+  if (rc != LPB_OK) return rc;
+  int kmax = -1;
+  if (general) {  // kmax from the host copy of b (no device round trip inside the pipeline)
+    int best = 0;
+    for (int64_t k = 0; k < B; ++k) {
+      int cnt = 0;
+      const double* bk = b + k * m;
+      for (int i = 0; i < m; ++i) cnt += (bk[i] < 0.0);
+      best = std::max(best, cnt);
+    }
+    kmax = best;
+  }
+  LPB_CUDA(c, cudaEventRecord(c->ev0, c->stream));
+  for (int q = 0; q < nch; ++q) {
+    const int64_t lp0 = B * q / nch, lp1 = B * (q + 1) / nch, cnt = lp1 - lp0;
+    cudaStream_t s = c->chunk_streams[q];
+    LPB_CUDA(c, cudaStreamWaitEvent(s, c->ev0, 0));
+    if (general) {
+      LPB_CUDA(c, cudaMemcpyAsync(c->d_A + lp0 * m * (int64_t)n, A + lp0 * m * (int64_t)n,
+                                  8 * cnt * m * (int64_t)n, cudaMemcpyHostToDevice, s));
+      LPB_CUDA(c, cudaMemcpyAsync(c->d_b + lp0 * m, b + lp0 * m, 8 * cnt * m,
+                                  cudaMemcpyHostToDevice, s));
+      LPB_CUDA(c, cudaMemcpyAsync(c->d_c + lp0 * n, cv + lp0 * n, 8 * cnt * n,
+                                  cudaMemcpyHostToDevice, s));
+      rc = run_general(c, s, lp0, cnt, c->d_A + lp0 * m * (int64_t)n, c->d_b + lp0 * m,
+                       c->d_c + lp0 * n, nox, kmax, c->d_ticket + q, &c->last_launches);
+    } else {
+      const int64_t bstride = shared ? 0 : 2 * (int64_t)n;
+      if (q == 0 || !shared)
+        LPB_CUDA(c, cudaMemcpyAsync(c->d_b + lp0 * bstride, b + lp0 * bstride,
+                                    8 * (shared ? 2 * (int64_t)n : cnt * bstride),
+                                    cudaMemcpyHostToDevice, s));
+      if (shared && q == 0) LPB_CUDA(c, cudaEventRecord(c->chunk_done[0], s));
+      if (shared && q > 0) LPB_CUDA(c, cudaStreamWaitEvent(s, c->chunk_done[0], 0));
+      LPB_CUDA(c, cudaMemcpyAsync(c->d_c + lp0 * n, cv + lp0 * n, 8 * cnt * n,
+                                  cudaMemcpyHostToDevice, s));
+      rc = run_hyperbox(c, s, lp0, cnt, c->d_c + lp0 * n, c->d_b + lp0 * bstride, shared, nox,
+                        &c->last_launches);
+    }
+    if (rc != LPB_OK) return rc;
+    if (o_status) LPB_CUDA(c, cudaMemcpyAsync(o_status + lp0, c->d_status + lp0, 4 * cnt, cudaMemcpyDefault, s));
+    if (o_obj) LPB_CUDA(c, cudaMemcpyAsync(o_obj + lp0, c->d_obj + lp0, 8 * cnt, cudaMemcpyDefault, s));
+    if (o_x) LPB_CUDA(c, cudaMemcpyAsync(o_x + lp0 * n, c->d_x + lp0 * n, 8 * cnt * (int64_t)n, cudaMemcpyDefault, s));
+    if (o_iters) LPB_CUDA(c, cudaMemcpyAsync(o_iters + 2 * lp0, c->d_iters + 2 * lp0, 8 * cnt, cudaMemcpyDefault, s));
+    cudaEvent_t done;
+    LPB_CUDA(c, cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+    LPB_CUDA(c, cudaEventRecord(done, s));
+    LPB_CUDA(c, cudaStreamWaitEvent(c->stream, done, 0));
+    cudaEventDestroy(done);  // destruction is deferred until the event completes
+  }
+  LPB_CUDA(c, cudaEventRecord(c->ev1, c->stream));
+  c->solved = true;
+  if (!(flags & LPB_ASYNC)) LPB_CUDA(c, cudaStreamSynchronize(c->stream));
+  return LPB_OK;
+}
+
+extern "C" int lpb_solve_batch(lpb_ctx* c, const double* A, const double* b, const double* cv,
+                               uint32_t flags) {
+  return solve_impl(c, A, b, cv, flags, nullptr, nullptr, nullptr, nullptr);
+}
+
+extern "C" int lpb_solve_batch_into(lpb_ctx* c, const double* A, const double* b,
+                                    const double* cv, uint32_t flags, int32_t* status,
+                                    double* obj, double* x, int32_t* iters) {
+  return solve_impl(c, A, b, cv, flags, status, obj, x, iters);
+}
+
+extern "C" int lpb_results(lpb_ctx* c, int32_t* status, double* obj, double* x,
+                           int32_t* iters) {
+  if (!c) return LPB_EINVAL;
+  if (!c->solved) return LPB_ESTATE;
+  if (x && c->last_nox) return LPB_EINVAL;
+  LPB_CUDA(c, cudaSetDevice(c->device));
+  const int64_t B = c->batch;
+  if (status) LPB_CUDA(c, cudaMemcpyAsync(status, c->d_status, 4 * B, cudaMemcpyDefault, c->stream));
+  if (obj) LPB_CUDA(c, cudaMemcpyAsync(obj, c->d_obj, 8 * B, cudaMemcpyDefault, c->stream));
+  if (x) LPB_CUDA(c, cudaMemcpyAsync(x, c->d_x, 8 * B * (int64_t)c->n, cudaMemcpyDefault, c->stream));
+  if (iters) LPB_CUDA(c, cudaMemcpyAsync(iters, c->d_iters, 8 * B, cudaMemcpyDefault, c->stream));
+  LPB_CUDA(c, cudaStreamSynchronize(c->stream));
+  return LPB_OK;
+}
+
+extern "C" int lpb_result_device_ptrs(lpb_ctx* c, int32_t** status, double** obj, double** x,
+                                      int32_t** iters) {
+  if (!c) return LPB_EINVAL;
+  if (status) *status = c->d_status;
+  if (obj) *obj = c->d_obj;
+  if (x) *x = c->d_x;
+  if (iters) *iters = c->d_iters;
+  return LPB_OK;
+}
+
+extern "C" int lpb_sync(lpb_ctx* c) {
+  if (!c) return LPB_EINVAL;
+  LPB_CUDA(c, cudaSetDevice(c->device));
+  LPB_CUDA(c, cudaStreamSynchronize(c->stream));
+  return LPB_OK;
+}
+
+extern "C" int lpb_last_timing(lpb_ctx* c, double* solve_ms, double* e2e_ms) {
+  if (!c) return LPB_EINVAL;
+  if (!c->solved) return LPB_ESTATE;
+  LPB_CUDA(c, cudaSetDevice(c->device));
+  LPB_CUDA(c, cudaEventSynchronize(c->ev1));
+  float ms = 0.f;
+  LPB_CUDA(c, cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+  if (solve_ms) *solve_ms = c->host_path ? std::nan("") : (double)ms;
+  if (e2e_ms) *e2e_ms = (double)ms;
+  return LPB_OK;
+}
+
+extern "C" int lpb_last_launch_info(lpb_ctx* c, int32_t* launches, int32_t* kernel_class) {
+  if (!c) return LPB_EINVAL;
+  if (launches) *launches = c->last_launches;
+  if (kernel_class) *kernel_class = c->last_class;
+  return LPB_OK;
+}

@@ -1,0 +1,70 @@
+// lpb_internal.cuh — kernel argument blocks and launcher declarations shared by the
+// translation units of liblpb.so (never installed; the public ABI is include/lpb.h).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace lpb {
+
+// Per-LP status codes (must equal LPB_OPTIMAL.. in include/lpb.h).
+enum : int32_t { ST_OPTIMAL = 0, ST_UNBOUNDED = 1, ST_INFEASIBLE = 2, ST_ITER_LIMIT = 3,
+                 ST_NUMERICAL = 4 };
+
+// Size classes (lpb_options.kernel_class / lpb_last_launch_info).
+enum : int32_t { CLASS_AUTO = 0, CLASS_S = 1, CLASS_M = 2, CLASS_L = 3, CLASS_R = 4,
+                 CLASS_H = 5 };
+
+struct SimplexArgs {
+  int64_t batch;
+  int m, n;
+  const double* A;  // batch x m x n
+  const double* b;  // batch x m
+  const double* c;  // batch x n
+  int32_t* status;
+  double* obj;
+  double* x;        // may be null (LPB_NO_X)
+  int32_t* iters;   // batch x 2
+  double eps_enter, eps_piv, eps_phase1;
+  int max_iter;     // > 0
+  int bland_K;      // > 0: Bland mode after K consecutive degenerate pivots; <= 0: never
+  int kmax;         // layout capacity for artificial (b_i < 0) rows
+  int* ticket;      // persistent-scheduler counter, zeroed before each launch
+};
+
+struct HyperboxArgs {
+  int64_t batch;
+  int n;
+  const double* l;    // batch x n directions (the objective c)
+  const double* box;  // [hi(n); -lo(n)] shared, or batch x 2n
+  int shared_box;
+  int32_t* status;
+  double* obj;
+  double* x;          // may be null
+};
+
+// ---- M / L classes: one LP per CTA (cl = 1) or per cl-CTA cluster, tableau in SMEM ----
+size_t block_smem_bytes(int cl, int m, int n, int kmax);
+bool block_fits(int cl, int m, int n, int kmax);
+cudaError_t launch_simplex_block(int cl, const SimplexArgs& a, int grid_override,
+                                 cudaStream_t s, int* ctas_out);
+
+// ---- S class: one LP per thread, tableau in the thread's private SMEM slice ----
+bool thread_fits(int m, int n);
+cudaError_t launch_simplex_thread(const SimplexArgs& a, int grid_override, cudaStream_t s);
+
+// ---- R class: one LP per CTA, tableau resident in registers ----
+bool reg_fits(int m, int n, int kmax);
+cudaError_t launch_simplex_reg(const SimplexArgs& a, int grid_override, cudaStream_t s,
+                               int* ctas_out);
+
+// ---- prepass: kmax = max over LPs of #{i : b_i < 0} ----
+cudaError_t launch_count_art(const double* b, int64_t batch, int m, int* kmax_dev,
+                             cudaStream_t s);
+
+// ---- H class: hyperbox closed form (Eq. 6) ----
+cudaError_t launch_hyperbox(const HyperboxArgs& a, cudaStream_t s);
+
+int device_sm_count();
+
+}  // namespace lpb

@@ -1,0 +1,513 @@
+// simplex_block.cu — M and L size classes: one LP per thread block (cl = 1) or per
+// thread-block cluster of cl CTAs (cl = 2, 4) with the CONDENSED fp64 simplex tableau
+// resident in shared memory (distributed shared memory across the cluster).
+//
+// The method is the paper's dense-tableau simplex (§3.1 Steps 1-3, lines 91-103;
+// §4.2 "we assign a CUDA block of threads to solve an LP", line 114), re-laid out for
+// sm_100a:
+//   * condensed (dictionary) tableau: only the nonbasic columns + RHS are stored, (R) x (W)
+//     with R = m+1 (+1 phase-I row when some b_i < 0) and W = n + k + 1 (k = #{b_i < 0});
+//     the column of the leaving variable is swapped into the entering position.  Every
+//     stored value is bit-identical to the corresponding full-tableau entry of the oracle
+//     (readings R12/R13).
+//   * the tableau never touches HBM: A, b, c are read once, status/obj/x/iters written once.
+//   * Step 1 / Step 2 reductions ("parallel reduction ... two auxiliary
+//     arrays Data and Indices") are (value, key) warp-shuffle butterflies + one SMEM slot
+//     per warp, + one DSMEM slot per CTA for clusters.
+//   * the L class splits the nonbasic positions across the cluster's CTAs (the paper's
+//     "mapping an LP problem with more than one thread blocks"); the RHS
+//     column is replicated in every CTA, so the pivot row stays CTA-local and only the
+//     pivot column (R doubles) and two reduction partials cross DSMEM per pivot.
+//   * persistent CTAs/clusters pull LP indices from an atomic ticket (pivot counts per LP
+//     vary by 10x).
+// Arithmetic contract (parity with oracle/lpb_oracle.c): IEEE __ddiv_rn for ratios and the
+// pivot row, explicit __fma_rn(-f, r, t) for the update, __dadd_rn in ascending row order
+// for the phase-I row; compiled with -fmad=false so nothing else is contracted.
+#include <cooperative_groups.h>
+
+#include <cfloat>
+#include <climits>
+
+#include "lpb_internal.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace lpb {
+namespace {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int DEAD = INT_MAX;  // a dead (left artificial) nonbasic position
+constexpr int NT = 256;        // threads per CTA
+constexpr int NW = NT / 32;
+
+struct Cand {
+  double v;
+  int key;  // tie-break key: variable index / row / basis key
+  int pos;  // < 0: no candidate
+};
+
+enum { MAX_V = 0, MIN_KEY = 1, MIN_V = 2 };
+
+template <int MODE>
+__device__ __forceinline__ bool better(const Cand& a, const Cand& b) {
+  if (a.pos < 0) return false;
+  if (b.pos < 0) return true;
+  if (MODE == MAX_V) return a.v > b.v || (a.v == b.v && a.key < b.key);
+  if (MODE == MIN_KEY) return a.key < b.key;
+  return a.v < b.v || (a.v == b.v && a.key < b.key);
+}
+
+template <int MODE>
+__device__ __forceinline__ Cand warp_reduce(Cand c) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    Cand o;
+    o.v = __shfl_xor_sync(FULL, c.v, off);
+    o.key = __shfl_xor_sync(FULL, c.key, off);
+    o.pos = __shfl_xor_sync(FULL, c.pos, off);
+    if (better<MODE>(o, c)) c = o;
+  }
+  return c;
+}
+
+struct Ctl {
+  double theta;
+  double binf;
+  int lp;
+  int l;
+  int k;
+  int pad;
+};
+
+struct Smem {
+  double* T;      // rows x S
+  double* colE;   // pivot column (all rows), filled by the owner CTA
+  double* prow;   // new pivot row (local columns)
+  int* nbvar;     // local position -> variable index (or DEAD)
+  int* bkey;      // row -> key of its basic variable (>= 0 real, < 0 artificial)
+  int* negrows;   // ascending list of rows with b_i < 0
+  int* wcount;    // NW ints
+  Cand* wslots;   // 2 x NW
+  Cand* cslots;   // 2 x CL
+  Ctl* ctl;
+};
+
+template <int CL>
+struct Cluster {
+  int rank;
+  __device__ Cluster() {
+    if constexpr (CL > 1) rank = (int)cg::this_cluster().block_rank();
+    else rank = 0;
+  }
+  __device__ __forceinline__ void sync() const {
+    if constexpr (CL > 1) cg::this_cluster().sync();
+    else __syncthreads();
+  }
+  template <class T>
+  __device__ __forceinline__ T* remote(T* p, int q) const {
+    if constexpr (CL > 1) return cg::this_cluster().map_shared_rank(p, q);
+    else return p;
+  }
+};
+
+// Block-wide (value,key) reduction; result identical in every thread.
+template <int MODE>
+__device__ __forceinline__ Cand block_reduce(Cand c, Cand* slots) {
+  c = warp_reduce<MODE>(c);
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) slots[w] = c;
+  __syncthreads();
+  Cand r{0.0, 0, -1};
+  if (lane < NW) r = slots[lane];
+  return warp_reduce<MODE>(r);
+}
+
+// Cluster-wide reduction: block reduce, publish the CTA partial into every CTA's slot
+// `rank`, cluster barrier, reduce the CL partials.
+template <int MODE, int CL>
+__device__ __forceinline__ Cand cluster_reduce(Cand c, const Smem& s, int& par,
+                                               const Cluster<CL>& cl) {
+  Cand* ws = s.wslots + par * NW;
+  Cand* cs = s.cslots + par * CL;
+  par ^= 1;
+  Cand r = block_reduce<MODE>(c, ws);
+  if constexpr (CL == 1) {
+    return r;
+  } else {
+    if (threadIdx.x == 0)
+      for (int q = 0; q < CL; ++q) *cl.remote(cs + cl.rank, q) = r;
+    cl.sync();
+    Cand best = cs[0];
+#pragma unroll
+    for (int q = 1; q < CL; ++q) {
+      const Cand o = cs[q];
+      if (better<MODE>(o, best)) best = o;
+    }
+    return best;
+  }
+}
+
+// Step 3 (Listing 1) on the condensed tableau, CTA-local part.
+// colE[] (pivot column, all rows) is already in this CTA's SMEM.  Row l becomes the pivot
+// row divided by PE; the entering position e (owned by CTA `owner` at local column jloc)
+// receives the leaving variable's column: rl = 1/PE in row l, fma(-f_i, rl, 0) elsewhere.
+__device__ __forceinline__ void pivot_local(const Smem& s, int S, int Wa, int nrow, int l,
+                                            bool own, int jloc, int ent_var) {
+  const int tid = threadIdx.x;
+  const double pe = s.colE[l];
+  for (int j = tid; j < Wa; j += NT) {
+    const double num = (own && j == jloc) ? 1.0 : s.T[l * S + j];
+    s.prow[j] = __ddiv_rn(num, pe);
+  }
+  if (tid == 0) {
+    const int leaving = s.bkey[l];
+    s.bkey[l] = ent_var;
+    if (own) s.nbvar[jloc] = leaving < 0 ? DEAD : leaving;
+  }
+  __syncthreads();
+  // flat (i, j) walk over nrow x Wa with an incremental divmod
+  int i = tid / Wa, j = tid - (tid / Wa) * Wa;
+  const int dq = NT / Wa, dr = NT - (NT / Wa) * Wa;
+  const int jswap = own ? jloc : -1;
+  for (; i < nrow;) {
+    double* t = s.T + i * S + j;
+    const double p = s.prow[j];
+    if (i == l) {
+      *t = p;
+    } else {
+      const double f = -s.colE[i];
+      *t = __fma_rn(f, p, (j == jswap) ? 0.0 : *t);
+    }
+    j += dr;
+    i += dq;
+    if (j >= Wa) { j -= Wa; ++i; }
+  }
+  __syncthreads();
+}
+
+template <int CL>
+__global__ void __launch_bounds__(NT) simplex_block_kernel(SimplexArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const Cluster<CL> cl;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int m = a.m, n = a.n;
+  const int Q = (n + a.kmax + CL - 1) / CL;  // nonbasic positions per CTA (capacity)
+  const int S = (Q + 1) | 1;                 // odd row stride: conflict-free column reads
+  const int RC = m + 2;
+
+  Smem s;
+  s.T = reinterpret_cast<double*>(smem_raw);
+  s.colE = s.T + (size_t)RC * S;
+  s.prow = s.colE + RC;
+  s.nbvar = reinterpret_cast<int*>(s.prow + (Q + 1));
+  s.bkey = s.nbvar + (Q + 1);
+  s.negrows = s.bkey + m;
+  s.wcount = s.negrows + m;
+  uintptr_t p = reinterpret_cast<uintptr_t>(s.wcount + NW);
+  p = (p + 15) & ~uintptr_t(15);
+  s.wslots = reinterpret_cast<Cand*>(p);
+  s.cslots = s.wslots + 2 * NW;
+  s.ctl = reinterpret_cast<Ctl*>(s.cslots + 2 * CL);
+
+  int par = 0;
+  for (;;) {
+    if (cl.rank == 0 && tid == 0) {
+      const int t = atomicAdd(a.ticket, 1);
+      for (int q = 0; q < CL; ++q) cl.remote(s.ctl, q)->lp = t;
+    }
+    cl.sync();
+    const int64_t lp = s.ctl->lp;
+    if (lp >= a.batch) break;
+
+    const double* __restrict__ Ak = a.A + lp * (int64_t)m * n;
+    const double* __restrict__ bk = a.b + lp * (int64_t)m;
+    const double* __restrict__ ck = a.c + lp * (int64_t)n;
+
+    // ---- build (reading R7): negated rows, basis keys, |b|_inf ----
+    int k = 0;
+    double binf = 0.0;
+    for (int base = 0; base < m; base += NT) {
+      const int i = base + tid;
+      const double bi = (i < m) ? __ldg(bk + i) : 0.0;
+      const bool neg = (i < m) && (bi < 0.0);
+      binf = fmax(binf, fabs(bi));
+      const unsigned bal = __ballot_sync(FULL, neg);
+      if (lane == 0) s.wcount[w] = __popc(bal);
+      __syncthreads();
+      int off = k, tot = 0;
+      for (int q = 0; q < NW; ++q) {
+        const int cq = s.wcount[q];
+        if (q < w) off += cq;
+        tot += cq;
+      }
+      if (neg) s.negrows[off + __popc(bal & ((1u << lane) - 1u))] = i;
+      if (i < m) s.bkey[i] = neg ? (i - m) : (n + i);
+      k += tot;
+      __syncthreads();
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) binf = fmax(binf, __shfl_xor_sync(FULL, binf, off));
+    if (lane == 0) s.wslots[w].v = binf;
+    __syncthreads();
+    binf = s.wslots[0].v;
+    for (int q = 1; q < NW; ++q) binf = fmax(binf, s.wslots[q].v);
+    __syncthreads();
+
+    int st = -1, it1 = 0, it2 = 0;
+    const int cnt = max(0, min(Q, n + k - cl.rank * Q));  // live local positions
+    const int Wa = cnt + 1;                               // + RHS at local column cnt
+    const int g0 = cl.rank * Q;
+    if (k > a.kmax) st = ST_NUMERICAL;  // cannot happen: kmax comes from the prepass
+
+    if (st < 0) {
+      for (int i = w; i < m; i += NW) {
+        const bool neg = s.bkey[i] < 0;
+        for (int j = lane; j < Wa; j += 32) {
+          const int gp = g0 + j;
+          double v;
+          if (j == cnt) {
+            v = __ldg(bk + i);
+            v = neg ? -v : v;
+          } else if (gp < n) {
+            v = __ldg(Ak + (int64_t)i * n + gp);
+            v = neg ? -v : v;
+          } else {
+            v = (i == s.negrows[gp - n]) ? -1.0 : (neg ? -0.0 : 0.0);
+          }
+          s.T[i * S + j] = v;
+        }
+      }
+      for (int j = tid; j < Wa; j += NT) {
+        const int gp = g0 + j;
+        s.T[m * S + j] = (j < cnt && gp < n) ? __ldg(ck + gp) : 0.0;
+        if (j < cnt) s.nbvar[j] = gp < n ? gp : n + s.negrows[gp - n];
+      }
+      __syncthreads();
+      if (k > 0) {  // phase-I row: ascending-row sums of the negated rows (R7)
+        for (int j = tid; j < Wa; j += NT) {
+          double acc = 0.0;
+          for (int t = 0; t < k; ++t) acc = __dadd_rn(acc, s.T[s.negrows[t] * S + j]);
+          s.T[(m + 1) * S + j] = acc;
+        }
+      }
+      __syncthreads();
+    }
+
+    // ---- Steps 1-3 loop, two phases ----
+    int phase = (k > 0) ? 1 : 2, stall = 0;
+    while (st < 0) {
+      const int objrow = (phase == 1) ? m + 1 : m;
+      const int nrow = (phase == 1) ? m + 2 : m + 1;
+      const bool bland = a.bland_K > 0 && stall >= a.bland_K;
+      // Step 1: entering variable (LPC/Dantzig, lowest variable index on ties; Bland)
+      Cand ce{0.0, 0, -1};
+      for (int j = tid; j < cnt; j += NT) {
+        const int var = s.nbvar[j];
+        const double d = s.T[objrow * S + j];
+        if (var != DEAD && d > a.eps_enter) {
+          const Cand cd{d, var, g0 + j};
+          if (bland ? better<MIN_KEY>(cd, ce) : better<MAX_V>(cd, ce)) ce = cd;
+        }
+      }
+      ce = bland ? cluster_reduce<MIN_KEY, CL>(ce, s, par, cl)
+                 : cluster_reduce<MAX_V, CL>(ce, s, par, cl);
+      if (ce.pos < 0) {
+        if (phase == 2) { st = ST_OPTIMAL; break; }
+        // phase switch (R8, R9): infeasibility test, drive artificials out, drop phase-I row
+        const double wstar = s.T[(m + 1) * S + cnt];
+        if (wstar > a.eps_phase1 * fmax(1.0, binf)) { st = ST_INFEASIBLE; break; }
+        for (int l = 0; l < m; ++l) {
+          if (s.bkey[l] >= 0) continue;
+          Cand cd{0.0, 0, -1};
+          for (int j = tid; j < cnt; j += NT) {
+            const int var = s.nbvar[j];
+            const double v = fabs(s.T[l * S + j]);
+            if (var != DEAD && v > a.eps_piv) {
+              const Cand cc{v, var, g0 + j};
+              if (better<MAX_V>(cc, cd)) cd = cc;
+            }
+          }
+          cd = cluster_reduce<MAX_V, CL>(cd, s, par, cl);
+          if (cd.pos < 0) continue;  // redundant row: the artificial stays basic at 0
+          const int owner = cd.pos / Q, jloc = cd.pos - owner * Q;
+          if (cl.rank == owner) {
+            for (int i = tid; i < m + 2; i += NT) {
+              const double v = s.T[i * S + jloc];
+              for (int q = 0; q < CL; ++q) cl.remote(s.colE, q)[i] = v;
+            }
+          }
+          cl.sync();
+          pivot_local(s, S, Wa, m + 2, l, cl.rank == owner, jloc, cd.key);
+          ++it1;
+        }
+        phase = 2;
+        stall = 0;
+        continue;
+      }
+      if (it1 + it2 >= a.max_iter) { st = ST_ITER_LIMIT; break; }
+      // Step 2: ratio test on the owner CTA (RHS is replicated), sentinel = no candidate
+      const int owner = ce.pos / Q, jloc = ce.pos - owner * Q;
+      if (cl.rank == owner) {
+        Cand cr{0.0, 0, -1};
+        for (int i = tid; i < m; i += NT) {
+          const double ai = s.T[i * S + jloc];
+          if (ai > a.eps_piv) {
+            const Cand cc{__ddiv_rn(s.T[i * S + cnt], ai), bland ? s.bkey[i] : i, i};
+            if (better<MIN_V>(cc, cr)) cr = cc;
+          }
+        }
+        Cand* ws = s.wslots + par * NW;
+        par ^= 1;
+        cr = block_reduce<MIN_V>(cr, ws);
+        for (int i = tid; i < nrow; i += NT) {
+          const double v = s.T[i * S + jloc];
+          for (int q = 0; q < CL; ++q) cl.remote(s.colE, q)[i] = v;
+        }
+        if (tid == 0)
+          for (int q = 0; q < CL; ++q) {
+            Ctl* c = cl.remote(s.ctl, q);
+            c->l = cr.pos;
+            c->theta = cr.v;
+          }
+      } else {
+        par ^= 1;  // keep the slot parity identical in every CTA
+      }
+      cl.sync();
+      const int l = s.ctl->l;
+      const double theta = s.ctl->theta;
+      if (l < 0) { st = (phase == 2) ? ST_UNBOUNDED : ST_NUMERICAL; break; }
+      // Step 3: pivot
+      pivot_local(s, S, Wa, nrow, l, cl.rank == owner, jloc, ce.key);
+      if (phase == 1) ++it1; else ++it2;
+      stall = (theta > 0.0) ? 0 : stall + 1;
+    }
+
+    // ---- extract (R10) ----
+    if (cl.rank == 0) {
+      if (tid == 0) {
+        a.status[lp] = st;
+        a.iters[2 * lp] = it1;
+        a.iters[2 * lp + 1] = it2;
+        a.obj[lp] = (st == ST_OPTIMAL) ? -s.T[m * S + cnt]
+                  : (st == ST_UNBOUNDED) ? __longlong_as_double(0x7ff0000000000000ll)
+                  : (st == ST_INFEASIBLE) ? __longlong_as_double(0xfff0000000000000ll)
+                                          : __longlong_as_double(0x7ff8000000000000ll);
+      }
+      if (a.x) {
+        double* xk = a.x + lp * (int64_t)n;
+        const double fill = (st == ST_OPTIMAL) ? 0.0 : __longlong_as_double(0x7ff8000000000000ll);
+        for (int j = tid; j < n; j += NT) xk[j] = fill;
+        __syncthreads();
+        if (st == ST_OPTIMAL)
+          for (int i = tid; i < m; i += NT) {
+            const int key = s.bkey[i];
+            if (key >= 0 && key < n) xk[key] = s.T[i * S + cnt];
+          }
+      }
+    }
+    cl.sync();
+  }
+}
+
+}  // namespace
+
+size_t block_smem_bytes(int cl, int m, int n, int kmax) {
+  const int Q = (n + kmax + cl - 1) / cl;
+  const int S = (Q + 1) | 1;
+  size_t bytes = sizeof(double) * ((size_t)(m + 2) * S + (m + 2) + (Q + 1));
+  bytes += sizeof(int) * ((size_t)(Q + 1) + 2 * (size_t)m + NW);
+  bytes = (bytes + 15) & ~size_t(15);
+  bytes += sizeof(Cand) * (2 * NW + 2 * cl) + sizeof(Ctl);
+  return bytes;
+}
+
+bool block_fits(int cl, int m, int n, int kmax) {
+  return block_smem_bytes(cl, m, n, kmax) <= 227 * 1024;
+}
+
+template <int CL>
+static cudaError_t launch_cl(const SimplexArgs& a, int grid_override, cudaStream_t s,
+                             int* ctas_out) {
+  const size_t smem = block_smem_bytes(CL, a.m, a.n, a.kmax);
+  cudaError_t e = cudaFuncSetAttribute(simplex_block_kernel<CL>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const int sms = device_sm_count();
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  cfg.blockDim = dim3(NT);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  int resident = 0;
+  if constexpr (CL == 1) {
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, simplex_block_kernel<1>, NT,
+                                                      smem);
+    if (e != cudaSuccess) return e;
+    resident = per_sm * sms;
+  } else {
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CL;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cfg.gridDim = dim3(CL * sms);
+    int clusters = 0;
+    e = cudaOccupancyMaxActiveClusters(&clusters, simplex_block_kernel<CL>, &cfg);
+    if (e != cudaSuccess) return e;
+    resident = clusters * CL;
+  }
+  if (resident <= 0) return cudaErrorInvalidConfiguration;
+  int64_t want = a.batch * CL;
+  int grid = (int)(want < resident ? want : resident);
+  if (grid_override > 0) grid = grid_override * CL;
+  grid = (grid / CL) * CL;
+  if (grid < CL) grid = CL;
+  cfg.gridDim = dim3(grid);
+  if (ctas_out) *ctas_out = grid;
+  return cudaLaunchKernelEx(&cfg, simplex_block_kernel<CL>, a);
+}
+
+cudaError_t launch_simplex_block(int cl, const SimplexArgs& a, int grid_override,
+                                 cudaStream_t s, int* ctas_out) {
+  switch (cl) {
+    case 1: return launch_cl<1>(a, grid_override, s, ctas_out);
+    case 2: return launch_cl<2>(a, grid_override, s, ctas_out);
+    case 4: return launch_cl<4>(a, grid_override, s, ctas_out);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+// Prepass: kmax = max_k #{i : b_ki < 0}.  One warp per LP, ballot counts.
+__global__ void count_art_kernel(const double* __restrict__ b, int64_t batch, int m,
+                                 int* __restrict__ kmax) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  int best = 0;
+  for (int64_t lp = warp; lp < batch; lp += nwarps) {
+    const double* bk = b + lp * m;
+    int cnt = 0;
+    for (int i = lane; i < m; i += 32) cnt += (__ldg(bk + i) < 0.0);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) cnt += __shfl_xor_sync(FULL, cnt, off);
+    best = max(best, cnt);
+  }
+  if (lane == 0 && best > 0) atomicMax(kmax, best);
+}
+
+cudaError_t launch_count_art(const double* b, int64_t batch, int m, int* kmax_dev,
+                             cudaStream_t s) {
+  cudaError_t e = cudaMemsetAsync(kmax_dev, 0, sizeof(int), s);
+  if (e != cudaSuccess) return e;
+  int64_t warps = batch;
+  const int64_t cap = (int64_t)device_sm_count() * 64;
+  if (warps > cap) warps = cap;
+  const int threads = 256;
+  const int blocks = (int)((warps * 32 + threads - 1) / threads);
+  count_art_kernel<<<blocks, threads, 0, s>>>(b, batch, m, kmax_dev);
+  return cudaGetLastError();
+}
+
+}  // namespace lpb

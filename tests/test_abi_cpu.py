@@ -1,0 +1,65 @@
+"""C-ABI library checks that need no GPU: it loads, exports every symbol include/lpb.h
+declares, and its argument validation / pure-host entry points behave as documented."""
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HDR = os.path.join(ROOT, "include", "lpb.h")
+LIB = os.path.join(ROOT, "paper_1609_08114_b200", "liblpb.so")
+
+
+@pytest.fixture(scope="module")
+def lib():
+    if not os.path.exists(LIB):
+        from paper_1609_08114_b200 import build as b
+        b.build()
+    return ctypes.CDLL(LIB)
+
+
+def _declared():
+    src = open(HDR).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(lpb_[a-z_]+)\s*\(", src)))
+
+
+def test_exports_every_declared_symbol(lib):
+    names = _declared()
+    assert len(names) >= 12
+    for nm in names:
+        assert hasattr(lib, nm), nm
+
+
+def test_default_options_and_strerror(lib):
+    from paper_1609_08114_b200 import lpb
+    o = lpb.default_options()
+    assert o.struct_size == ctypes.sizeof(lpb.Options)
+    assert o.eps_enter == 1e-9 and o.eps_piv == 1e-9 and o.eps_phase1 == 1e-9
+    assert o.max_iter == 0 and o.bland_after == 0 and o.device == -1 and o.n_chunks == 0
+    lib.lpb_strerror.restype = ctypes.c_char_p
+    assert lib.lpb_strerror(-5) == b"no compiled size class fits this LP size"
+    assert lib.lpb_default_options(None) == -1
+
+
+def test_create_argument_validation_without_gpu(lib):
+    P = ctypes.c_void_p
+    ctx = P()
+    # invalid shapes / kinds are rejected before any CUDA call
+    assert lib.lpb_create(ctypes.byref(ctx), 0, 5, 5, 0, None) == -1
+    assert lib.lpb_create(ctypes.byref(ctx), 10, 0, 5, 0, None) == -1
+    assert lib.lpb_create(ctypes.byref(ctx), 10, 5, 5, 7, None) == -1
+    assert lib.lpb_create(ctypes.byref(ctx), 10, 5, 4, 1, None) == -1  # hyperbox needs m=2n
+    assert lib.lpb_create(None, 10, 5, 5, 0, None) == -1
+    assert lib.lpb_create(ctypes.byref(ctx), 10, 4000, 4000, 0, None) == -5  # too big
+    assert lib.lpb_destroy(None) == 0
+
+
+def test_binding_struct_matches_header():
+    """ctypes Options mirrors lpb_options field by field (names and order)."""
+    from paper_1609_08114_b200 import lpb
+    src = re.sub(r"/\*.*?\*/", "", open(HDR).read(), flags=re.S)
+    body = re.search(r"typedef struct \{(.*?)\} lpb_options;", src, re.S).group(1)
+    fields = re.findall(r"(\w+)\s*;", body)
+    assert fields == [f[0] for f in lpb.Options._fields_]

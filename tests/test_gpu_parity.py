@@ -1,0 +1,190 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element by element,
+on the same seeded inputs.  Pass bar (BASELINE.json north_star): status bit-exact,
+objective within 1e-9*max(1,|obj|), primal residual <= 1e-9; in addition the iteration
+counts and fp64 values are required to be identical (the kernels reproduce the oracle's
+arithmetic; a mismatch is a bug, not a tolerance question -- SURVEY §8(c) C-P18)."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import lpgen
+import oracle
+from gpu_util import compare, gpu_solve
+
+pytestmark = pytest.mark.gpu
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "lp_fixtures.json")))
+CLASSES = ["M", "L"]
+
+
+def _classes_for(m, n):
+    return CLASSES
+
+
+@pytest.mark.parametrize("klass", CLASSES)
+def test_golden_fixtures(klass):
+    for fx in GOLD["fixtures"]:
+        A = np.array([fx["A"]], float)
+        b = np.array([fx["b"]], float)
+        c = np.array([fx["c"]], float)
+        o = oracle.solve(A, b, c)
+        g = gpu_solve(A, b, c, kernel_class=klass)
+        compare(A, b, c, g, o)
+        assert g["status"][0] == fx["status"], fx["name"]
+
+
+@pytest.mark.parametrize("klass", CLASSES)
+def test_klee_minty_and_chvatal(klass):
+    for n in range(2, 10):
+        A, b, c = lpgen.klee_minty(n)
+        A, b, c = A[None], b[None], c[None]
+        g = gpu_solve(A, b, c, kernel_class=klass)
+        assert g["status"][0] == 0 and g["obj"][0] == 100.0 ** (n - 1)
+        assert list(g["iters"][0]) == [0, 2 ** n - 1]
+    ch = GOLD["chvatal_cycling"]
+    A, b, c = (np.array([ch[k]], float) for k in ("A", "b", "c"))
+    for K, piv in ch["pivots_by_K"].items():
+        g = gpu_solve(A, b, c, kernel_class=klass, bland_after=int(K))
+        assert g["status"][0] == 0 and g["obj"][0] == 1.0 and g["iters"][0][1] == piv
+    g = gpu_solve(A, b, c, kernel_class=klass, bland_after=-1, max_iter=300)
+    assert g["status"][0] == oracle.ITER_LIMIT
+
+
+CASES = [
+    ("G1", 5, 5, 3000), ("G1", 28, 28, 600), ("G1", 100, 100, 200), ("G1", 60, 13, 300),
+    ("G1", 7, 64, 300), ("G1", 1, 1, 50), ("G1", 1, 9, 50), ("G1", 9, 1, 50),
+    ("mix", 6, 6, 3000), ("mixneg", 6, 6, 3000), ("mixneg", 20, 20, 500),
+    ("mix", 100, 100, 60), ("G2", 8, 8, 2000), ("G2", 50, 50, 100), ("G2light", 60, 60, 60),
+    ("deg", 8, 8, 3000), ("degneg", 8, 8, 3000), ("degneg", 20, 20, 1000),
+]
+
+
+def _gen(gen, B, m, n, seed):
+    if gen == "G1":
+        return lpgen.signed_bounded(B, m, n, seed)
+    if gen == "G2":
+        return lpgen.twophase_signed(B, m, n, seed)
+    if gen == "G2light":
+        return lpgen.twophase_light(B, m, n, seed)
+    if gen.startswith("mix"):
+        return lpgen.status_mix(B, m, n, seed, infeasible_start=gen.endswith("neg"))
+    return lpgen.degenerate(B, m, n, seed, negative_b=gen.endswith("neg"))
+
+
+@pytest.mark.parametrize("klass", CLASSES)
+@pytest.mark.parametrize("gen,m,n,B", CASES, ids=[f"{g}-{m}x{n}" for g, m, n, _ in CASES])
+def test_random_batches(klass, gen, m, n, B):
+    A, b, c = _gen(gen, B, m, n, 1000 + 7 * m + n)
+    o = oracle.solve(A, b, c)
+    g = gpu_solve(A, b, c, kernel_class=klass)
+    compare(A, b, c, g, o)
+
+
+@pytest.mark.parametrize("K", [1, 3])
+def test_bland_coverage_degenerate(K):
+    """G-deg with small Bland thresholds: exercises Bland mode and artificial drive-outs."""
+    for neg in (False, True):
+        A, b, c = lpgen.degenerate(4000, 8, 8, 50 + K + neg, negative_b=neg)
+        o = oracle.solve(A, b, c, bland_after=K)
+        for klass in CLASSES:
+            g = gpu_solve(A, b, c, kernel_class=klass, bland_after=K)
+            compare(A, b, c, g, o)
+
+
+def test_iteration_limit_status():
+    A, b, c = lpgen.signed_bounded(200, 30, 30, 77)
+    o = oracle.solve(A, b, c, max_iter=5)
+    g = gpu_solve(A, b, c, max_iter=5)
+    compare(A, b, c, g, o)
+    assert np.any(g["status"] == oracle.ITER_LIMIT)
+
+
+def test_host_path_equals_device_path_and_chunking():
+    A, b, c = lpgen.status_mix(997, 10, 12, 5, infeasible_start=True)
+    gd = gpu_solve(A, b, c)
+    for nch in (1, 3, 10):
+        gh = gpu_solve(A, b, c, path="host", n_chunks=nch)
+        for k in ("status", "iters"):
+            assert np.array_equal(gd[k], gh[k])
+        assert np.array_equal(gd["obj"], gh["obj"], equal_nan=True)
+        assert np.array_equal(gd["x"], gh["x"], equal_nan=True)
+
+
+def test_scheduling_invariance_grid_and_class():
+    A, b, c = lpgen.status_mix(1500, 16, 16, 6, infeasible_start=True)
+    ref = gpu_solve(A, b, c, kernel_class="M")
+    for kw in (dict(kernel_class="M", grid_ctas=1), dict(kernel_class="M", grid_ctas=37),
+               dict(kernel_class="L"), dict(kernel_class="L", grid_ctas=3)):
+        g = gpu_solve(A, b, c, **kw)
+        for k in ("status", "iters"):
+            assert np.array_equal(ref[k], g[k]), kw
+        assert np.array_equal(ref["obj"], g["obj"], equal_nan=True), kw
+
+
+def test_batch_of_one_and_repeat_solves():
+    import torch
+
+    from paper_1609_08114_b200 import lpb
+    A, b, c = lpgen.signed_bounded(1, 12, 9, 3)
+    o = oracle.solve(A, b, c)
+    s = lpb.Solver(1, 12, 9)
+    At, bt, ct = (torch.from_numpy(v).cuda() for v in (A, b, c))
+    for _ in range(3):
+        s.solve_device(At, bt, ct, sync=True)
+        r = {k: v.cpu().numpy() for k, v in s.device_results().items()}
+        compare(A, b, c, r, o)
+    s.close()
+
+
+def test_abi_errors_on_gpu():
+    import ctypes
+
+    from paper_1609_08114_b200 import lpb
+    s = lpb.Solver(4, 3, 3)
+    st = np.empty(4, np.int32)
+    assert lpb._lib.lpb_results(s._ctx, st.ctypes.data_as(ctypes.c_void_p), None, None, None) == lpb.ESTATE
+    assert lpb._lib.lpb_solve_batch(s._ctx, None, None, None, 0) == lpb.EINVAL
+    s.close()
+
+
+# ---------------- hyperbox (type 3) ----------------
+
+@pytest.mark.parametrize("n,B", [(1, 1000), (2, 5000), (5, 200000), (7, 10001), (28, 60000),
+                                 (33, 3001)])
+def test_hyperbox_bit_exact(n, B):
+    import torch
+
+    from paper_1609_08114_b200 import lpb
+    lo, hi, dirs = lpgen.hyperbox(B, n, 60 + n)
+    dirs = dirs.copy()
+    dirs[: min(B, 7), 0] = -0.0  # the l_i = -0.0 branch takes hi (C15)
+    o = oracle.hyperbox(lo, hi, dirs)
+    g = lpb.hyperbox(lo, hi, torch.from_numpy(dirs).cuda())
+    assert np.array_equal(g["status"].cpu().numpy(), o["status"])
+    assert np.array_equal(g["obj"].cpu().numpy(), o["obj"])
+    assert np.array_equal(g["x"].cpu().numpy(), o["x"])
+    gh = lpb.hyperbox(lo, hi, dirs)  # host pipeline path
+    assert np.array_equal(gh["obj"], o["obj"]) and np.array_equal(gh["x"], o["x"])
+
+
+def test_hyperbox_per_lp_box_and_empty():
+    import torch
+
+    from paper_1609_08114_b200 import lpb
+    B, n = 3000, 6
+    g0 = lpgen.rng(9)
+    lo = g0.uniform(-1, 1, (B, n))
+    hi = lo + g0.uniform(-0.1, 1, (B, n))  # some boxes empty
+    dirs = g0.standard_normal((B, n))
+    o = oracle.hyperbox(lo, hi, dirs)
+    box = torch.from_numpy(np.ascontiguousarray(np.concatenate([hi, -lo], axis=1))).cuda()
+    s = lpb.Solver(B, 2 * n, n, lpb.HYPERBOX)
+    s.solve_device(None, box, torch.from_numpy(dirs).cuda(), sync=True)
+    r = {k: v.cpu().numpy() for k, v in s.device_results().items()}
+    assert np.array_equal(r["status"], o["status"])
+    assert np.array_equal(r["obj"], o["obj"])
+    assert np.array_equal(r["x"], o["x"], equal_nan=True)
+    assert np.any(o["status"] == oracle.INFEASIBLE)
+    s.close()
