@@ -107,7 +107,7 @@ extern "C" const char* lpb_last_error(lpb_ctx* c) { return c ? c->err : ""; }
 
 // Size-class capacity check at the best case (no artificial rows).
 static bool general_fits_any(int m, int n) {
-  return thread_fits(m, n) || block_fits(1, m, n, 0) || block_fits(2, m, n, 0) ||
+  return reg_fits(m, n, 0) || block_fits(1, m, n, 0) || block_fits(2, m, n, 0) ||
          block_fits(4, m, n, 0);
 }
 
@@ -197,8 +197,7 @@ static int choose_class(const lpb_ctx* c, int kmax, int* cl) {
   const int m = c->m, n = c->n;
   const int forced = c->opt.kernel_class;
   *cl = 1;
-  if (forced == CLASS_S) return thread_fits(m, n) ? CLASS_S : -1;
-  if (forced == CLASS_R) return reg_fits(m, n, kmax) ? CLASS_R : -1;
+  if (forced == CLASS_R || forced == CLASS_S) return reg_fits(m, n, kmax) ? CLASS_R : -1;
   if (forced == CLASS_M) return block_fits(1, m, n, kmax) ? CLASS_M : -1;
   if (forced == CLASS_L) {
     for (int q : {2, 4})
@@ -236,21 +235,17 @@ static void fill_args(const lpb_ctx* c, SimplexArgs& a, int64_t lp0, int64_t cnt
 }
 
 // Enqueue the general-LP kernels for one resident chunk on stream s.
+// The size class depends on kmax = max #{b_i < 0} (it sets the condensed width n + k):
+// when a register layout holds even the worst case k = m, no prepass is needed; otherwise
+// one tiny prepass kernel + a 4-byte D2H give kmax first.
 static int run_general(lpb_ctx* c, cudaStream_t s, int64_t lp0, int64_t cnt, const double* A,
                        const double* b, const double* cv, bool nox, int kmax_known,
                        int* ticket, int* launches) {
   int kmax = kmax_known;
-  const bool s_class = (c->opt.kernel_class == CLASS_S) ||
-                       (c->opt.kernel_class == CLASS_AUTO && thread_fits(c->m, c->n));
-  SimplexArgs a;
-  if (s_class) {
-    if (!thread_fits(c->m, c->n)) return LPB_ETOOBIG;
-    fill_args(c, a, lp0, cnt, A, b, cv, nox, c->m, ticket);
-    LPB_CUDA(c, launch_simplex_thread(a, c->opt.grid_ctas, s));
-    *launches += 1;
-    c->last_class = CLASS_S;
-    return LPB_OK;
-  }
+  const int forced = c->opt.kernel_class;
+  const bool r_ok_worst = reg_fits(c->m, c->n, c->m);
+  if (kmax < 0 && r_ok_worst && (forced == CLASS_AUTO || forced == CLASS_R || forced == CLASS_S))
+    kmax = c->m;  // worst-case capacity, no prepass
   if (kmax < 0) {  // device prepass: kmax over the chunk (one tiny kernel + 4-byte D2H)
     LPB_CUDA(c, launch_count_art(b, cnt, c->m, c->d_kmax, s));
     LPB_CUDA(c, cudaMemcpyAsync(c->h_kmax, c->d_kmax, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -261,6 +256,7 @@ static int run_general(lpb_ctx* c, cudaStream_t s, int64_t lp0, int64_t cnt, con
   int cl = 1;
   const int klass = choose_class(c, kmax, &cl);
   if (klass < 0) return LPB_ETOOBIG;
+  SimplexArgs a;
   fill_args(c, a, lp0, cnt, A, b, cv, nox, kmax, ticket);
   LPB_CUDA(c, cudaMemsetAsync(ticket, 0, sizeof(int), s));
   int ctas = 0;

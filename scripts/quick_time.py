@@ -23,5 +23,7 @@ def tm(name, B=None, klass=None):
     it = r['iters'].float().mean(0).tolist()
     print(name, B, 'class', s.launch_info(), 'ms', ['%.3f' % t for t in ts], 'LPs/s %.3e' % (s.batch / (min(ts) / 1e3)), 'iters', it, flush=True)
 for a in sys.argv[1:]:
-    nm, B = a.split(':') if ':' in a else (a, None)
-    tm(nm, int(B) if B else None)
+    parts = a.split(':')
+    nm = parts[0]; B = int(parts[1]) if len(parts) > 1 and parts[1] else None
+    kl = parts[2] if len(parts) > 2 else None
+    tm(nm, B, kl)

@@ -16,11 +16,13 @@ from gpu_util import compare, gpu_solve
 pytestmark = pytest.mark.gpu
 
 GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "lp_fixtures.json")))
-CLASSES = ["M", "L"]
+CLASSES = ["R", "M", "L"]
 
 
-def _classes_for(m, n):
-    return CLASSES
+def _reg_fits(m, n, k):
+    # mirrors the instantiated register layouts in csrc/simplex_reg.cu (capacity m x (n+k))
+    caps = [(8, 12, 1), (16, 24, 1), (32, 32, 1), (64, 64, 1), (112, 112, 0), (112, 112, 1)]
+    return any(m <= r and n + k <= c and (k == 0 or two) for r, c, two in caps)
 
 
 @pytest.mark.parametrize("klass", CLASSES)
@@ -77,6 +79,8 @@ def _gen(gen, B, m, n, seed):
 @pytest.mark.parametrize("gen,m,n,B", CASES, ids=[f"{g}-{m}x{n}" for g, m, n, _ in CASES])
 def test_random_batches(klass, gen, m, n, B):
     A, b, c = _gen(gen, B, m, n, 1000 + 7 * m + n)
+    if klass == "R" and not _reg_fits(m, n, int((b < 0).sum(axis=1).max())):
+        pytest.skip("no register layout for this size")
     o = oracle.solve(A, b, c)
     g = gpu_solve(A, b, c, kernel_class=klass)
     compare(A, b, c, g, o)
