@@ -1,22 +1,25 @@
-// simplex_reg.cu — R class: one LP per thread block with the condensed fp64 tableau
-// RESIDENT IN REGISTERS (the B200 register file is 256 KB per SM: two 100x100 tableaux).
+// simplex_reg.cu — R class: one LP per thread block (one warp for small LPs) with the
+// condensed fp64 tableau RESIDENT IN REGISTERS (256 KB register file per SM).
 //
 // Same method and arithmetic as simplex_block.cu / the oracle (§3.1 Steps 1-3,
-// Listing 1; two-phase PAPER.md:76), different storage:
+// Listing 1; two-phase PAPER.md:76), different storage and reductions:
 //   * thread (tr, tc) of a TR x TC grid owns constraint rows i = tr + TR*a (a < A) and
 //     nonbasic positions p = tc + TC*b (b < BC): double T[A][BC] in registers;
-//   * the objective row(s) are REPLICATED in every thread for its positions (d2[BC], d1[BC]),
-//     so Step 1 (Dantzig argmax) is a register scan + one warp butterfly in every warp --
-//     no barrier;
-//   * the RHS column lives in SMEM and is updated LAZILY: the owners of the next pivot
-//     column (one thread per row) apply the previous pivot's RHS update to their rows just
-//     before they use it in the ratio test (each row by exactly one thread, race-free);
-//   * per pivot: owners of column e publish it (SMEM, double-buffered) and their ratio-test
-//     partial -> barrier 1 -> everyone reduces the TR partials; the owners of row l publish
-//     the pivot row / PE -> barrier 2 -> every thread applies T -= f * prow to its registers
-//     (A*BC DFMAs, no per-element branches; row l and column e are fixed up afterwards).
-// The update is one __fma_rn(-f_i, prow_p, T_ip) per element, the pivot row an IEEE
-// division, the ratio an IEEE division: bit-identical to oracle/lpb_oracle.c.
+//   * the objective row(s) are REPLICATED in every thread for its positions (d2, d1), so
+//     Step 1 (Dantzig argmax) is a register scan + a REDUX-based warp argmax
+//     in every warp (no barrier);
+//   * Step 2 (ratio test): the owners of column e publish it to SMEM; each
+//     lane of a warp then takes one of the warp's rows (one IEEE division per lane), applies
+//     the previous pivot's RHS update to it (the RHS column lives in SMEM and is updated
+//     lazily, each row by exactly one lane), and the warp argmin goes to a per-warp partial
+//     -> barrier 1 -> every warp reduces the partials;
+//   * Step 3: the owners of row l publish prow = row / PE -> barrier 2 ->
+//     every thread applies T_ip = fma(-f_i, prow_p, T_ip) to its registers (A*BC DFMAs with
+//     no per-element branch), then row l and position e are fixed up.
+// Reductions use order-preserving integer keys and the sm_100 REDUX (__reduce_*_sync)
+// instructions: (value, tie key) argmax/argmin in three warp-wide REDUX steps.
+// All arithmetic matches oracle/lpb_oracle.c bit for bit (IEEE __ddiv_rn, explicit
+// __fma_rn, ascending __dadd_rn sums).
 #include <climits>
 #include <cstdlib>
 
@@ -29,43 +32,51 @@ constexpr unsigned FULL = 0xffffffffu;
 constexpr int DEADV = INT_MAX;
 
 __device__ __forceinline__ double neg_inf() { return __longlong_as_double(0xfff0000000000000ll); }
+__device__ __forceinline__ double pos_inf() { return __longlong_as_double(0x7ff0000000000000ll); }
+__device__ __forceinline__ double qnan() { return __longlong_as_double(0x7ff8000000000000ll); }
 
-struct Cand {
-  double v;
-  int key;
-  int pos;
-};
-enum { MAX_V = 0, MIN_KEY = 1, MIN_V = 2 };
+// Order-preserving 64-bit key of a double; -0.0 is folded to +0.0 first so that IEEE
+// equality (-0 == +0) remains a tie, as in the oracle's comparisons.
+__device__ __forceinline__ unsigned long long okey(double d) {
+  const unsigned long long u = (unsigned long long)__double_as_longlong(__dadd_rn(d, 0.0));
+  return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+}
+__device__ __forceinline__ unsigned ikey(int t) { return (unsigned)t ^ 0x80000000u; }
 
-template <int MODE>
-__device__ __forceinline__ bool better(const Cand& a, const Cand& b) {
-  if (a.pos < 0) return false;
-  if (b.pos < 0) return true;
-  if (MODE == MAX_V) return a.v > b.v || (a.v == b.v && a.key < b.key);
-  if (MODE == MIN_KEY) return a.key < b.key;
-  return a.v < b.v || (a.v == b.v && a.key < b.key);
+// Warp argmax of (key desc, tie asc) over lanes with `valid`; returns the winner lane or -1.
+// Must be called by all 32 lanes.
+__device__ __forceinline__ int warp_argmax(bool valid, unsigned long long k, unsigned tie) {
+  if (__ballot_sync(FULL, valid) == 0u) return -1;
+  const unsigned hi = valid ? (unsigned)(k >> 32) : 0u;
+  const unsigned mhi = __reduce_max_sync(FULL, hi);
+  const bool c1 = valid && hi == mhi;
+  const unsigned lo = c1 ? (unsigned)k : 0u;
+  const unsigned mlo = __reduce_max_sync(FULL, lo);
+  const bool c2 = c1 && (unsigned)k == mlo;
+  const unsigned t = c2 ? tie : 0xffffffffu;
+  const unsigned mt = __reduce_min_sync(FULL, t);
+  return __ffs(__ballot_sync(FULL, c2 && tie == mt)) - 1;
 }
 
-template <int MODE>
-__device__ __forceinline__ Cand warp_reduce(Cand c) {
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) {
-    Cand o;
-    o.v = __shfl_xor_sync(FULL, c.v, off);
-    o.key = __shfl_xor_sync(FULL, c.key, off);
-    o.pos = __shfl_xor_sync(FULL, c.pos, off);
-    if (better<MODE>(o, c)) c = o;
-  }
-  return c;
+// Warp argmin of (key asc, tie asc) over lanes with `valid`; returns the winner lane or -1.
+__device__ __forceinline__ int warp_argmin(bool valid, unsigned long long k, unsigned tie) {
+  if (__ballot_sync(FULL, valid) == 0u) return -1;
+  const unsigned hi = valid ? (unsigned)(k >> 32) : 0xffffffffu;
+  const unsigned mhi = __reduce_min_sync(FULL, hi);
+  const bool c1 = valid && hi == mhi;
+  const unsigned lo = c1 ? (unsigned)k : 0xffffffffu;
+  const unsigned mlo = __reduce_min_sync(FULL, lo);
+  const bool c2 = c1 && (unsigned)k == mlo;
+  const unsigned t = c2 ? tie : 0xffffffffu;
+  const unsigned mt = __reduce_min_sync(FULL, t);
+  return __ffs(__ballot_sync(FULL, c2 && tie == mt)) - 1;
 }
 
-// Barrier of one LP group (NT threads).  A CTA may hold G independent groups (one LP each,
-// named barriers 1..G) so that G register-resident tableaux share an SM without the
-// register-allocation rounding of G separate CTAs.
+// Barrier of the LP's thread group.
 template <int NT>
-__device__ __forceinline__ void gsync(int g) {
+__device__ __forceinline__ void gsync() {
   if constexpr (NT == 32) __syncwarp();
-  else asm volatile("bar.sync %0, %1;" ::"r"(g + 1), "n"(NT) : "memory");
+  else __syncthreads();
 }
 
 #define LPB_CASES(BODY)                                                                     \
@@ -74,7 +85,13 @@ __device__ __forceinline__ void gsync(int g) {
   BODY(20) BODY(21) BODY(22) BODY(23) BODY(24) BODY(25) BODY(26) BODY(27) BODY(28)         \
   BODY(29) BODY(30) BODY(31)
 
-template <int TR, int TC, int A, int BC, bool TWO>
+struct Part {  // a (value, tie, index) reduction partial
+  double v;
+  int tie;
+  int idx;
+};
+
+template <int TR, int TC, int A, int BC>
 struct RegSmem {
   static constexpr int RCAP = TR * A, CCAP = TC * BC, NWARP = (TR * TC) / 32;
   double colE[2][RCAP];  // pivot column (constraint rows), double-buffered by pivot parity
@@ -84,25 +101,25 @@ struct RegSmem {
   int bkey[RCAP];        // row -> basic variable key (>= 0 real, < 0 artificial)
   int nbvar[CCAP];       // position -> nonbasic variable index (DEADV: dead / padding)
   int negrows[RCAP];     // ascending rows with b_i < 0
-  int wcount[NWARP > 0 ? NWARP : 1];
-  Cand part[TR];         // ratio-test partial per thread-row
-  Cand wpart[NWARP > 0 ? NWARP : 1];
+  int wcount[NWARP];
+  Part part[NWARP];      // ratio-test partial per warp
   double prow_rhs;
-  double binf;
   int lp;
   int leaving;
 };
 
-template <int TR, int TC, int A, int BC, bool TWO, int MINB, int G>
-__global__ void __launch_bounds__(TR * TC * G, MINB) simplex_reg_kernel(SimplexArgs a) {
+template <int TR, int TC, int A, int BC, bool TWO, int MINB>
+__global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs a) {
   constexpr int NT = TR * TC, RCAP = TR * A, CCAP = TC * BC, NWARP = NT / 32;
-  static_assert(NT % 32 == 0 && TR <= 32 && TC <= 32 && A <= 32 && BC <= 32, "layout");
-  using SM = RegSmem<TR, TC, A, BC, TWO>;
-  __shared__ SM smg[G];
-  const int g = threadIdx.x / NT;
-  SM& sm = smg[g];
-  const int tid = threadIdx.x - g * NT, lane = tid & 31, w = tid >> 5;
+  constexpr int RPW = 32 / TC;  // thread-rows per warp
+  static_assert(NT % 32 == 0 && 32 % TC == 0 && TR <= 32 && A <= 32 && BC <= 32, "layout");
+  static_assert(RPW * A <= 32, "the warp's rows must fit its lanes");
+  __shared__ RegSmem<TR, TC, A, BC> sm;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int tr = tid / TC, tc = tid - (tid / TC) * TC;
+  // the row this lane serves in the warp-parallel ratio test
+  const int rrow = (w * RPW + lane % RPW) + TR * (lane / RPW);
+  const bool rlane = lane < RPW * A;
   const int m = a.m, n = a.n;
 
   double T[A][BC];
@@ -111,14 +128,14 @@ __global__ void __launch_bounds__(TR * TC * G, MINB) simplex_reg_kernel(SimplexA
 
   for (;;) {
     if (tid == 0) sm.lp = atomicAdd(a.ticket, 1);
-    gsync<NT>(g);
+    gsync<NT>();
     const int64_t lp = sm.lp;
     if (lp >= a.batch) break;
     const double* __restrict__ Ak = a.A + lp * (int64_t)m * n;
     const double* __restrict__ bk = a.b + lp * (int64_t)m;
     const double* __restrict__ ck = a.c + lp * (int64_t)n;
 
-    // ---- build: negated rows (ascending), basis keys, |b|_inf, RHS ----
+    // ---- build: negated rows (ascending), basis keys, |b|_inf, RHS (R7) ----
     int k = 0;
     double binf = 0.0;
     for (int base = 0; base < m; base += NT) {
@@ -128,7 +145,7 @@ __global__ void __launch_bounds__(TR * TC * G, MINB) simplex_reg_kernel(SimplexA
       binf = fmax(binf, fabs(bi));
       const unsigned bal = __ballot_sync(FULL, neg);
       if (lane == 0) sm.wcount[w] = __popc(bal);
-      gsync<NT>(g);
+      gsync<NT>();
       int off = k, tot = 0;
 #pragma unroll
       for (int q = 0; q < NWARP; ++q) {
@@ -142,22 +159,20 @@ __global__ void __launch_bounds__(TR * TC * G, MINB) simplex_reg_kernel(SimplexA
         sm.rhs[i] = neg ? -bi : bi;
       }
       k += tot;
-      gsync<NT>(g);
+      gsync<NT>();
     }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) binf = fmax(binf, __shfl_xor_sync(FULL, binf, off));
-    if (lane == 0) sm.wpart[w].v = binf;
-    gsync<NT>(g);
-    binf = sm.wpart[0].v;
+    if (lane == 0) sm.part[w].v = binf;
+    gsync<NT>();
 #pragma unroll
-    for (int q = 1; q < NWARP; ++q) binf = fmax(binf, sm.wpart[q].v);
+    for (int q = 0; q < NWARP; ++q) binf = fmax(binf, sm.part[q].v);
     const int npos = n + k;
     int st = (m > RCAP || npos > CCAP || (!TWO && k > 0)) ? ST_NUMERICAL : -1;
     for (int p = tid; p < CCAP; p += NT)
       sm.nbvar[p] = (p < n) ? p : (p < npos ? n + sm.negrows[p - n] : DEADV);
     for (int i = m + tid; i < RCAP; i += NT) sm.rhs[i] = 0.0;
 
-    // tile + phase-II replica
 #pragma unroll
     for (int ai = 0; ai < A; ++ai) {
       const int i = tr + TR * ai;
@@ -185,25 +200,22 @@ __global__ void __launch_bounds__(TR * TC * G, MINB) simplex_reg_kernel(SimplexA
     }
     double z2 = 0.0, z1 = 0.0;
     if constexpr (TWO) {
-      // phase-I row: ascending-row sums of the negated rows (R7), computed once by thread-row
-      // 0 into SMEM scratch, then replicated into every thread's positions
+      // phase-I row: ascending-row sums of the negated rows, computed once by thread-row 0
+      // into SMEM scratch, then replicated into every thread's positions
       if (k > 0 && st < 0) {
         if (tr == 0) {
-          for (int b = 0; b < BC; ++b) {
-            const int p = tc + TC * b;
-            if (p >= npos) continue;
+          for (int p = tc; p < npos; p += TC) {
             double acc = 0.0;
             for (int t = 0; t < k; ++t) {
               const int r = sm.negrows[t];
-              double v;
-              if (p < n) v = -__ldg(Ak + (int64_t)r * n + p);
-              else v = (r == sm.negrows[p - n]) ? -1.0 : -0.0;
+              const double v = (p < n) ? -__ldg(Ak + (int64_t)r * n + p)
+                                       : ((r == sm.negrows[p - n]) ? -1.0 : -0.0);
               acc = __dadd_rn(acc, v);
             }
             sm.prow[p] = acc;
           }
         }
-        gsync<NT>(g);
+        gsync<NT>();
 #pragma unroll
         for (int b = 0; b < BC; ++b) {
           const int p = tc + TC * b;
@@ -215,19 +227,18 @@ __global__ void __launch_bounds__(TR * TC * G, MINB) simplex_reg_kernel(SimplexA
         for (int b = 0; b < BC; ++b) d1[b] = neg_inf();
       }
     }
-    gsync<NT>(g);
+    gsync<NT>();
 
     // ---- Steps 1-3, two phases ----
-    // One straight-line pivot body; `drive` selects the artificial drive-out pivots of the
-    // phase switch (R9) instead of Steps 1-2.
     int it1 = 0, it2 = 0, stall = 0, phase = (TWO && k > 0) ? 1 : 2;
     int par = 0, l_prev = -1, dl = 0;
     bool pend = false, drive = false;
     while (st < 0) {
       const bool bland = a.bland_K > 0 && stall >= a.bland_K;
-      int e = -1, evar = 0;
-      int l = -1;
+      const bool p1 = TWO && phase == 1;
+      int e = -1, evar = 0, l = -1;
       if (drive) {
+        // phase switch (R9): drive the next basic artificial out on max |T[l][p]|
         while (dl < m && sm.bkey[dl] >= 0) ++dl;
         if (dl >= m) {
           drive = false;
@@ -236,7 +247,10 @@ __global__ void __launch_bounds__(TR * TC * G, MINB) simplex_reg_kernel(SimplexA
           continue;
         }
         l = dl++;
-        Cand cd{0.0, 0, -1};
+        bool val = false;
+        double bv = 0.0;
+        unsigned bvar = 0;
+        int bp = -1;
         if (tr == l % TR) {
           const int al = l / TR;
 #pragma unroll
@@ -245,118 +259,159 @@ __global__ void __launch_bounds__(TR * TC * G, MINB) simplex_reg_kernel(SimplexA
 #pragma unroll
             for (int ai = 1; ai < A; ++ai) v = (ai == al) ? T[ai][b] : v;
             v = fabs(v);
-            if (d2[b] != neg_inf() && v > a.eps_piv) {  // live position (not dead / padding)
-              const Cand cc{v, sm.nbvar[tc + TC * b], tc + TC * b};
-              if (better<MAX_V>(cc, cd)) cd = cc;
-            }
-          }
-        }
-        cd = warp_reduce<MAX_V>(cd);
-        if (lane == 0) sm.wpart[w] = cd;
-        gsync<NT>(g);
-        Cand r{0.0, 0, -1};
-        if (lane < NWARP) r = sm.wpart[lane];
-        cd = warp_reduce<MAX_V>(r);
-        gsync<NT>(g);
-        if (cd.pos < 0) continue;  // redundant row: the artificial stays basic at 0
-        e = cd.pos;
-        evar = cd.key;
-      } else {
-        // Step 1: entering position from the replicated objective row (warp-local)
-        Cand ce{0.0, 0, -1};
-        const bool p1 = TWO && phase == 1;
-        if (!bland) {
-          double bv = 0.0;
-          int bb = -1;
-#pragma unroll
-          for (int b = 0; b < BC; ++b) {
-            const double v = p1 ? d1[TWO ? b : 0] : d2[b];
-            if (v > a.eps_enter) {
-              if (bb < 0 || v > bv) {
+            if (d2[b] != neg_inf() && v > a.eps_piv) {  // live position
+              const int p = tc + TC * b;
+              const unsigned var = (unsigned)sm.nbvar[p];
+              if (!val || v > bv || (v == bv && var < bvar)) {
+                val = true;
                 bv = v;
-                bb = b;
-              } else if (v == bv && sm.nbvar[tc + TC * b] < sm.nbvar[tc + TC * bb]) {
-                bb = b;  // exact tie inside the thread: lowest variable index
+                bvar = var;
+                bp = p;
               }
             }
           }
-          if (bb >= 0) ce = Cand{bv, sm.nbvar[tc + TC * bb], tc + TC * bb};
-          ce = warp_reduce<MAX_V>(ce);
-        } else {
+        }
+        const int wl = warp_argmax(val, okey(bv), bvar);
+        Part pw{0.0, INT_MAX, -1};
+        if (wl >= 0) {
+          pw.v = __shfl_sync(FULL, bv, wl);
+          pw.tie = (int)__shfl_sync(FULL, bvar, wl);
+          pw.idx = __shfl_sync(FULL, bp, wl);
+        }
+        if (lane == 0) sm.part[w] = pw;
+        gsync<NT>();
+        const Part q = (lane < NWARP) ? sm.part[lane] : Part{0.0, INT_MAX, -1};
+        const int ql = warp_argmax(q.idx >= 0, okey(q.v), (unsigned)q.tie);
+        gsync<NT>();
+        if (ql < 0) continue;  // redundant row: the artificial stays basic at 0
+        e = __shfl_sync(FULL, q.idx, ql);
+        evar = __shfl_sync(FULL, q.tie, ql);
+      } else {
+        // Step 1: entering position from the replicated objective row (warp-local)
+        double bv = neg_inf();
+        int bb = 0;
+        unsigned bvar = 0;
+        bool val;
+        if (!bland) {
+#pragma unroll
+          for (int b = 0; b < BC; ++b) {
+            const double v = p1 ? d1[TWO ? b : 0] : d2[b];
+            const bool take = v > bv;  // first maximum: lowest b on ties (fixed below)
+            bv = take ? v : bv;
+            bb = take ? b : bb;
+          }
+          val = bv > a.eps_enter;
+          bool tie = false;
+#pragma unroll
+          for (int b = 0; b < BC; ++b) {
+            const double v = p1 ? d1[TWO ? b : 0] : d2[b];
+            tie |= (b != bb) && (v == bv);
+          }
+          bvar = val ? (unsigned)sm.nbvar[tc + TC * bb] : 0u;
+          if (__any_sync(FULL, val && tie)) {  // rare: exact tie inside a thread -> var index
+            if (val && tie) {
+#pragma unroll
+              for (int b = 0; b < BC; ++b) {
+                const double v = p1 ? d1[TWO ? b : 0] : d2[b];
+                const unsigned var = (unsigned)sm.nbvar[tc + TC * b];
+                if (v == bv && var < bvar) {
+                  bvar = var;
+                  bb = b;
+                }
+              }
+            }
+          }
+        } else {  // Bland: the lowest variable index with d > eps_enter
+          val = false;
+          bvar = 0xffffffffu;
 #pragma unroll
           for (int b = 0; b < BC; ++b) {
             const double v = p1 ? d1[TWO ? b : 0] : d2[b];
             if (v > a.eps_enter) {
-              const Cand cc{v, sm.nbvar[tc + TC * b], tc + TC * b};
-              if (better<MIN_KEY>(cc, ce)) ce = cc;
+              const unsigned var = (unsigned)sm.nbvar[tc + TC * b];
+              if (var < bvar) {
+                bvar = var;
+                bb = b;
+                bv = v;
+                val = true;
+              }
             }
           }
-          ce = warp_reduce<MIN_KEY>(ce);
         }
-        if (ce.pos < 0) {
+        const int wl = bland ? warp_argmin(val, 0ull, bvar) : warp_argmax(val, okey(bv), bvar);
+        if (wl < 0) {
           if (phase == 2) { st = ST_OPTIMAL; break; }
           if (z1 > a.eps_phase1 * fmax(1.0, binf)) { st = ST_INFEASIBLE; break; }
-          drive = true;  // phase-I optimum with w* ~ 0: drive artificials out (R9)
+          drive = true;  // phase-I optimum with w* ~ 0
           dl = 0;
           continue;
         }
         if (it1 + it2 >= a.max_iter) { st = ST_ITER_LIMIT; break; }
-        e = ce.pos;
-        evar = ce.key;
+        e = __shfl_sync(FULL, tc + TC * bb, wl);
+        evar = (int)__shfl_sync(FULL, bvar, wl);
       }
 
-      // Step 2 part 1 (owners of position e): apply the pending RHS update to my rows,
-      // publish column e (+ its objective-row entries) and my ratio-test partial.
+      // Step 2a: the owners of position e publish column e (+ objective-row entries)
       const int be = e / TC, etc = e - be * TC;
+      double* colE = sm.colE[par];
       if (tc == etc) {
-        Cand cr{0.0, 0, -1};
-        const double prr = sm.prow_rhs;
-#pragma unroll
-        for (int ai = 0; ai < A; ++ai) {
-          const int i = tr + TR * ai;
-          double v = T[ai][0];
-#pragma unroll
-          for (int b = 1; b < BC; ++b) v = (b == be) ? T[ai][b] : v;
-          sm.colE[par][i] = v;
-          if (i < m) {
-            double r = sm.rhs[i];
-            if (pend) {
-              r = (i == l_prev) ? prr : __fma_rn(-sm.colE[par ^ 1][i], prr, r);
-              sm.rhs[i] = r;
-            }
-            if (!drive && v > a.eps_piv) {
-              const Cand cc{__ddiv_rn(r, v), bland ? sm.bkey[i] : i, i};
-              if (better<MIN_V>(cc, cr)) cr = cc;
-            }
-          }
-        }
-        if (tr == 0) {
-          double v2 = d2[0];
-#pragma unroll
-          for (int b = 1; b < BC; ++b) v2 = (b == be) ? d2[b] : v2;
-          sm.fobj[par][0] = v2;
-          if constexpr (TWO) {
-            double v1 = d1[0];
-#pragma unroll
-            for (int b = 1; b < BC; ++b) v1 = (b == be) ? d1[b] : v1;
-            sm.fobj[par][1] = v1;
-          }
-        }
-        if (!drive) sm.part[tr] = cr;
+#define LPB_PUB(x)                                                                    \
+  case x:                                                                             \
+    if constexpr ((x) < BC) {                                                         \
+      _Pragma("unroll") for (int ai = 0; ai < A; ++ai) colE[tr + TR * ai] = T[ai][x]; \
+      if (tr == 0) {                                                                  \
+        sm.fobj[par][0] = d2[x];                                                      \
+        if constexpr (TWO) sm.fobj[par][1] = d1[x];                                   \
+      }                                                                               \
+    }                                                                                 \
+    break;
+        switch (be) { LPB_CASES(LPB_PUB) default: break; }
+#undef LPB_PUB
       }
-      gsync<NT>(g);  // barrier 1
+      __syncwarp();
+      // Step 2b: lane-parallel lazy RHS update + ratio test over the warp's rows
+      {
+        bool val = false;
+        double ratio = 0.0;
+        int tie = INT_MAX;
+        const int i = rrow;
+        if (rlane && i < m) {
+          double r = sm.rhs[i];
+          if (pend) {
+            const double prr = sm.prow_rhs;
+            r = (i == l_prev) ? prr : __fma_rn(-sm.colE[par ^ 1][i], prr, r);
+            sm.rhs[i] = r;
+          }
+          if (!drive) {
+            const double v = colE[i];
+            val = v > a.eps_piv;
+            ratio = __ddiv_rn(r, val ? v : 1.0);
+            tie = bland ? sm.bkey[i] : i;
+          }
+        }
+        if (!drive) {
+          const int wl = warp_argmin(val, okey(ratio), ikey(tie));
+          Part pw{0.0, INT_MAX, -1};
+          if (wl >= 0) {
+            pw.v = __shfl_sync(FULL, ratio, wl);
+            pw.tie = __shfl_sync(FULL, tie, wl);
+            pw.idx = __shfl_sync(FULL, i, wl);
+          }
+          if (lane == 0) sm.part[w] = pw;
+        }
+      }
+      gsync<NT>();  // barrier 1
       double theta = 0.0;
-      if (!drive) {  // Step 2 part 2: argmin over the TR partials, in every warp
-        Cand cr{0.0, 0, -1};
-        if (lane < TR) cr = sm.part[lane];
-        cr = warp_reduce<MIN_V>(cr);
-        if (cr.pos < 0) { st = (phase == 2) ? ST_UNBOUNDED : ST_NUMERICAL; break; }
-        l = cr.pos;
-        theta = cr.v;
+      if (!drive) {  // Step 2c: argmin over the warp partials, in every warp
+        const Part q = (lane < NWARP) ? sm.part[lane] : Part{0.0, INT_MAX, -1};
+        const int ql = warp_argmin(q.idx >= 0, okey(q.v), ikey(q.tie));
+        if (ql < 0) { st = (phase == 2) ? ST_UNBOUNDED : ST_NUMERICAL; break; }
+        l = __shfl_sync(FULL, q.idx, ql);
+        theta = __shfl_sync(FULL, q.v, ql);
       }
 
-      // Step 3 (PAPER.md:163-172): pivot row / PE by the owners of row l
-      const double pe = sm.colE[par][l];
+      // Step 3: pivot row / PE by the owners of row l (PAPER.md:163)
+      const double pe = colE[l];
       if (tid == 0) {
         const int lv = sm.bkey[l];
         sm.bkey[l] = evar;
@@ -365,19 +420,20 @@ __global__ void __launch_bounds__(TR * TC * G, MINB) simplex_reg_kernel(SimplexA
       }
       const int ltr = l % TR, al = l / TR;
       if (tr == ltr) {
-#pragma unroll
-        for (int b = 0; b < BC; ++b) {
-          const int p = tc + TC * b;
-          double v = T[0][b];
-#pragma unroll
-          for (int ai = 1; ai < A; ++ai) v = (ai == al) ? T[ai][b] : v;
-          sm.prow[p] = __ddiv_rn(p == e ? 1.0 : v, pe);
-        }
+#define LPB_PROW(x)                                                                 \
+  case x:                                                                           \
+    if constexpr ((x) < A) {                                                        \
+      _Pragma("unroll") for (int b = 0; b < BC; ++b) {                              \
+        const int p = tc + TC * b;                                                  \
+        sm.prow[p] = __ddiv_rn(p == e ? 1.0 : T[x][b], pe);                         \
+      }                                                                             \
+    }                                                                               \
+    break;
+        switch (al) { LPB_CASES(LPB_PROW) default: break; }
+#undef LPB_PROW
         if (tc == 0) sm.prow_rhs = __ddiv_rn(sm.rhs[l], pe);
       }
-      gsync<NT>(g);  // barrier 2
-      // update: T_ip = fma(-f_i, prow_p, T_ip) on every owned element, then fix row l and
-      // position e
+      gsync<NT>();  // barrier 2
       {
         const double prr = sm.prow_rhs;
         const int leaving = sm.leaving;
@@ -387,12 +443,6 @@ __global__ void __launch_bounds__(TR * TC * G, MINB) simplex_reg_kernel(SimplexA
         const double f2 = -sm.fobj[par][0];
         const bool upd1 = TWO && phase == 1;
         const double f1 = TWO ? -sm.fobj[par][1] : 0.0;
-#pragma unroll
-        for (int ai = 0; ai < A; ++ai) {
-          const double fi = -sm.colE[par][tr + TR * ai];
-#pragma unroll
-          for (int b = 0; b < BC; ++b) T[ai][b] = __fma_rn(fi, pv[b], T[ai][b]);
-        }
 #pragma unroll
         for (int b = 0; b < BC; ++b) {
           d2[b] = __fma_rn(f2, pv[b], d2[b]);
@@ -404,7 +454,13 @@ __global__ void __launch_bounds__(TR * TC * G, MINB) simplex_reg_kernel(SimplexA
         if constexpr (TWO) {
           if (upd1) z1 = __fma_rn(f1, prr, z1);
         }
-        if (tr == ltr) {
+#pragma unroll
+        for (int ai = 0; ai < A; ++ai) {
+          const double fi = -colE[tr + TR * ai];
+#pragma unroll
+          for (int b = 0; b < BC; ++b) T[ai][b] = __fma_rn(fi, pv[b], T[ai][b]);
+        }
+        if (tr == ltr) {  // row l becomes the pivot row
 #define LPB_ROWFIX(x)                                                                  \
   case x:                                                                              \
     if constexpr ((x) < A) {                                                           \
@@ -414,22 +470,21 @@ __global__ void __launch_bounds__(TR * TC * G, MINB) simplex_reg_kernel(SimplexA
           switch (al) { LPB_CASES(LPB_ROWFIX) default: break; }
 #undef LPB_ROWFIX
         }
-        if (tc == etc) {
+        if (tc == etc) {  // position e receives the leaving variable's column
           const double rl = sm.prow[e];
-#define LPB_COLFIX(x)                                                            \
-  case x:                                                                        \
-    if constexpr ((x) < BC) {                                                    \
-      _Pragma("unroll") for (int ai = 0; ai < A; ++ai) T[ai][x] =                \
-          (tr + TR * ai == l) ? rl                                               \
-                              : __fma_rn(-sm.colE[par][tr + TR * ai], rl, 0.0);  \
-      if (leaving < 0) {                                                         \
-        d2[x] = neg_inf();                                                       \
-        if constexpr (TWO) d1[x] = neg_inf();                                    \
-      } else {                                                                   \
-        d2[x] = __fma_rn(f2, rl, 0.0);                                           \
-        if constexpr (TWO) { if (upd1) d1[x] = __fma_rn(f1, rl, 0.0); }          \
-      }                                                                          \
-    }                                                                            \
+#define LPB_COLFIX(x)                                                              \
+  case x:                                                                          \
+    if constexpr ((x) < BC) {                                                      \
+      _Pragma("unroll") for (int ai = 0; ai < A; ++ai) T[ai][x] =                  \
+          (tr + TR * ai == l) ? rl : __fma_rn(-colE[tr + TR * ai], rl, 0.0);       \
+      if (leaving < 0) {                                                           \
+        d2[x] = neg_inf();                                                         \
+        if constexpr (TWO) d1[x] = neg_inf();                                      \
+      } else {                                                                     \
+        d2[x] = __fma_rn(f2, rl, 0.0);                                             \
+        if constexpr (TWO) { if (upd1) d1[x] = __fma_rn(f1, rl, 0.0); }            \
+      }                                                                            \
+    }                                                                              \
     break;
           switch (be) { LPB_CASES(LPB_COLFIX) default: break; }
 #undef LPB_COLFIX
@@ -440,7 +495,7 @@ __global__ void __launch_bounds__(TR * TC * G, MINB) simplex_reg_kernel(SimplexA
       par ^= 1;
       if (drive) {
         ++it1;
-        gsync<NT>(g);  // the next drive-out scan reads bkey
+        gsync<NT>();  // the next drive-out scan reads bkey
       } else {
         if (phase == 1) ++it1; else ++it2;
         stall = (theta > 0.0) ? 0 : stall + 1;
@@ -448,7 +503,7 @@ __global__ void __launch_bounds__(TR * TC * G, MINB) simplex_reg_kernel(SimplexA
     }
 
     // ---- extract (R10) ----
-    gsync<NT>(g);
+    gsync<NT>();
     if (st == ST_OPTIMAL && pend) {  // apply the last pending RHS update
       const double prr = sm.prow_rhs;
       for (int i = tid; i < m; i += NT)
@@ -459,21 +514,20 @@ __global__ void __launch_bounds__(TR * TC * G, MINB) simplex_reg_kernel(SimplexA
       a.iters[2 * lp] = it1;
       a.iters[2 * lp + 1] = it2;
       a.obj[lp] = (st == ST_OPTIMAL) ? -z2
-                : (st == ST_UNBOUNDED) ? __longlong_as_double(0x7ff0000000000000ll)
-                : (st == ST_INFEASIBLE) ? neg_inf() : __longlong_as_double(0x7ff8000000000000ll);
+                : (st == ST_UNBOUNDED) ? pos_inf() : (st == ST_INFEASIBLE) ? neg_inf() : qnan();
     }
     if (a.x) {
       double* xk = a.x + lp * (int64_t)n;
-      const double fill = (st == ST_OPTIMAL) ? 0.0 : __longlong_as_double(0x7ff8000000000000ll);
+      const double fill = (st == ST_OPTIMAL) ? 0.0 : qnan();
       for (int j = tid; j < n; j += NT) xk[j] = fill;
-      gsync<NT>(g);
+      gsync<NT>();
       if (st == ST_OPTIMAL)
         for (int i = tid; i < m; i += NT) {
           const int key = sm.bkey[i];
           if (key >= 0 && key < n) xk[key] = sm.rhs[i];
         }
     }
-    gsync<NT>(g);
+    gsync<NT>();
   }
 }
 
@@ -481,36 +535,35 @@ struct RegCfg {
   int rcap, ccap, two, id;
 };
 
-// Instantiated layouts: {id, TR, TC, A, BC, TWO, MINB, G}
+// Instantiated layouts: {id, TR, TC, A, BC, TWO, MINB}
 #define LPB_REG_CONFIGS(X)           \
-  X(0, 8, 4, 1, 3, true, 16, 1)      \
-  X(1, 8, 4, 2, 6, true, 12, 1)      \
-  X(2, 8, 4, 4, 8, true, 6, 1)       \
-  X(3, 16, 8, 4, 8, true, 2, 1)      \
-  X(4, 16, 16, 7, 7, false, 1, 1)    \
-  X(5, 16, 16, 7, 7, true, 1, 1)     \
-  X(6, 8, 16, 13, 7, false, 2, 1)
+  X(0, 8, 4, 1, 3, true, 16)         \
+  X(1, 8, 4, 2, 6, true, 12)         \
+  X(2, 8, 4, 4, 8, true, 6)          \
+  X(3, 16, 8, 4, 8, true, 2)         \
+  X(4, 16, 16, 7, 7, false, 1)       \
+  X(5, 16, 16, 7, 7, true, 1)        \
+  X(6, 8, 16, 13, 7, false, 2)
 
-template <int TR, int TC, int A, int BC, bool TWO, int MINB, int G>
+template <int TR, int TC, int A, int BC, bool TWO, int MINB>
 cudaError_t launch_one(const SimplexArgs& a, int grid_override, cudaStream_t s, int* ctas) {
-  auto kern = simplex_reg_kernel<TR, TC, A, BC, TWO, MINB, G>;
+  auto kern = simplex_reg_kernel<TR, TC, A, BC, TWO, MINB>;
   int per_sm = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TR * TC * G, 0);
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TR * TC, 0);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) per_sm = 1;
   int64_t grid = (int64_t)per_sm * device_sm_count();
-  const int64_t need = (a.batch + G - 1) / G;
-  if (grid > need) grid = need;
+  if (grid > a.batch) grid = a.batch;
   if (grid_override > 0) grid = grid_override;
   if (ctas) *ctas = (int)grid;
-  kern<<<(unsigned)grid, TR * TC * G, 0, s>>>(a);
+  kern<<<(unsigned)grid, TR * TC, 0, s>>>(a);
   return cudaGetLastError();
 }
 
 }  // namespace
 
 static const RegCfg kCfgs[] = {
-#define X(id, TR, TC, A, BC, TWO, MINB, G) {TR * A, TC * BC, TWO ? 1 : 0, id},
+#define X(id, TR, TC, A, BC, TWO, MINB) {TR * A, TC * BC, TWO ? 1 : 0, id},
     LPB_REG_CONFIGS(X)
 #undef X
 };
@@ -535,8 +588,8 @@ bool reg_fits(int m, int n, int kmax) { return pick_cfg(m, n, kmax) >= 0; }
 cudaError_t launch_simplex_reg(const SimplexArgs& a, int grid_override, cudaStream_t s,
                                int* ctas_out) {
   switch (pick_cfg(a.m, a.n, a.kmax)) {
-#define X(id, TR, TC, A, BC, TWO, MINB, G) \
-  case id: return launch_one<TR, TC, A, BC, TWO, MINB, G>(a, grid_override, s, ctas_out);
+#define X(id, TR, TC, A, BC, TWO, MINB) \
+  case id: return launch_one<TR, TC, A, BC, TWO, MINB>(a, grid_override, s, ctas_out);
     LPB_REG_CONFIGS(X)
 #undef X
     default: return cudaErrorInvalidValue;
