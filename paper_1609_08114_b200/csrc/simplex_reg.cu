@@ -14,8 +14,9 @@
 //     lazily, each row by exactly one lane), and the warp argmin goes to a per-warp partial
 //     -> barrier 1 -> every warp reduces the partials;
 //   * Step 3: the owners of row l publish prow = row / PE -> barrier 2 ->
-//     every thread applies T_ip = fma(-f_i, prow_p, T_ip) to its registers (A*BC DFMAs with
-//     no per-element branch), then row l and position e are fixed up.
+//     every thread applies T_ip = fma(f_i, prow_p, T_ip) to its registers (A*BC DFMAs with
+//     no per-element branch).  Row l and position e were zeroed when they were read, so the
+//     same fma produces the pivot row (f_l = 1) and the leaving variable's column.
 // Reductions use order-preserving integer keys and the sm_100 REDUX (__reduce_*_sync)
 // instructions: (value, tie key) argmax/argmin in three warp-wide REDUX steps.
 // All arithmetic matches oracle/lpb_oracle.c bit for bit (IEEE __ddiv_rn, explicit
@@ -193,10 +194,14 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
         T[ai][b] = v;
       }
     }
+    // alive: bit b set <=> my position tc + TC*b holds a live nonbasic variable (not padding,
+    // not a dead artificial); replaces per-position variable lookups in Step 1
+    unsigned alive = 0u;
 #pragma unroll
     for (int b = 0; b < BC; ++b) {
       const int p = tc + TC * b;
-      d2[b] = (p < n) ? __ldg(ck + p) : (p < npos ? 0.0 : neg_inf());
+      d2[b] = (p < n) ? __ldg(ck + p) : 0.0;
+      alive |= (p < npos && st < 0) ? (1u << b) : 0u;
     }
     double z2 = 0.0, z1 = 0.0;
     if constexpr (TWO) {
@@ -219,12 +224,12 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
 #pragma unroll
         for (int b = 0; b < BC; ++b) {
           const int p = tc + TC * b;
-          d1[b] = (p < npos) ? sm.prow[p] : neg_inf();
+          d1[b] = (p < npos) ? sm.prow[p] : 0.0;
         }
         for (int t = 0; t < k; ++t) z1 = __dadd_rn(z1, sm.rhs[sm.negrows[t]]);
       } else {
 #pragma unroll
-        for (int b = 0; b < BC; ++b) d1[b] = neg_inf();
+        for (int b = 0; b < BC; ++b) d1[b] = 0.0;
       }
     }
     gsync<NT>();
@@ -259,7 +264,7 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
 #pragma unroll
             for (int ai = 1; ai < A; ++ai) v = (ai == al) ? T[ai][b] : v;
             v = fabs(v);
-            if (d2[b] != neg_inf() && v > a.eps_piv) {  // live position
+            if (((alive >> b) & 1u) && v > a.eps_piv) {  // live position
               const int p = tc + TC * b;
               const unsigned var = (unsigned)sm.nbvar[p];
               if (!val || v > bv || (v == bv && var < bvar)) {
@@ -296,7 +301,7 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
 #pragma unroll
           for (int b = 0; b < BC; ++b) {
             const double v = p1 ? d1[TWO ? b : 0] : d2[b];
-            const bool take = v > bv;  // first maximum: lowest b on ties (fixed below)
+            const bool take = ((alive >> b) & 1u) && v > bv;  // first max: lowest b on ties
             bv = take ? v : bv;
             bb = take ? b : bb;
           }
@@ -305,7 +310,7 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
 #pragma unroll
           for (int b = 0; b < BC; ++b) {
             const double v = p1 ? d1[TWO ? b : 0] : d2[b];
-            tie |= (b != bb) && (v == bv);
+            tie |= ((alive >> b) & 1u) && (b != bb) && (v == bv);
           }
           bvar = val ? (unsigned)sm.nbvar[tc + TC * bb] : 0u;
           if (__any_sync(FULL, val && tie)) {  // rare: exact tie inside a thread -> var index
@@ -314,7 +319,7 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
               for (int b = 0; b < BC; ++b) {
                 const double v = p1 ? d1[TWO ? b : 0] : d2[b];
                 const unsigned var = (unsigned)sm.nbvar[tc + TC * b];
-                if (v == bv && var < bvar) {
+                if (((alive >> b) & 1u) && v == bv && var < bvar) {
                   bvar = var;
                   bb = b;
                 }
@@ -327,7 +332,7 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
 #pragma unroll
           for (int b = 0; b < BC; ++b) {
             const double v = p1 ? d1[TWO ? b : 0] : d2[b];
-            if (v > a.eps_enter) {
+            if (((alive >> b) & 1u) && v > a.eps_enter) {
               const unsigned var = (unsigned)sm.nbvar[tc + TC * b];
               if (var < bvar) {
                 bvar = var;
@@ -358,11 +363,16 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
 #define LPB_PUB(x)                                                                    \
   case x:                                                                             \
     if constexpr ((x) < BC) {                                                         \
-      _Pragma("unroll") for (int ai = 0; ai < A; ++ai) colE[tr + TR * ai] = T[ai][x]; \
+      _Pragma("unroll") for (int ai = 0; ai < A; ++ai) {                             \
+        colE[tr + TR * ai] = T[ai][x];                                                \
+        T[ai][x] = 0.0;                                                               \
+      }                                                                               \
       if (tr == 0) {                                                                  \
         sm.fobj[par][0] = d2[x];                                                      \
         if constexpr (TWO) sm.fobj[par][1] = d1[x];                                   \
       }                                                                               \
+      d2[x] = 0.0;                                                                    \
+      if constexpr (TWO) d1[x] = 0.0;                                                 \
     }                                                                                 \
     break;
         switch (be) { LPB_CASES(LPB_PUB) default: break; }
@@ -426,6 +436,7 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
       _Pragma("unroll") for (int b = 0; b < BC; ++b) {                              \
         const int p = tc + TC * b;                                                  \
         sm.prow[p] = __ddiv_rn(p == e ? 1.0 : T[x][b], pe);                         \
+        T[x][b] = 0.0;                                                              \
       }                                                                             \
     }                                                                               \
     break;
@@ -454,41 +465,16 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
         if constexpr (TWO) {
           if (upd1) z1 = __fma_rn(f1, prr, z1);
         }
+        // Row l and position e were zeroed when they were read (Step 2a / Step 3), so one
+        // fma per element yields the pivot row (f_l = 1: fma(1, prow, 0) = prow) and the
+        // leaving variable's column (fma(-f_i, rl, 0)) without any per-element branch.
 #pragma unroll
         for (int ai = 0; ai < A; ++ai) {
-          const double fi = -colE[tr + TR * ai];
+          const double fi = (tr + TR * ai == l) ? 1.0 : -colE[tr + TR * ai];
 #pragma unroll
           for (int b = 0; b < BC; ++b) T[ai][b] = __fma_rn(fi, pv[b], T[ai][b]);
         }
-        if (tr == ltr) {  // row l becomes the pivot row
-#define LPB_ROWFIX(x)                                                                  \
-  case x:                                                                              \
-    if constexpr ((x) < A) {                                                           \
-      _Pragma("unroll") for (int b = 0; b < BC; ++b) T[x][b] = pv[b];                  \
-    }                                                                                  \
-    break;
-          switch (al) { LPB_CASES(LPB_ROWFIX) default: break; }
-#undef LPB_ROWFIX
-        }
-        if (tc == etc) {  // position e receives the leaving variable's column
-          const double rl = sm.prow[e];
-#define LPB_COLFIX(x)                                                              \
-  case x:                                                                          \
-    if constexpr ((x) < BC) {                                                      \
-      _Pragma("unroll") for (int ai = 0; ai < A; ++ai) T[ai][x] =                  \
-          (tr + TR * ai == l) ? rl : __fma_rn(-colE[tr + TR * ai], rl, 0.0);       \
-      if (leaving < 0) {                                                           \
-        d2[x] = neg_inf();                                                         \
-        if constexpr (TWO) d1[x] = neg_inf();                                      \
-      } else {                                                                     \
-        d2[x] = __fma_rn(f2, rl, 0.0);                                             \
-        if constexpr (TWO) { if (upd1) d1[x] = __fma_rn(f1, rl, 0.0); }            \
-      }                                                                            \
-    }                                                                              \
-    break;
-          switch (be) { LPB_CASES(LPB_COLFIX) default: break; }
-#undef LPB_COLFIX
-        }
+        if (tc == etc && leaving < 0) alive &= ~(1u << be);  // an artificial left: dead
       }
       pend = true;
       l_prev = l;
