@@ -1,0 +1,23 @@
+/*
+ * lpb_selftest.h — diagnostic entry points of liblpb.so (not part of the solver API).
+ *
+ * lpb_selftest_div: checks the kernels' branch-free fp64 division (csrc/lpb_fp64.cuh) against
+ * the IEEE round-to-nearest division (__ddiv_rn) on n device-resident operand pairs.
+ *   a, b   : device pointers, n doubles each (b != 0, finite)
+ *   q      : device pointer, n doubles: the fast-path quotient (or the __ddiv_rn fallback
+ *            the kernels take when the fast path reports its range is exceeded)
+ *   out    : host pointer to 2 int64: [0] = #quotients whose bits differ from __ddiv_rn,
+ *            [1] = #pairs that needed the fallback
+ * Returns LPB_OK or LPB_ECUDA.  Synchronizes the current device.
+ */
+#ifndef LPB_SELFTEST_H_
+#define LPB_SELFTEST_H_
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+int lpb_selftest_div(const double* a, const double* b, double* q, int64_t n, int64_t* out);
+#ifdef __cplusplus
+}
+#endif
+#endif

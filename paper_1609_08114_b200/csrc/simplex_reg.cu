@@ -24,6 +24,7 @@
 #include <climits>
 #include <cstdlib>
 
+#include "lpb_fp64.cuh"
 #include "lpb_internal.cuh"
 
 namespace lpb {
@@ -395,7 +396,9 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
           if (!drive) {
             const double v = colE[i];
             val = v > a.eps_piv;
-            ratio = __ddiv_rn(r, val ? v : 1.0);
+            bool slow;
+            ratio = div_fast(r, val ? v : 1.0, slow);
+            if (slow) ratio = __ddiv_rn(r, val ? v : 1.0);  // rare: outside the fast range
             tie = bland ? sm.bkey[i] : i;
           }
         }
@@ -433,16 +436,31 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
 #define LPB_PROW(x)                                                                 \
   case x:                                                                           \
     if constexpr ((x) < A) {                                                        \
+      bool slow_any = false;                                                        \
+      double q[BC];                                                                 \
       _Pragma("unroll") for (int b = 0; b < BC; ++b) {                              \
         const int p = tc + TC * b;                                                  \
-        sm.prow[p] = __ddiv_rn(p == e ? 1.0 : T[x][b], pe);                         \
+        bool sl;                                                                    \
+        q[b] = div_fast(p == e ? 1.0 : T[x][b], pe, sl);                            \
+        slow_any |= sl;                                                             \
+      }                                                                             \
+      if (slow_any) {                                                               \
+        _Pragma("unroll") for (int b = 0; b < BC; ++b)                              \
+          q[b] = __ddiv_rn(tc + TC * b == e ? 1.0 : T[x][b], pe);                   \
+      }                                                                             \
+      _Pragma("unroll") for (int b = 0; b < BC; ++b) {                              \
+        sm.prow[tc + TC * b] = q[b];                                                \
         T[x][b] = 0.0;                                                              \
       }                                                                             \
     }                                                                               \
     break;
         switch (al) { LPB_CASES(LPB_PROW) default: break; }
 #undef LPB_PROW
-        if (tc == 0) sm.prow_rhs = __ddiv_rn(sm.rhs[l], pe);
+        if (tc == 0) {
+          bool sl;
+          const double q = div_fast(sm.rhs[l], pe, sl);
+          sm.prow_rhs = sl ? __ddiv_rn(sm.rhs[l], pe) : q;
+        }
       }
       gsync<NT>();  // barrier 2
       {

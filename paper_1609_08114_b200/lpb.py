@@ -63,6 +63,8 @@ _lib.lpb_last_launch_info.argtypes = [P, ctypes.POINTER(ctypes.c_int32),
 _lib.lpb_destroy.argtypes = [P]
 _lib.lpb_strerror.argtypes = [ctypes.c_int]
 _lib.lpb_strerror.restype = ctypes.c_char_p
+_lib.lpb_selftest_div.argtypes = [P, P, P, ctypes.c_int64, ctypes.POINTER(ctypes.c_int64)]
+_lib.lpb_selftest_div.restype = ctypes.c_int
 _lib.lpb_last_error.argtypes = [P]
 _lib.lpb_last_error.restype = ctypes.c_char_p
 for _f in ("lpb_default_options", "lpb_create", "lpb_solve_batch", "lpb_solve_batch_into",

@@ -20,7 +20,7 @@ def lib():
 
 
 def _declared():
-    src = open(HDR).read()
+    src = open(HDR).read() + open(os.path.join(ROOT, "include", "lpb_selftest.h")).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
     return sorted(set(re.findall(r"\b(lpb_[a-z_]+)\s*\(", src)))
 
