@@ -1,6 +1,7 @@
 """Build liblpb.so in-tree with nvcc for sm_100a (B200).
 
-    python -m paper_1609_08114_b200.build [--verbose]
+    python paper_1609_08114_b200/build.py [--verbose] [--force]
+(run it by path: importing the package first would load a possibly stale liblpb.so)
 
 Every .cu under csrc/ is compiled to an object with
     -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -fmad=false

@@ -19,7 +19,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "liblpb.so")
 if not os.path.exists(LIB_PATH):
-    raise ImportError(f"{LIB_PATH} is not built: run `python -m paper_1609_08114_b200.build` "
+    raise ImportError(f"{LIB_PATH} is not built: run `python paper_1609_08114_b200/build.py` "
                       "(no CPU fallback exists)")
 _lib = ctypes.CDLL(LIB_PATH)
 

@@ -14,8 +14,9 @@ LIB = os.path.join(ROOT, "paper_1609_08114_b200", "liblpb.so")
 @pytest.fixture(scope="module")
 def lib():
     if not os.path.exists(LIB):
-        from paper_1609_08114_b200 import build as b
-        b.build()
+        import subprocess
+        import sys
+        subprocess.check_call([sys.executable, os.path.join(ROOT, "paper_1609_08114_b200", "build.py")])
     return ctypes.CDLL(LIB)
 
 
