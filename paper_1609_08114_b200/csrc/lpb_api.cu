@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <new>
@@ -232,6 +233,11 @@ static void fill_args(const lpb_ctx* c, SimplexArgs& a, int64_t lp0, int64_t cnt
   a.bland_K = c->opt.bland_after == 0 ? n + m : c->opt.bland_after;
   a.kmax = kmax;
   a.ticket = ticket;
+  // bulk-copy prefetch needs every LP's A to start 16-byte aligned and be a multiple of 16
+  // bytes (m*n even), and to fit SMEM next to the register layouts' small SMEM state
+  const int64_t bytes = (int64_t)m * n * 8;
+  a.prefetch = (((uintptr_t)A & 15) == 0 && (m * (int64_t)n) % 2 == 0 && bytes <= 100 * 1024 &&
+                getenv("LPB_NO_PREFETCH") == nullptr) ? 1 : 0;
 }
 
 // Enqueue the general-LP kernels for one resident chunk on stream s.

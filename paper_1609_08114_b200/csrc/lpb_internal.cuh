@@ -30,6 +30,7 @@ struct SimplexArgs {
   int bland_K;      // > 0: Bland mode after K consecutive degenerate pivots; <= 0: never
   int kmax;         // layout capacity for artificial (b_i < 0) rows
   int* ticket;      // persistent-scheduler counter, zeroed before each launch
+  int prefetch;     // R class: A (m*n*8 bytes, 16-B aligned per LP) is bulk-prefetched to SMEM
 };
 
 struct HyperboxArgs {

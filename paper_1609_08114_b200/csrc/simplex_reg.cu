@@ -24,6 +24,7 @@
 #include <climits>
 #include <cstdlib>
 
+#include "lpb_async.cuh"
 #include "lpb_fp64.cuh"
 #include "lpb_internal.cuh"
 
@@ -97,6 +98,7 @@ template <int TR, int TC, int A, int BC>
 struct RegSmem {
   static constexpr int RCAP = TR * A, CCAP = TC * BC, NWARP = (TR * TC) / 32;
   double colE[2][RCAP];  // pivot column (constraint rows), double-buffered by pivot parity
+  double fcol[2][RCAP];  // update multipliers: -colE, and +1 for the pivot row
   double fobj[2][2];     // pivot-column entries of the phase-II / phase-I rows
   double rhs[RCAP];      // RHS column (lazily updated)
   double prow[CCAP];     // new pivot row (positions); scratch for the phase-I row at build
@@ -106,6 +108,7 @@ struct RegSmem {
   int wcount[NWARP];
   Part part[NWARP];      // ratio-test partial per warp
   double prow_rhs;
+  uint64_t mbar;         // completes when the prefetched A of LP `lp` has landed
   int lp;
   int leaving;
 };
@@ -127,13 +130,27 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
   double T[A][BC];
   double d2[BC];
   double d1[TWO ? BC : 1];
+  // the next LP's A is prefetched into SMEM (one bulk async copy) while this LP is solved
+  extern __shared__ __align__(16) double abuf[];
+  const bool pf = a.prefetch != 0;
+  const uint32_t abytes = (uint32_t)((int64_t)m * n * 8);
+  uint32_t mphase = 0;
+  if (tid == 0) {
+    mbar_init(&sm.mbar, 1);
+    const int t = atomicAdd(a.ticket, 1);
+    sm.lp = t;
+    if (pf && t < a.batch) bulk_load(abuf, a.A + (int64_t)t * m * n, abytes, &sm.mbar);
+  }
+  gsync<NT>();
 
   for (;;) {
-    if (tid == 0) sm.lp = atomicAdd(a.ticket, 1);
-    gsync<NT>();
     const int64_t lp = sm.lp;
     if (lp >= a.batch) break;
-    const double* __restrict__ Ak = a.A + lp * (int64_t)m * n;
+    if (pf) {
+      mbar_wait(&sm.mbar, mphase);
+      mphase ^= 1u;
+    }
+    const double* __restrict__ Ak = pf ? abuf : a.A + lp * (int64_t)m * n;
     const double* __restrict__ bk = a.b + lp * (int64_t)m;
     const double* __restrict__ ck = a.c + lp * (int64_t)n;
 
@@ -186,7 +203,7 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
         double v = 0.0;
         if (rowok && p < npos) {
           if (p < n) {
-            v = __ldg(Ak + (int64_t)i * n + p);
+            v = Ak[i * n + p];
             v = neg ? -v : v;
           } else {
             v = (i == sm.negrows[p - n]) ? -1.0 : (neg ? -0.0 : 0.0);
@@ -195,14 +212,12 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
         T[ai][b] = v;
       }
     }
-    // alive: bit b set <=> my position tc + TC*b holds a live nonbasic variable (not padding,
-    // not a dead artificial); replaces per-position variable lookups in Step 1
-    unsigned alive = 0u;
+    // padding positions (and, later, dead artificial positions) hold -inf in the objective
+    // replicas: never a Step-1 candidate, and fma(f, p, -inf) keeps them -inf
 #pragma unroll
     for (int b = 0; b < BC; ++b) {
       const int p = tc + TC * b;
-      d2[b] = (p < n) ? __ldg(ck + p) : 0.0;
-      alive |= (p < npos && st < 0) ? (1u << b) : 0u;
+      d2[b] = (p < n) ? __ldg(ck + p) : (p < npos ? 0.0 : neg_inf());
     }
     double z2 = 0.0, z1 = 0.0;
     if constexpr (TWO) {
@@ -214,7 +229,7 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
             double acc = 0.0;
             for (int t = 0; t < k; ++t) {
               const int r = sm.negrows[t];
-              const double v = (p < n) ? -__ldg(Ak + (int64_t)r * n + p)
+              const double v = (p < n) ? -Ak[r * n + p]
                                        : ((r == sm.negrows[p - n]) ? -1.0 : -0.0);
               acc = __dadd_rn(acc, v);
             }
@@ -225,15 +240,20 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
 #pragma unroll
         for (int b = 0; b < BC; ++b) {
           const int p = tc + TC * b;
-          d1[b] = (p < npos) ? sm.prow[p] : 0.0;
+          d1[b] = (p < npos) ? sm.prow[p] : neg_inf();
         }
         for (int t = 0; t < k; ++t) z1 = __dadd_rn(z1, sm.rhs[sm.negrows[t]]);
       } else {
 #pragma unroll
-        for (int b = 0; b < BC; ++b) d1[b] = 0.0;
+        for (int b = 0; b < BC; ++b) d1[b] = neg_inf();
       }
     }
-    gsync<NT>();
+    gsync<NT>();  // A has been consumed: the buffer may be refilled with the next LP
+    if (tid == 0) {
+      const int t = atomicAdd(a.ticket, 1);
+      sm.lp = t;
+      if (pf && t < a.batch) bulk_load(abuf, a.A + (int64_t)t * m * n, abytes, &sm.mbar);
+    }
 
     // ---- Steps 1-3, two phases ----
     int it1 = 0, it2 = 0, stall = 0, phase = (TWO && k > 0) ? 1 : 2;
@@ -265,7 +285,7 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
 #pragma unroll
             for (int ai = 1; ai < A; ++ai) v = (ai == al) ? T[ai][b] : v;
             v = fabs(v);
-            if (((alive >> b) & 1u) && v > a.eps_piv) {  // live position
+            if (d2[b] != neg_inf() && v > a.eps_piv) {  // live position
               const int p = tc + TC * b;
               const unsigned var = (unsigned)sm.nbvar[p];
               if (!val || v > bv || (v == bv && var < bvar)) {
@@ -302,7 +322,7 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
 #pragma unroll
           for (int b = 0; b < BC; ++b) {
             const double v = p1 ? d1[TWO ? b : 0] : d2[b];
-            const bool take = ((alive >> b) & 1u) && v > bv;  // first max: lowest b on ties
+            const bool take = v > bv;  // first maximum: lowest b on ties (fixed below)
             bv = take ? v : bv;
             bb = take ? b : bb;
           }
@@ -311,7 +331,7 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
 #pragma unroll
           for (int b = 0; b < BC; ++b) {
             const double v = p1 ? d1[TWO ? b : 0] : d2[b];
-            tie |= ((alive >> b) & 1u) && (b != bb) && (v == bv);
+            tie |= (b != bb) && (v == bv);
           }
           bvar = val ? (unsigned)sm.nbvar[tc + TC * bb] : 0u;
           if (__any_sync(FULL, val && tie)) {  // rare: exact tie inside a thread -> var index
@@ -320,7 +340,7 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
               for (int b = 0; b < BC; ++b) {
                 const double v = p1 ? d1[TWO ? b : 0] : d2[b];
                 const unsigned var = (unsigned)sm.nbvar[tc + TC * b];
-                if (((alive >> b) & 1u) && v == bv && var < bvar) {
+                if (v == bv && var < bvar) {
                   bvar = var;
                   bb = b;
                 }
@@ -333,7 +353,7 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
 #pragma unroll
           for (int b = 0; b < BC; ++b) {
             const double v = p1 ? d1[TWO ? b : 0] : d2[b];
-            if (((alive >> b) & 1u) && v > a.eps_enter) {
+            if (v > a.eps_enter) {
               const unsigned var = (unsigned)sm.nbvar[tc + TC * b];
               if (var < bvar) {
                 bvar = var;
@@ -380,26 +400,30 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
 #undef LPB_PUB
       }
       __syncwarp();
-      // Step 2b: lane-parallel lazy RHS update + ratio test over the warp's rows
+      // Step 2b: lane-parallel lazy RHS update + ratio test over the warp's rows; each lane
+      // also writes its row's update multiplier f_i = -colE_i
       {
         bool val = false;
         double ratio = 0.0;
         int tie = INT_MAX;
         const int i = rrow;
-        if (rlane && i < m) {
-          double r = sm.rhs[i];
-          if (pend) {
-            const double prr = sm.prow_rhs;
-            r = (i == l_prev) ? prr : __fma_rn(-sm.colE[par ^ 1][i], prr, r);
-            sm.rhs[i] = r;
-          }
-          if (!drive) {
-            const double v = colE[i];
-            val = v > a.eps_piv;
-            bool slow;
-            ratio = div_fast(r, val ? v : 1.0, slow);
-            if (slow) ratio = __ddiv_rn(r, val ? v : 1.0);  // rare: outside the fast range
-            tie = bland ? sm.bkey[i] : i;
+        if (rlane) {
+          const double v = colE[i];
+          sm.fcol[par][i] = -v;
+          if (i < m) {
+            double r = sm.rhs[i];
+            if (pend) {
+              const double prr = sm.prow_rhs;
+              r = (i == l_prev) ? prr : __fma_rn(sm.fcol[par ^ 1][i], prr, r);
+              sm.rhs[i] = r;
+            }
+            if (!drive) {
+              val = v > a.eps_piv;
+              bool slow;
+              ratio = div_fast(r, val ? v : 1.0, slow);
+              if (slow) ratio = __ddiv_rn(r, val ? v : 1.0);  // rare: outside the fast range
+              tie = bland ? sm.bkey[i] : i;
+            }
           }
         }
         if (!drive) {
@@ -430,6 +454,7 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
         sm.bkey[l] = evar;
         sm.nbvar[e] = lv >= 0 ? lv : DEADV;
         sm.leaving = lv;
+        sm.fcol[par][l] = 1.0;  // the pivot row: fma(1, prow, 0) = prow
       }
       const int ltr = l % TR, al = l / TR;
       if (tr == ltr) {
@@ -488,11 +513,21 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
         // leaving variable's column (fma(-f_i, rl, 0)) without any per-element branch.
 #pragma unroll
         for (int ai = 0; ai < A; ++ai) {
-          const double fi = (tr + TR * ai == l) ? 1.0 : -colE[tr + TR * ai];
+          const double fi = sm.fcol[par][tr + TR * ai];
 #pragma unroll
           for (int b = 0; b < BC; ++b) T[ai][b] = __fma_rn(fi, pv[b], T[ai][b]);
         }
-        if (tc == etc && leaving < 0) alive &= ~(1u << be);  // an artificial left: dead
+        if (leaving < 0 && tc == etc) {  // an artificial left: position e is dead (rare)
+#define LPB_DEAD(x)                            \
+  case x:                                      \
+    if constexpr ((x) < BC) {                  \
+      d2[x] = neg_inf();                       \
+      if constexpr (TWO) d1[x] = neg_inf();    \
+    }                                          \
+    break;
+          switch (be) { LPB_CASES(LPB_DEAD) default: break; }
+#undef LPB_DEAD
+        }
       }
       pend = true;
       l_prev = l;
@@ -511,7 +546,7 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
     if (st == ST_OPTIMAL && pend) {  // apply the last pending RHS update
       const double prr = sm.prow_rhs;
       for (int i = tid; i < m; i += NT)
-        sm.rhs[i] = (i == l_prev) ? prr : __fma_rn(-sm.colE[par ^ 1][i], prr, sm.rhs[i]);
+        sm.rhs[i] = (i == l_prev) ? prr : __fma_rn(sm.fcol[par ^ 1][i], prr, sm.rhs[i]);
     }
     if (tid == 0) {
       a.status[lp] = st;
@@ -552,15 +587,18 @@ struct RegCfg {
 template <int TR, int TC, int A, int BC, bool TWO, int MINB>
 cudaError_t launch_one(const SimplexArgs& a, int grid_override, cudaStream_t s, int* ctas) {
   auto kern = simplex_reg_kernel<TR, TC, A, BC, TWO, MINB>;
+  const size_t dsm = a.prefetch ? (size_t)a.m * a.n * 8 : 0;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm);
+  if (e != cudaSuccess) return e;
   int per_sm = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TR * TC, 0);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TR * TC, dsm);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) per_sm = 1;
   int64_t grid = (int64_t)per_sm * device_sm_count();
   if (grid > a.batch) grid = a.batch;
   if (grid_override > 0) grid = grid_override;
   if (ctas) *ctas = (int)grid;
-  kern<<<(unsigned)grid, TR * TC, 0, s>>>(a);
+  kern<<<(unsigned)grid, TR * TC, dsm, s>>>(a);
   return cudaGetLastError();
 }
 
