@@ -61,6 +61,7 @@ struct lpb_ctx {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   bool solved = false, last_nox = false, host_path = false;
   int last_launches = 0, last_class = 0;
+  long long* prof = nullptr;  // diagnostics: per-CTA phase counters (lpb_set_profile_buffer)
   char err[256] = {0};
 };
 
@@ -236,6 +237,7 @@ static void fill_args(const lpb_ctx* c, SimplexArgs& a, int64_t lp0, int64_t cnt
   // bulk-copy prefetch needs every LP's A to start 16-byte aligned and be a multiple of 16
   // bytes (m*n even), and to fit SMEM next to the register layouts' small SMEM state
   const int64_t bytes = (int64_t)m * n * 8;
+  a.prof = c->prof;
   a.prefetch = (((uintptr_t)A & 15) == 0 && (m * (int64_t)n) % 2 == 0 && bytes <= 100 * 1024 &&
                 getenv("LPB_NO_PREFETCH") == nullptr) ? 1 : 0;
 }
@@ -462,6 +464,12 @@ extern "C" int lpb_last_timing(lpb_ctx* c, double* solve_ms, double* e2e_ms) {
   LPB_CUDA(c, cudaEventElapsedTime(&ms, c->ev0, c->ev1));
   if (solve_ms) *solve_ms = c->host_path ? std::nan("") : (double)ms;
   if (e2e_ms) *e2e_ms = (double)ms;
+  return LPB_OK;
+}
+
+extern "C" int lpb_set_profile_buffer(lpb_ctx* c, long long* dev_buf) {
+  if (!c) return LPB_EINVAL;
+  c->prof = dev_buf;
   return LPB_OK;
 }
 

@@ -31,6 +31,7 @@ struct SimplexArgs {
   int kmax;         // layout capacity for artificial (b_i < 0) rows
   int* ticket;      // persistent-scheduler counter, zeroed before each launch
   int prefetch;     // R class: A (m*n*8 bytes, 16-B aligned per LP) is bulk-prefetched to SMEM
+  long long* prof;  // optional per-CTA phase cycle counters (diagnostics), normally null
 };
 
 struct HyperboxArgs {

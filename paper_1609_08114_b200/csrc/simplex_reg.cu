@@ -113,6 +113,15 @@ struct RegSmem {
   int leaving;
 };
 
+// Optional phase profiler (SimplexArgs::prof != nullptr): warp 0 of every CTA accumulates
+// clock64() deltas per pivot phase into prof[blockIdx.x * 8 + phase].  Off by default.
+#define LPB_PROF_MARK(ph)                                                 \
+  if (prof_on) {                                                          \
+    const long long t_ = clock64();                                       \
+    pacc[ph] += t_ - pt;                                                  \
+    pt = t_;                                                              \
+  }
+
 template <int TR, int TC, int A, int BC, bool TWO, int MINB>
 __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs a) {
   constexpr int NT = TR * TC, RCAP = TR * A, CCAP = TC * BC, NWARP = NT / 32;
@@ -126,6 +135,9 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
   const int rrow = (w * RPW + lane % RPW) + TR * (lane / RPW);
   const bool rlane = lane < RPW * A;
   const int m = a.m, n = a.n;
+  const bool prof_on = a.prof != nullptr && w == 0;
+  long long pacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long pt = clock64();
 
   double T[A][BC];
   double d2[BC];
@@ -313,6 +325,7 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
         e = __shfl_sync(FULL, q.idx, ql);
         evar = __shfl_sync(FULL, q.tie, ql);
       } else {
+        LPB_PROF_MARK(7)
         // Step 1: entering position from the replicated objective row (warp-local)
         double bv = neg_inf();
         int bb = 0;
@@ -377,6 +390,7 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
         evar = (int)__shfl_sync(FULL, bvar, wl);
       }
 
+      LPB_PROF_MARK(0)
       // Step 2a: the owners of position e publish column e (+ objective-row entries)
       const int be = e / TC, etc = e - be * TC;
       double* colE = sm.colE[par];
@@ -400,6 +414,7 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
 #undef LPB_PUB
       }
       __syncwarp();
+      LPB_PROF_MARK(1)
       // Step 2b: lane-parallel lazy RHS update + ratio test over the warp's rows; each lane
       // also writes its row's update multiplier f_i = -colE_i
       {
@@ -437,7 +452,9 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
           if (lane == 0) sm.part[w] = pw;
         }
       }
+      LPB_PROF_MARK(2)
       gsync<NT>();  // barrier 1
+      LPB_PROF_MARK(3)
       double theta = 0.0;
       if (!drive) {  // Step 2c: argmin over the warp partials, in every warp
         const Part q = (lane < NWARP) ? sm.part[lane] : Part{0.0, INT_MAX, -1};
@@ -447,6 +464,7 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
         theta = __shfl_sync(FULL, q.v, ql);
       }
 
+      LPB_PROF_MARK(4)
       // Step 3: pivot row / PE by the owners of row l
       const double pe = colE[l];
       if (tid == 0) {
@@ -487,7 +505,9 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
           sm.prow_rhs = sl ? __ddiv_rn(sm.rhs[l], pe) : q;
         }
       }
+      LPB_PROF_MARK(5)
       gsync<NT>();  // barrier 2
+      LPB_PROF_MARK(6)
       {
         const double prr = sm.prow_rhs;
         const int leaving = sm.leaving;
@@ -568,6 +588,8 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
     }
     gsync<NT>();
   }
+  if (prof_on && lane == 0)
+    for (int q = 0; q < 8; ++q) atomicAdd((unsigned long long*)&a.prof[blockIdx.x * 8 + q], (unsigned long long)pacc[q]);
 }
 
 struct RegCfg {
