@@ -139,6 +139,11 @@ int lpb_sync(lpb_ctx* c);
  * copy for host-pointer solves (equal to solve_ms for device-pointer solves). */
 int lpb_last_timing(lpb_ctx* c, double* solve_ms, double* e2e_ms);
 
+/* Device-event duration of the last device-pointer solve's dominant kernel alone (the
+ * simplex or hyperbox kernel, without the size prepass).  Errors: LPB_ESTATE when the last
+ * solve was not a device-pointer solve. */
+int lpb_last_kernel_timing(lpb_ctx* c, double* kernel_ms);
+
 /* Number of kernel launches the last solve issued (for the bench's gpu_launches count),
  * and the size class it dispatched to (1 S, 2 M, 3 L, 4 R, 5 H). */
 int lpb_last_launch_info(lpb_ctx* c, int32_t* launches, int32_t* kernel_class);

@@ -228,3 +228,63 @@ def make_config(name: str, B: int | None = None):
         return hyperbox(Bv, cfg["n"], cfg["seed"])
     gen = {"G1": signed_bounded, "G2": twophase_signed}[cfg["gen"]]
     return gen(Bv, cfg["m"], cfg["n"], cfg["seed"])
+
+
+# ---- shards of a seeded batch (multi-GPU: each rank generates only its LPs) ----
+# numpy's PCG64 draws exactly one 64-bit output per uniform double, so the draws of LPs
+# [lo, hi) of an array drawn for the whole batch are reached with bit_generator.advance().
+
+class _ShardDraw:
+    def __init__(self, seed: int, B: int, lo: int, hi: int):
+        self.bg = np.random.PCG64(seed)
+        self.g = np.random.Generator(self.bg)
+        self.B, self.lo, self.hi = B, lo, hi
+
+    def uniform(self, low, high, per_lp: int, shape):
+        self.bg.advance(self.lo * per_lp)
+        out = self.g.uniform(low, high, size=(self.hi - self.lo,) + tuple(shape))
+        self.bg.advance((self.B - self.hi) * per_lp)
+        return out
+
+
+def signed_bounded_shard(B: int, m: int, n: int, seed: int, lo: int, hi: int):
+    """LPs [lo, hi) of signed_bounded(B, m, n, seed), bit-identical, without drawing the rest."""
+    d = _ShardDraw(seed, B, lo, hi)
+    A = d.uniform(-10.0, 10.0, m * n, (m, n))
+    A[:, 0, :] = d.uniform(1.0, 10.0, n, (n,))
+    b = d.uniform(1.0, 100.0, m, (m,))
+    c = d.uniform(-10.0, 10.0, n, (n,))
+    return A, b, c
+
+
+def twophase_signed_shard(B: int, m: int, n: int, seed: int, lo: int, hi: int):
+    """LPs [lo, hi) of twophase_signed(B, m, n, seed), bit-identical."""
+    d = _ShardDraw(seed, B, lo, hi)
+    kk = min(int(math.ceil(m / 4)), m - 1)
+    A = d.uniform(-10.0, 10.0, m * n, (m, n))
+    A[:, 0, :] = d.uniform(1.0, 10.0, n, (n,))
+    xs = d.uniform(0.0, 1.0, n, (n,))
+    slack = d.uniform(1.0, 100.0, m, (m,))
+    keys = d.uniform(0.0, 1.0, max(m - 1, 0), (max(m - 1, 0),))
+    cover = d.uniform(1.0, 10.0, max(kk, 0) * n, (max(kk, 0), n))
+    cover_slack = d.uniform(0.0, 1.0, max(kk, 0), (max(kk, 0),))
+    c = d.uniform(-10.0, 10.0, n, (n,))
+    b = np.maximum(np.einsum("bij,bj->bi", A, xs), 0.0) + slack
+    if kk > 0:
+        Bs = hi - lo
+        rows = 1 + np.argsort(keys, axis=1, kind="stable")[:, :kk]
+        bi = np.arange(Bs)[:, None]
+        A[bi, rows, :] = -cover
+        b[bi, rows] = np.einsum("bkj,bj->bk", -cover, xs) + cover_slack
+    return A, b, c
+
+
+def make_config_shard(name: str, B: int, lo: int, hi: int):
+    """LPs [lo, hi) of config `name` drawn for a batch of B (general configs are drawn
+    shard-locally; hyperbox directions use normals, so the batch is drawn and sliced)."""
+    cfg = CONFIGS[name]
+    if cfg["kind"] == "hyperbox":
+        lo_b, hi_b, dirs = hyperbox(B, cfg["n"], cfg["seed"])
+        return lo_b, hi_b, np.ascontiguousarray(dirs[lo:hi])
+    f = {"G1": signed_bounded_shard, "G2": twophase_signed_shard}[cfg["gen"]]
+    return f(B, cfg["m"], cfg["n"], cfg["seed"], lo, hi)

@@ -59,6 +59,8 @@ struct lpb_ctx {
   std::vector<cudaStream_t> chunk_streams;
   std::vector<cudaEvent_t> chunk_done;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaEvent_t kev0 = nullptr, kev1 = nullptr;  // around the dominant (solve) kernel
+  bool kev_valid = false;
   bool solved = false, last_nox = false, host_path = false;
   int last_launches = 0, last_class = 0;
   long long* prof = nullptr;  // diagnostics: per-CTA phase counters (lpb_set_profile_buffer)
@@ -161,6 +163,8 @@ extern "C" int lpb_create(lpb_ctx** out, int64_t batch, int32_t m, int32_t n, in
   if (e == cudaSuccess) e = cudaMallocHost(&c->h_kmax, sizeof(int));
   if (e == cudaSuccess) e = cudaEventCreate(&c->ev0);
   if (e == cudaSuccess) e = cudaEventCreate(&c->ev1);
+  if (e == cudaSuccess) e = cudaEventCreate(&c->kev0);
+  if (e == cudaSuccess) e = cudaEventCreate(&c->kev1);
   if (e != cudaSuccess) {
     const bool oom = (e == cudaErrorMemoryAllocation);
     set_cuda_err(c, e, "lpb_create");
@@ -189,6 +193,8 @@ extern "C" int lpb_destroy(lpb_ctx* c) {
   if (c->h_kmax) cudaFreeHost(c->h_kmax);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
+  if (c->kev0) cudaEventDestroy(c->kev0);
+  if (c->kev1) cudaEventDestroy(c->kev1);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   delete c;
   return LPB_OK;
@@ -268,10 +274,16 @@ static int run_general(lpb_ctx* c, cudaStream_t s, int64_t lp0, int64_t cnt, con
   fill_args(c, a, lp0, cnt, A, b, cv, nox, kmax, ticket);
   LPB_CUDA(c, cudaMemsetAsync(ticket, 0, sizeof(int), s));
   int ctas = 0;
+  const bool timed = (s == c->stream);
+  if (timed) LPB_CUDA(c, cudaEventRecord(c->kev0, s));
   if (klass == CLASS_R) {
     LPB_CUDA(c, launch_simplex_reg(a, c->opt.grid_ctas, s, &ctas));
   } else {
     LPB_CUDA(c, launch_simplex_block(cl, a, c->opt.grid_ctas, s, &ctas));
+  }
+  if (timed) {
+    LPB_CUDA(c, cudaEventRecord(c->kev1, s));
+    c->kev_valid = true;
   }
   *launches += 1;
   c->last_class = klass;
@@ -289,7 +301,13 @@ static int run_hyperbox(lpb_ctx* c, cudaStream_t s, int64_t lp0, int64_t cnt, co
   h.status = c->d_status + lp0;
   h.obj = c->d_obj + lp0;
   h.x = nox ? nullptr : c->d_x + lp0 * c->n;
+  const bool timed = (s == c->stream);
+  if (timed) LPB_CUDA(c, cudaEventRecord(c->kev0, s));
   LPB_CUDA(c, launch_hyperbox(h, s));
+  if (timed) {
+    LPB_CUDA(c, cudaEventRecord(c->kev1, s));
+    c->kev_valid = true;
+  }
   *launches += 1;
   c->last_class = CLASS_H;
   return LPB_OK;
@@ -328,6 +346,7 @@ static int solve_impl(lpb_ctx* c, const double* A, const double* b, const double
   if (o_x && nox) return LPB_EINVAL;
   LPB_CUDA(c, cudaSetDevice(c->device));
   c->solved = false;
+  c->kev_valid = false;
   c->last_launches = 0;
   c->last_nox = nox;
   const int64_t B = c->batch;
@@ -470,6 +489,17 @@ extern "C" int lpb_last_timing(lpb_ctx* c, double* solve_ms, double* e2e_ms) {
 extern "C" int lpb_set_profile_buffer(lpb_ctx* c, long long* dev_buf) {
   if (!c) return LPB_EINVAL;
   c->prof = dev_buf;
+  return LPB_OK;
+}
+
+extern "C" int lpb_last_kernel_timing(lpb_ctx* c, double* kernel_ms) {
+  if (!c || !kernel_ms) return LPB_EINVAL;
+  if (!c->solved || !c->kev_valid) return LPB_ESTATE;
+  LPB_CUDA(c, cudaSetDevice(c->device));
+  LPB_CUDA(c, cudaEventSynchronize(c->kev1));
+  float ms = 0.f;
+  LPB_CUDA(c, cudaEventElapsedTime(&ms, c->kev0, c->kev1));
+  *kernel_ms = (double)ms;
   return LPB_OK;
 }
 

@@ -58,6 +58,8 @@ _lib.lpb_result_device_ptrs.argtypes = [P, P, P, P, P]
 _lib.lpb_sync.argtypes = [P]
 _lib.lpb_last_timing.argtypes = [P, ctypes.POINTER(ctypes.c_double),
                                  ctypes.POINTER(ctypes.c_double)]
+_lib.lpb_last_kernel_timing.argtypes = [P, ctypes.POINTER(ctypes.c_double)]
+_lib.lpb_last_kernel_timing.restype = ctypes.c_int
 _lib.lpb_last_launch_info.argtypes = [P, ctypes.POINTER(ctypes.c_int32),
                                       ctypes.POINTER(ctypes.c_int32)]
 _lib.lpb_destroy.argtypes = [P]
@@ -199,6 +201,12 @@ class Solver:
         s, e = ctypes.c_double(), ctypes.c_double()
         _check(_lib.lpb_last_timing(self._ctx, ctypes.byref(s), ctypes.byref(e)), self._ctx)
         return s.value, e.value
+
+    def kernel_ms(self):
+        """Device time of the last device-pointer solve's dominant kernel."""
+        k = ctypes.c_double()
+        _check(_lib.lpb_last_kernel_timing(self._ctx, ctypes.byref(k)), self._ctx)
+        return k.value
 
     def launch_info(self):
         n, k = ctypes.c_int32(), ctypes.c_int32()

@@ -55,3 +55,15 @@ def test_config_table():
     assert lpgen.CONFIGS["cfg2"]["B"] == 50000 and lpgen.CONFIGS["cfg5"]["B"] == 6003000
     A, b, c = lpgen.make_config("cfg3", B=3)
     assert A.shape == (3, 200, 200) and np.all((b < 0).sum(axis=1) == 50)
+
+
+def test_shards_equal_slices_of_the_full_batch():
+    for gen, sh in ((lpgen.signed_bounded, lpgen.signed_bounded_shard),
+                    (lpgen.twophase_signed, lpgen.twophase_signed_shard)):
+        full = gen(23, 9, 7, 11)
+        for lo, hi in ((0, 5), (5, 23), (17, 18)):
+            part = sh(23, 9, 7, 11, lo, hi)
+            for f, p in zip(full, part):
+                assert np.array_equal(f[lo:hi], p)
+    lo_b, hi_b, d = lpgen.make_config_shard("cfg4", 5000, 100, 300)
+    assert np.array_equal(d, lpgen.hyperbox(5000, 5, 4)[2][100:300])
