@@ -123,14 +123,22 @@ def _hptr(a):
     return a.ctypes.data_as(ctypes.c_void_p)
 
 
+_PINNED = {}
+
+
 def pinned_empty(shape, dtype=np.float64) -> np.ndarray:
-    """A numpy view of page-locked host memory (torch pin_memory), for the host path."""
+    """A numpy view of page-locked host memory (torch pin_memory), for the host path.
+    The owning torch tensor is kept alive until ``pinned_release(array)``."""
     import torch
     tdt = {np.float64: torch.float64, np.int32: torch.int32}[np.dtype(dtype).type]
     t = torch.empty(shape, dtype=tdt, pin_memory=True)
     a = t.numpy()
-    a._pin_owner = t  # type: ignore[attr-defined]  (keep the torch storage alive)
+    _PINNED[a.ctypes.data] = t
     return a
+
+
+def pinned_release(a: np.ndarray) -> None:
+    _PINNED.pop(a.ctypes.data, None)
 
 
 class Solver:
