@@ -86,7 +86,8 @@ typedef struct {
   int32_t bland_after; /* 0 -> n+m consecutive degenerate pivots switch to Bland's rule;
                           < 0 -> never (pure Dantzig)                                         */
   int32_t device;      /* CUDA device ordinal; -1 -> the current device                       */
-  void* stream;        /* cudaStream_t to run on; NULL -> a stream owned by the context       */
+  void* stream;        /* cudaStream_t to run on (cudaStreamLegacy = 0x1 for the legacy default
+                          stream); NULL -> a non-blocking stream owned by the context          */
   int32_t n_chunks;    /* host-pointer pipeline depth; 0 -> 10 if batch > 100 else 1
                           (the paper's stream count)                            */
   int32_t kernel_class;/* 0 auto; 1 S (thread/LP), 2 M (block/LP), 3 L (2-CTA cluster/LP),

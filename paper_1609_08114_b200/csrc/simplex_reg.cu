@@ -602,9 +602,9 @@ struct RegCfg {
   X(1, 8, 4, 2, 6, true, 12)         \
   X(2, 8, 4, 4, 8, true, 6)          \
   X(3, 16, 8, 4, 8, true, 2)         \
+  X(6, 8, 16, 13, 7, false, 2)       \
   X(4, 16, 16, 7, 7, false, 1)       \
-  X(5, 16, 16, 7, 7, true, 1)        \
-  X(6, 8, 16, 13, 7, false, 2)
+  X(5, 16, 16, 7, 7, true, 1)
 
 template <int TR, int TC, int A, int BC, bool TWO, int MINB>
 cudaError_t launch_one(const SimplexArgs& a, int grid_override, cudaStream_t s, int* ctas) {

@@ -149,7 +149,9 @@ class Solver:
         if device is None:
             device = torch.cuda.current_device() if torch.cuda.is_available() else 0
         if stream is None and torch.cuda.is_available():
-            stream = torch.cuda.current_stream(device).cuda_stream
+            # torch's current stream; handle 0 is the legacy default stream, which the ABI
+            # must receive as cudaStreamLegacy (0x1) -- NULL would mean "own stream"
+            stream = torch.cuda.current_stream(device).cuda_stream or 0x1
         self.batch, self.m, self.n, self.kind = int(batch), int(m), int(n), kind
         self.device = device
         self.opts = default_options(device=int(device), stream=stream, **opts)

@@ -1,0 +1,25 @@
+#!/bin/bash
+# Runs on the GPU box: bench lines for every config + ncu evidence (launch lists, full captures).
+# Usage: bash scripts/profile_round.sh <tag>
+TAG=${1:-r01}
+OUT=gpurun_out/$TAG
+mkdir -p $OUT
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $OUT/gpu.txt
+for cf in cfg2 cfg1 cfg4 cfg5; do
+  timeout 900 python bench.py --config $cf > $OUT/bench_$cf.json 2> $OUT/bench_$cf.err
+done
+timeout 900 python bench.py --config cfg3 --steps 2 --warmup 1 --e2e-steps 1 > $OUT/bench_cfg3.json 2> $OUT/bench_cfg3.err
+timeout 300 python bench.py --impl reference --config cfg2 --steps 3 --warmup 1 > $OUT/ref_cfg2.json 2>&1
+# launch lists (cold-cache, serialised: compare shares, not absolutes)
+for cf in cfg2 cfg5 cfg1; do
+  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_$cf.csv \
+    python bench.py --config $cf --steps 2 --warmup 1 --e2e-steps 0 --no-cpu-baseline > /dev/null 2>&1
+done
+# full captures of the dominant kernels
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:simplex_reg -c 1 -o $OUT/full_cfg2 \
+  python bench.py --config cfg2 --steps 1 --warmup 0 --e2e-steps 0 --no-cpu-baseline > /dev/null 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:hyperbox -c 1 -o $OUT/full_cfg5 \
+  python bench.py --config cfg5 --steps 1 --warmup 0 --e2e-steps 0 --no-cpu-baseline > /dev/null 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:simplex_block -c 1 -o $OUT/full_cfg3 \
+  python scripts/prof_one.py cfg3:444 1 > /dev/null 2>&1
+ls -la $OUT

@@ -21,7 +21,8 @@ CLASSES = ["R", "M", "L"]
 
 def _reg_fits(m, n, k):
     # mirrors the instantiated register layouts in csrc/simplex_reg.cu (capacity m x (n+k))
-    caps = [(8, 12, 1), (16, 24, 1), (32, 32, 1), (64, 64, 1), (112, 112, 0), (112, 112, 1)]
+    caps = [(8, 12, 1), (16, 24, 1), (32, 32, 1), (64, 64, 1), (104, 112, 0), (112, 112, 0),
+            (112, 112, 1)]
     return any(m <= r and n + k <= c and (k == 0 or two) for r, c, two in caps)
 
 
