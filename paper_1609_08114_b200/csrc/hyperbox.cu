@@ -44,12 +44,25 @@ __global__ void __launch_bounds__(HB_NT) hyperbox_kernel(HyperboxArgs a) {
     const int total = rows * n;
     const double* __restrict__ src = a.l + lp0 * n;
     {
+      // batches of UNR independent streaming loads per thread before the SMEM stores, so that
+      // UNR x 256 x (CTAs/SM) 8-byte loads are in flight per SM (latency x bandwidth)
+      constexpr int UNR = 8;
       int r = r0, j = j0;
-      for (int f = tid; f < total; f += HB_NT) {
-        tile[r * S + j] = __ldcs(src + f);  // streamed once: evict-first
-        j += dr;
-        r += dq;
-        if (j >= n) { j -= n; ++r; }
+      for (int f0 = 0; f0 < total; f0 += UNR * HB_NT) {
+        double v[UNR];
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+          const int f = f0 + u * HB_NT + tid;
+          v[u] = (f < total) ? __ldcs(src + f) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+          const int f = f0 + u * HB_NT + tid;
+          if (f < total) tile[r * S + j] = v[u];
+          j += dr;
+          r += dq;
+          if (j >= n) { j -= n; ++r; }
+        }
       }
     }
     __syncthreads();
@@ -113,12 +126,19 @@ cudaError_t launch_hyperbox(const HyperboxArgs& a, cudaStream_t s) {
   const int S = a.n | 1;
   const size_t smem = sizeof(double) * ((size_t)HB_NT * S + 2 * (size_t)a.n);
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
-  cudaError_t e = cudaFuncSetAttribute(hyperbox_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, hyperbox_kernel, HB_NT, smem);
-  if (e != cudaSuccess) return e;
+  static int cached_dev = -1, per_sm = 0;
+  static size_t cached_smem = (size_t)-1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev != cached_dev || smem != cached_smem) {
+    cudaError_t e = cudaFuncSetAttribute(hyperbox_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, hyperbox_kernel, HB_NT, smem);
+    if (e != cudaSuccess) return e;
+    cached_dev = dev;
+    cached_smem = smem;
+  }
   const int64_t ntiles = (a.batch + HB_NT - 1) / HB_NT;
   int64_t grid = (int64_t)per_sm * device_sm_count();
   if (grid > ntiles) grid = ntiles;

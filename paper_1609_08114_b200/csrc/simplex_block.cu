@@ -28,6 +28,7 @@
 #include <cfloat>
 #include <climits>
 
+#include "lpb_fp64.cuh"
 #include "lpb_internal.cuh"
 
 namespace cg = cooperative_groups;
@@ -82,6 +83,7 @@ struct Ctl {
 struct Smem {
   double* T;      // rows x S
   double* colE;   // pivot column (all rows), filled by the owner CTA
+  double* fcol;   // update multipliers: -colE_i, +1 for the pivot row
   double* prow;   // new pivot row (local columns)
   int* nbvar;     // local position -> variable index (or DEAD)
   int* bkey;      // row -> key of its basic variable (>= 0 real, < 0 artificial)
@@ -151,13 +153,28 @@ __device__ __forceinline__ Cand cluster_reduce(Cand c, const Smem& s, int& par,
 // colE[] (pivot column, all rows) is already in this CTA's SMEM.  Row l becomes the pivot
 // row divided by PE; the entering position e (owned by CTA `owner` at local column jloc)
 // receives the leaving variable's column: rl = 1/PE in row l, fma(-f_i, rl, 0) elsewhere.
+// Implementation: row l and column jloc are zeroed once their values are captured, and the
+// multiplier of row l is +1, so ONE fma per element, T_ij = fma(fcol_i, prow_j, T_ij), yields
+// the pivot row (fma(1, prow, 0)), the swapped column (fma(-f_i, rl, 0)) and every other
+// element -- no per-element branch.  Warps walk rows, lanes walk columns (conflict-free
+// SMEM rows, odd stride), the lane's prow values stay in registers.
 __device__ __forceinline__ void pivot_local(const Smem& s, int S, int Wa, int nrow, int l,
                                             bool own, int jloc, int ent_var) {
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const double pe = s.colE[l];
   for (int j = tid; j < Wa; j += NT) {
-    const double num = (own && j == jloc) ? 1.0 : s.T[l * S + j];
-    s.prow[j] = __ddiv_rn(num, pe);
+    const bool sw = own && j == jloc;
+    double* tl = s.T + l * S + j;
+    const double num = sw ? 1.0 : *tl;
+    bool slow;
+    double q = div_fast(num, pe, slow);
+    if (slow) q = __ddiv_rn(num, pe);
+    s.prow[j] = q;
+    *tl = 0.0;
+  }
+  for (int i = tid; i < nrow; i += NT) {
+    s.fcol[i] = (i == l) ? 1.0 : -s.colE[i];
+    if (own) s.T[i * S + jloc] = 0.0;
   }
   if (tid == 0) {
     const int leaving = s.bkey[l];
@@ -165,22 +182,21 @@ __device__ __forceinline__ void pivot_local(const Smem& s, int S, int Wa, int nr
     if (own) s.nbvar[jloc] = leaving < 0 ? DEAD : leaving;
   }
   __syncthreads();
-  // flat (i, j) walk over nrow x Wa with an incremental divmod
-  int i = tid / Wa, j = tid - (tid / Wa) * Wa;
-  const int dq = NT / Wa, dr = NT - (NT / Wa) * Wa;
-  const int jswap = own ? jloc : -1;
-  for (; i < nrow;) {
-    double* t = s.T + i * S + j;
-    const double p = s.prow[j];
-    if (i == l) {
-      *t = p;
-    } else {
-      const double f = -s.colE[i];
-      *t = __fma_rn(f, p, (j == jswap) ? 0.0 : *t);
+  constexpr int MAXC = 8;  // Wa <= 256 local columns per CTA
+  double pr[MAXC];
+#pragma unroll
+  for (int c = 0; c < MAXC; ++c) {
+    const int j = lane + 32 * c;
+    pr[c] = (j < Wa) ? s.prow[j] : 0.0;
+  }
+  const int nch = (Wa + 31) >> 5;
+  for (int i = w; i < nrow; i += NW) {
+    const double f = s.fcol[i];
+    double* row = s.T + i * S + lane;
+#pragma unroll
+    for (int c = 0; c < MAXC; ++c) {
+      if (c < nch && lane + 32 * c < Wa) row[32 * c] = __fma_rn(f, pr[c], row[32 * c]);
     }
-    j += dr;
-    i += dq;
-    if (j >= Wa) { j -= Wa; ++i; }
   }
   __syncthreads();
 }
@@ -198,7 +214,8 @@ __global__ void __launch_bounds__(NT) simplex_block_kernel(SimplexArgs a) {
   Smem s;
   s.T = reinterpret_cast<double*>(smem_raw);
   s.colE = s.T + (size_t)RC * S;
-  s.prow = s.colE + RC;
+  s.fcol = s.colE + RC;
+  s.prow = s.fcol + RC;
   s.nbvar = reinterpret_cast<int*>(s.prow + (Q + 1));
   s.bkey = s.nbvar + (Q + 1);
   s.negrows = s.bkey + m;
@@ -352,7 +369,10 @@ __global__ void __launch_bounds__(NT) simplex_block_kernel(SimplexArgs a) {
         for (int i = tid; i < m; i += NT) {
           const double ai = s.T[i * S + jloc];
           if (ai > a.eps_piv) {
-            const Cand cc{__ddiv_rn(s.T[i * S + cnt], ai), bland ? s.bkey[i] : i, i};
+            bool slow;
+            double r = div_fast(s.T[i * S + cnt], ai, slow);
+            if (slow) r = __ddiv_rn(s.T[i * S + cnt], ai);
+            const Cand cc{r, bland ? s.bkey[i] : i, i};
             if (better<MIN_V>(cc, cr)) cr = cc;
           }
         }
@@ -414,7 +434,7 @@ __global__ void __launch_bounds__(NT) simplex_block_kernel(SimplexArgs a) {
 size_t block_smem_bytes(int cl, int m, int n, int kmax) {
   const int Q = (n + kmax + cl - 1) / cl;
   const int S = (Q + 1) | 1;
-  size_t bytes = sizeof(double) * ((size_t)(m + 2) * S + (m + 2) + (Q + 1));
+  size_t bytes = sizeof(double) * ((size_t)(m + 2) * S + 2 * (size_t)(m + 2) + (Q + 1));
   bytes += sizeof(int) * ((size_t)(Q + 1) + 2 * (size_t)m + NW);
   bytes = (bytes + 15) & ~size_t(15);
   bytes += sizeof(Cand) * (2 * NW + 2 * cl) + sizeof(Ctl);
@@ -422,41 +442,52 @@ size_t block_smem_bytes(int cl, int m, int n, int kmax) {
 }
 
 bool block_fits(int cl, int m, int n, int kmax) {
-  return block_smem_bytes(cl, m, n, kmax) <= 227 * 1024;
+  const int Q = (n + kmax + cl - 1) / cl;  // pivot_local keeps <= 8 columns per lane
+  return Q + 1 <= 256 && block_smem_bytes(cl, m, n, kmax) <= 227 * 1024;
 }
 
 template <int CL>
 static cudaError_t launch_cl(const SimplexArgs& a, int grid_override, cudaStream_t s,
                              int* ctas_out) {
   const size_t smem = block_smem_bytes(CL, a.m, a.n, a.kmax);
-  cudaError_t e = cudaFuncSetAttribute(simplex_block_kernel<CL>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
   const int sms = device_sm_count();
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute attr[1];
   cfg.blockDim = dim3(NT);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  int resident = 0;
-  if constexpr (CL == 1) {
-    int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, simplex_block_kernel<1>, NT,
-                                                      smem);
-    if (e != cudaSuccess) return e;
-    resident = per_sm * sms;
-  } else {
+  if constexpr (CL > 1) {
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = CL;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cfg.gridDim = dim3(CL * sms);
-    int clusters = 0;
-    e = cudaOccupancyMaxActiveClusters(&clusters, simplex_block_kernel<CL>, &cfg);
+  }
+  // attribute + occupancy queries are host round trips: cache per (device, smem size)
+  static int cached_dev = -1, resident = 0;
+  static size_t cached_smem = (size_t)-1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev != cached_dev || smem != cached_smem) {
+    cudaError_t e = cudaFuncSetAttribute(simplex_block_kernel<CL>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    resident = clusters * CL;
+    if constexpr (CL == 1) {
+      int per_sm = 0;
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, simplex_block_kernel<1>, NT,
+                                                        smem);
+      if (e != cudaSuccess) return e;
+      resident = per_sm * sms;
+    } else {
+      cfg.gridDim = dim3(CL * sms);
+      int clusters = 0;
+      e = cudaOccupancyMaxActiveClusters(&clusters, simplex_block_kernel<CL>, &cfg);
+      if (e != cudaSuccess) return e;
+      resident = clusters * CL;
+    }
+    cached_dev = dev;
+    cached_smem = smem;
   }
   if (resident <= 0) return cudaErrorInvalidConfiguration;
   int64_t want = a.batch * CL;

@@ -610,13 +610,20 @@ template <int TR, int TC, int A, int BC, bool TWO, int MINB>
 cudaError_t launch_one(const SimplexArgs& a, int grid_override, cudaStream_t s, int* ctas) {
   auto kern = simplex_reg_kernel<TR, TC, A, BC, TWO, MINB>;
   const size_t dsm = a.prefetch ? (size_t)a.m * a.n * 8 : 0;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm);
-  if (e != cudaSuccess) return e;
-  int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TR * TC, dsm);
-  if (e != cudaSuccess) return e;
-  if (per_sm < 1) per_sm = 1;
-  int64_t grid = (int64_t)per_sm * device_sm_count();
+  // attribute + occupancy queries are host round trips: cache them per (device, smem size)
+  static int cached_dev = -1, per_sm = 0;
+  static size_t cached_dsm = (size_t)-1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev != cached_dev || dsm != cached_dsm) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm);
+    if (e != cudaSuccess) return e;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TR * TC, dsm);
+    if (e != cudaSuccess) return e;
+    cached_dev = dev;
+    cached_dsm = dsm;
+  }
+  int64_t grid = (int64_t)(per_sm < 1 ? 1 : per_sm) * device_sm_count();
   if (grid > a.batch) grid = a.batch;
   if (grid_override > 0) grid = grid_override;
   if (ctas) *ctas = (int)grid;
