@@ -12,6 +12,9 @@
 // The box (2n fp64) is shared by the batch (LPB_SHARED_BOX, the paper's experiment,
 // PAPER.md:313) and lives in SMEM; a per-LP box is read from global memory.
 // This kernel is HBM-bound: 8n bytes in + (8n + 12) bytes out per LP.
+#include <cstdlib>
+
+#include "lpb_async.cuh"
 #include "lpb_internal.cuh"
 
 namespace lpb {
@@ -120,9 +123,83 @@ __global__ void __launch_bounds__(HB_NT) hyperbox_kernel(HyperboxArgs a) {
   }
 }
 
+
+// Shared-box fast path: tiles of LPT*256 directions stream HBM -> SMEM with bulk async copies
+// (cp.async.bulk, one per tile) through a STAGES-deep ring, so several tiles per SM are in
+// flight while the current one is evaluated (HBM latency x bandwidth needs ~44 KB in flight
+// per SM).  The tile stays dense in SMEM; x = h is produced in the coalesced store pass
+// directly from the sign of l (no write-back).
+__global__ void __launch_bounds__(HB_NT, 1)
+hyperbox_tma_kernel(HyperboxArgs a, int lpt, int stages) {
+  extern __shared__ __align__(16) unsigned char hraw[];
+  const int n = a.n, tid = threadIdx.x;
+  const int tile_lps = lpt * HB_NT;
+  const size_t tile_elems = (size_t)tile_lps * n;
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(hraw);                 // [stages]
+  double* blo = reinterpret_cast<double*>(hraw + 16 * 8);            // [n]
+  double* bhi = blo + n;                                              // [n]
+  double* buf = bhi + n + ((2 * n) & 1);                              // [stages][tile]
+  buf = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(buf) + 15) & ~uintptr_t(15));
+  for (int i = tid; i < n; i += HB_NT) {
+    bhi[i] = a.box[i];
+    blo[i] = -a.box[n + i];
+  }
+  bool empty = false;
+  for (int i = 0; i < n; ++i) empty |= (-a.box[n + i] > a.box[i]);
+  const int64_t nfull = a.batch / tile_lps;  // full tiles go through the TMA ring
+  if (tid == 0) {
+    for (int st = 0; st < stages; ++st) mbar_init(&mbar[st], 1);
+    for (int st = 0; st < stages; ++st) {
+      const int64_t t = blockIdx.x + (int64_t)st * gridDim.x;
+      if (t < nfull)
+        bulk_load(buf + st * tile_elems, a.l + t * tile_elems, (uint32_t)(tile_elems * 8), &mbar[st]);
+    }
+  }
+  __syncthreads();
+  const int r0 = tid / n, j0 = tid - r0 * n;
+  const int dq = HB_NT / n, dr = HB_NT - dq * n;
+  int k = 0;
+  for (int64_t t = blockIdx.x; t < nfull; t += gridDim.x, ++k) {
+    const int st = k % stages;
+    mbar_wait(&mbar[st], (uint32_t)((k / stages) & 1));
+    const double* tb = buf + st * tile_elems;
+    const int64_t lp0 = t * tile_lps;
+    for (int q = 0; q < lpt; ++q) {
+      const int r = q * HB_NT + tid;
+      const double* row = tb + (size_t)r * n;
+      double acc = 0.0;
+      for (int i = 0; i < n; ++i) {
+        const double li = row[i];
+        acc = __fma_rn(li, (li < 0.0) ? blo[i] : bhi[i], acc);
+      }
+      __stcs(a.status + lp0 + r, empty ? ST_INFEASIBLE : ST_OPTIMAL);
+      __stcs(a.obj + lp0 + r, empty ? __longlong_as_double(0xfff0000000000000ll) : acc);
+    }
+    if (a.x) {
+      double* __restrict__ dst = a.x + lp0 * n;
+      const int total = tile_lps * n;
+      int j = j0;
+      for (int f = tid; f < total; f += HB_NT) {
+        const double li = tb[f];
+        __stcs(dst + f, empty ? __longlong_as_double(0x7ff8000000000000ll)
+                              : ((li < 0.0) ? blo[j] : bhi[j]));
+        j += dr;
+        if (j >= n) j -= n;
+      }
+    }
+    __syncthreads();  // every read of this stage is done: refill it
+    if (tid == 0) {
+      const int64_t tn = t + (int64_t)stages * gridDim.x;
+      if (tn < nfull)
+        bulk_load(buf + st * tile_elems, a.l + tn * tile_elems, (uint32_t)(tile_elems * 8), &mbar[st]);
+    }
+  }
+  (void)r0; (void)dq;
+}
+
 }  // namespace
 
-cudaError_t launch_hyperbox(const HyperboxArgs& a, cudaStream_t s) {
+static cudaError_t launch_hyperbox_plain(const HyperboxArgs& a, cudaStream_t s) {
   const int S = a.n | 1;
   const size_t smem = sizeof(double) * ((size_t)HB_NT * S + 2 * (size_t)a.n);
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
@@ -145,6 +222,52 @@ cudaError_t launch_hyperbox(const HyperboxArgs& a, cudaStream_t s) {
   if (grid < 1) grid = 1;
   hyperbox_kernel<<<(unsigned)grid, HB_NT, smem, s>>>(a);
   return cudaGetLastError();
+}
+
+cudaError_t launch_hyperbox(const HyperboxArgs& a, cudaStream_t s) {
+  // Shared box and 16-byte aligned directions: TMA-ring kernel over the full tiles, the plain
+  // kernel over the ragged tail (and for per-LP boxes).
+  const int n = a.n;
+  int lpt = 1;
+  while (lpt < 8 && (size_t)(2 * lpt) * HB_NT * n * 8 <= 56 * 1024) lpt *= 2;
+  const size_t tile_bytes = (size_t)lpt * HB_NT * n * 8;
+  int stages = (int)((200 * 1024) / tile_bytes);
+  if (stages > 4) stages = 4;
+  const bool tma = a.shared_box && stages >= 2 && (tile_bytes % 16) == 0 &&
+                   (reinterpret_cast<uintptr_t>(a.l) & 15) == 0 && getenv("LPB_NO_TMA") == nullptr;
+  const int64_t tile_lps = (int64_t)lpt * HB_NT;
+  const int64_t nfull = tma ? a.batch / tile_lps : 0;
+  if (nfull > 0) {
+    const size_t smem = 16 * 8 + 16 * (size_t)((2 * n + 2 + 1) / 2) + 16 + stages * tile_bytes;
+    static size_t cached_smem = (size_t)-1;
+    static int cached_dev = -1;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (smem != cached_smem || dev != cached_dev) {
+      cudaError_t e = cudaFuncSetAttribute(hyperbox_tma_kernel,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      cached_smem = smem;
+      cached_dev = dev;
+    }
+    int64_t grid = device_sm_count();
+    if (grid > nfull) grid = nfull;
+    hyperbox_tma_kernel<<<(unsigned)grid, HB_NT, smem, s>>>(a, lpt, stages);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  const int64_t done = nfull * tile_lps;
+  if (done < a.batch) {
+    HyperboxArgs t = a;
+    t.batch = a.batch - done;
+    t.l = a.l + done * n;
+    t.status = a.status + done;
+    t.obj = a.obj + done;
+    t.x = a.x ? a.x + done * n : nullptr;
+    if (!a.shared_box) t.box = a.box + done * 2 * (int64_t)n;
+    return launch_hyperbox_plain(t, s);
+  }
+  return cudaSuccess;
 }
 
 }  // namespace lpb

@@ -33,3 +33,107 @@ extern "C" int lpb_selftest_div(const double* a, const double* b, double* q, int
   out[1] = (int64_t)h[1];
   return LPB_OK;
 }
+
+// ---- latency microbenchmarks of the simplex kernels' building blocks (diagnostics) ----
+namespace {
+constexpr unsigned FULLM = 0xffffffffu;
+__device__ __forceinline__ unsigned long long okey_t(double d) {
+  const unsigned long long u = (unsigned long long)__double_as_longlong(__dadd_rn(d, 0.0));
+  return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+}
+__device__ __forceinline__ int argmax_redux(bool valid, unsigned long long k, unsigned tie) {
+  if (__ballot_sync(FULLM, valid) == 0u) return -1;
+  const unsigned hi = valid ? (unsigned)(k >> 32) : 0u;
+  const unsigned mhi = __reduce_max_sync(FULLM, hi);
+  const bool c1 = valid && hi == mhi;
+  const unsigned lo = c1 ? (unsigned)k : 0u;
+  const unsigned mlo = __reduce_max_sync(FULLM, lo);
+  const bool c2 = c1 && (unsigned)k == mlo;
+  const unsigned t = c2 ? tie : 0xffffffffu;
+  const unsigned mt = __reduce_min_sync(FULLM, t);
+  return __ffs(__ballot_sync(FULLM, c2 && tie == mt)) - 1;
+}
+__global__ void lat_kernel(const double* in, long long* out, int iters) {
+  const int lane = threadIdx.x & 31;
+  double v = in[threadIdx.x];
+  long long t0, t1;
+  int acc = 0;
+  // 0: REDUX-based (value, tie) warp argmax
+  t0 = clock64();
+  for (int i = 0; i < iters; ++i) {
+    const int wl = argmax_redux(v > 0.0, okey_t(v), (unsigned)lane);
+    acc += wl;
+    v = __dadd_rn(v, (double)(wl & 1));
+  }
+  t1 = clock64();
+  if (threadIdx.x == 0) out[0] = (t1 - t0) / iters;
+  // 1: shuffle butterfly argmax (5 rounds, double value + int key)
+  t0 = clock64();
+  for (int i = 0; i < iters; ++i) {
+    double bv = v;
+    int bk = lane;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const double ov = __shfl_xor_sync(FULLM, bv, off);
+      const int ok = __shfl_xor_sync(FULLM, bk, off);
+      if (ov > bv || (ov == bv && ok < bk)) { bv = ov; bk = ok; }
+    }
+    acc += bk;
+    v = __dadd_rn(v, (double)(bk & 1));
+  }
+  t1 = clock64();
+  if (threadIdx.x == 0) out[1] = (t1 - t0) / iters;
+  // 2: dependent div_fast chain
+  t0 = clock64();
+  double q = v + 1.5;
+  for (int i = 0; i < iters; ++i) {
+    bool slow;
+    q = lpb::div_fast(q + 3.0, 1.25 + (double)(i & 3), slow);
+  }
+  t1 = clock64();
+  if (threadIdx.x == 0) out[2] = (t1 - t0) / iters;
+  // 3: dependent DFMA chain
+  t0 = clock64();
+  double z = q;
+  for (int i = 0; i < iters; ++i) z = __fma_rn(z, 0.999, 1e-3);
+  t1 = clock64();
+  if (threadIdx.x == 0) out[3] = (t1 - t0) / iters;
+  // 4: __syncthreads round trip
+  t0 = clock64();
+  for (int i = 0; i < iters; ++i) __syncthreads();
+  t1 = clock64();
+  if (threadIdx.x == 0) out[4] = (t1 - t0) / iters;
+  // 5: dependent SHFL (int)
+  t0 = clock64();
+  int s = lane;
+  for (int i = 0; i < iters; ++i) s = __shfl_sync(FULLM, s, (s + 1) & 31);
+  t1 = clock64();
+  if (threadIdx.x == 0) out[5] = (t1 - t0) / iters;
+  // 6: dependent REDUX
+  t0 = clock64();
+  unsigned r = lane;
+  for (int i = 0; i < iters; ++i) r = __reduce_max_sync(FULLM, r + lane);
+  t1 = clock64();
+  if (threadIdx.x == 0) out[6] = (t1 - t0) / iters;
+  // 7: dependent DSETP->select chain (one step of a register argmax scan)
+  t0 = clock64();
+  double bv2 = -1.0;
+  for (int i = 0; i < iters; ++i) { const double c = z + (double)i; bv2 = (c > bv2) ? c : bv2 * 0.5; }
+  t1 = clock64();
+  if (threadIdx.x == 0) out[7] = (t1 - t0) / iters;
+  if (threadIdx.x == 0) out[8] = acc + s + (int)r + (int)bv2 + (int)z;
+}
+}  // namespace
+
+extern "C" int lpb_selftest_latency(int threads, long long* out9) {
+  double* d_in = nullptr;
+  long long* d_out = nullptr;
+  if (cudaMalloc(&d_in, 1024 * sizeof(double)) != cudaSuccess) return LPB_ECUDA;
+  cudaMalloc(&d_out, 16 * sizeof(long long));
+  cudaMemset(d_in, 0, 1024 * sizeof(double));
+  lat_kernel<<<1, threads>>>(d_in, d_out, 1000);
+  const cudaError_t e = cudaMemcpy(out9, d_out, 9 * sizeof(long long), cudaMemcpyDeviceToHost);
+  cudaFree(d_in);
+  cudaFree(d_out);
+  return e == cudaSuccess ? LPB_OK : LPB_ECUDA;
+}
