@@ -47,12 +47,16 @@ __device__ __forceinline__ unsigned long long okey(double d) {
 __device__ __forceinline__ unsigned ikey(int t) { return (unsigned)t ^ 0x80000000u; }
 
 // Warp argmax of (key desc, tie asc) over lanes with `valid`; returns the winner lane or -1.
-// Must be called by all 32 lanes.
+// Must be called by all 32 lanes.  Fast path: one REDUX on the key's high word; only when
+// several lanes share it (rare for real-valued data) are the low word and the tie key
+// reduced as well.
 __device__ __forceinline__ int warp_argmax(bool valid, unsigned long long k, unsigned tie) {
-  if (__ballot_sync(FULL, valid) == 0u) return -1;
   const unsigned hi = valid ? (unsigned)(k >> 32) : 0u;
   const unsigned mhi = __reduce_max_sync(FULL, hi);
   const bool c1 = valid && hi == mhi;
+  const unsigned b1 = __ballot_sync(FULL, c1);
+  if (b1 == 0u) return -1;
+  if ((b1 & (b1 - 1u)) == 0u) return __ffs(b1) - 1;
   const unsigned lo = c1 ? (unsigned)k : 0u;
   const unsigned mlo = __reduce_max_sync(FULL, lo);
   const bool c2 = c1 && (unsigned)k == mlo;
@@ -63,10 +67,12 @@ __device__ __forceinline__ int warp_argmax(bool valid, unsigned long long k, uns
 
 // Warp argmin of (key asc, tie asc) over lanes with `valid`; returns the winner lane or -1.
 __device__ __forceinline__ int warp_argmin(bool valid, unsigned long long k, unsigned tie) {
-  if (__ballot_sync(FULL, valid) == 0u) return -1;
   const unsigned hi = valid ? (unsigned)(k >> 32) : 0xffffffffu;
   const unsigned mhi = __reduce_min_sync(FULL, hi);
   const bool c1 = valid && hi == mhi;
+  const unsigned b1 = __ballot_sync(FULL, c1);
+  if (b1 == 0u) return -1;
+  if ((b1 & (b1 - 1u)) == 0u) return __ffs(b1) - 1;
   const unsigned lo = c1 ? (unsigned)k : 0xffffffffu;
   const unsigned mlo = __reduce_min_sync(FULL, lo);
   const bool c2 = c1 && (unsigned)k == mlo;
@@ -92,6 +98,8 @@ struct Part {  // a (value, tie, index) reduction partial
   double v;
   int tie;
   int idx;
+  int leave;  // basis key of row idx (the leaving variable if idx wins)
+  int pad;
 };
 
 template <int TR, int TC, int A, int BC>
@@ -101,20 +109,22 @@ struct RegSmem {
   double fcol[2][RCAP];  // update multipliers: -colE, and +1 for the pivot row
   double fobj[2][2];     // pivot-column entries of the phase-II / phase-I rows
   double rhs[RCAP];      // RHS column (lazily updated)
-  double prow[CCAP];     // new pivot row (positions); scratch for the phase-I row at build
+  double prow[CCAP];     // scratch for the phase-I row at build
+  double pslot[2][NWARP][CCAP];  // each warp's speculative scaled pivot row (its candidate)
+  double prr[2][NWARP];          // ... and its RHS / PE
   int bkey[RCAP];        // row -> basic variable key (>= 0 real, < 0 artificial)
-  int nbvar[CCAP];       // position -> nonbasic variable index (DEADV: dead / padding)
+  int nbvar[NWARP][CCAP];  // position -> nonbasic variable index, one copy per warp
   int negrows[RCAP];     // ascending rows with b_i < 0
   int wcount[NWARP];
-  Part part[NWARP];      // ratio-test partial per warp
-  double prow_rhs;
+  Part part[2][NWARP];   // ratio-test partial per warp (double-buffered by pivot parity)
   uint64_t mbar;         // completes when the prefetched A of LP `lp` has landed
   int lp;
-  int leaving;
 };
 
 // Optional phase profiler (SimplexArgs::prof != nullptr): warp 0 of every CTA accumulates
-// clock64() deltas per pivot phase into prof[blockIdx.x * 8 + phase].  Off by default.
+// clock64() deltas per pivot phase into prof[blockIdx.x * 8 + phase]: 7 build/loop head,
+// 0 Step 1, 1 publish column, 2 ratio + speculative pivot row, 3 barrier wait, 4 partial
+// reduce, 5 bookkeeping, 6 update.  Off by default.
 #define LPB_PROF_MARK(ph)                                                 \
   if (prof_on) {                                                          \
     const long long t_ = clock64();                                       \
@@ -194,14 +204,17 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
     }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) binf = fmax(binf, __shfl_xor_sync(FULL, binf, off));
-    if (lane == 0) sm.part[w].v = binf;
+    if (lane == 0) sm.part[0][w].v = binf;
     gsync<NT>();
 #pragma unroll
-    for (int q = 0; q < NWARP; ++q) binf = fmax(binf, sm.part[q].v);
+    for (int q = 0; q < NWARP; ++q) binf = fmax(binf, sm.part[0][q].v);
     const int npos = n + k;
     int st = (m > RCAP || npos > CCAP || (!TWO && k > 0)) ? ST_NUMERICAL : -1;
-    for (int p = tid; p < CCAP; p += NT)
-      sm.nbvar[p] = (p < n) ? p : (p < npos ? n + sm.negrows[p - n] : DEADV);
+    for (int p = tid; p < CCAP; p += NT) {
+      const int v = (p < n) ? p : (p < npos ? n + sm.negrows[p - n] : DEADV);
+#pragma unroll
+      for (int q = 0; q < NWARP; ++q) sm.nbvar[q][p] = v;
+    }
     for (int i = m + tid; i < RCAP; i += NT) sm.rhs[i] = 0.0;
 
 #pragma unroll
@@ -268,9 +281,16 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
     }
 
     // ---- Steps 1-3, two phases ----
+    // ONE block barrier per pivot: every warp scales its own ratio-test winner row
+    // speculatively (a warp's candidate row always lies in the warp's own thread-rows), and
+    // after the barrier every warp reads the winning warp's scaled pivot row.  All other
+    // SMEM traffic is warp-local (colE, fcol, rhs, bkey of a row are touched only by the
+    // warp owning that row; nbvar has one copy per warp).
     int it1 = 0, it2 = 0, stall = 0, phase = (TWO && k > 0) ? 1 : 2;
     int par = 0, l_prev = -1, dl = 0;
+    double prr_prev = 0.0;
     bool pend = false, drive = false;
+    int* nbv = sm.nbvar[w];
     while (st < 0) {
       const bool bland = a.bland_K > 0 && stall >= a.bland_K;
       const bool p1 = TWO && phase == 1;
@@ -299,7 +319,7 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
             v = fabs(v);
             if (d2[b] != neg_inf() && v > a.eps_piv) {  // live position
               const int p = tc + TC * b;
-              const unsigned var = (unsigned)sm.nbvar[p];
+              const unsigned var = (unsigned)nbv[p];
               if (!val || v > bv || (v == bv && var < bvar)) {
                 val = true;
                 bv = v;
@@ -310,15 +330,15 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
           }
         }
         const int wl = warp_argmax(val, okey(bv), bvar);
-        Part pw{0.0, INT_MAX, -1};
+        Part pw{0.0, INT_MAX, -1, 0, 0};
         if (wl >= 0) {
           pw.v = __shfl_sync(FULL, bv, wl);
           pw.tie = (int)__shfl_sync(FULL, bvar, wl);
           pw.idx = __shfl_sync(FULL, bp, wl);
         }
-        if (lane == 0) sm.part[w] = pw;
+        if (lane == 0) sm.part[par][w] = pw;
         gsync<NT>();
-        const Part q = (lane < NWARP) ? sm.part[lane] : Part{0.0, INT_MAX, -1};
+        const Part q = (lane < NWARP) ? sm.part[par][lane] : Part{0.0, INT_MAX, -1, 0, 0};
         const int ql = warp_argmax(q.idx >= 0, okey(q.v), (unsigned)q.tie);
         gsync<NT>();
         if (ql < 0) continue;  // redundant row: the artificial stays basic at 0
@@ -346,13 +366,13 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
             const double v = p1 ? d1[TWO ? b : 0] : d2[b];
             tie |= (b != bb) && (v == bv);
           }
-          bvar = val ? (unsigned)sm.nbvar[tc + TC * bb] : 0u;
+          bvar = val ? (unsigned)nbv[tc + TC * bb] : 0u;
           if (__any_sync(FULL, val && tie)) {  // rare: exact tie inside a thread -> var index
             if (val && tie) {
 #pragma unroll
               for (int b = 0; b < BC; ++b) {
                 const double v = p1 ? d1[TWO ? b : 0] : d2[b];
-                const unsigned var = (unsigned)sm.nbvar[tc + TC * b];
+                const unsigned var = (unsigned)nbv[tc + TC * b];
                 if (v == bv && var < bvar) {
                   bvar = var;
                   bb = b;
@@ -367,7 +387,7 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
           for (int b = 0; b < BC; ++b) {
             const double v = p1 ? d1[TWO ? b : 0] : d2[b];
             if (v > a.eps_enter) {
-              const unsigned var = (unsigned)sm.nbvar[tc + TC * b];
+              const unsigned var = (unsigned)nbv[tc + TC * b];
               if (var < bvar) {
                 bvar = var;
                 bb = b;
@@ -383,15 +403,17 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
           if (z1 > a.eps_phase1 * fmax(1.0, binf)) { st = ST_INFEASIBLE; break; }
           drive = true;  // phase-I optimum with w* ~ 0
           dl = 0;
+          gsync<NT>();  // the drive-out scan reads bkey written by other warps
           continue;
         }
         if (it1 + it2 >= a.max_iter) { st = ST_ITER_LIMIT; break; }
         e = __shfl_sync(FULL, tc + TC * bb, wl);
         evar = (int)__shfl_sync(FULL, bvar, wl);
       }
-
       LPB_PROF_MARK(0)
-      // Step 2a: the owners of position e publish column e (+ objective-row entries)
+
+      // Step 2a: the owners of position e publish column e (+ objective-row entries) and
+      // zero it (so the update produces the leaving variable's column)
       const int be = e / TC, etc = e - be * TC;
       double* colE = sm.colE[par];
       if (tc == etc) {
@@ -417,103 +439,119 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
       LPB_PROF_MARK(1)
       // Step 2b: lane-parallel lazy RHS update + ratio test over the warp's rows; each lane
       // also writes its row's update multiplier f_i = -colE_i
-      {
-        bool val = false;
-        double ratio = 0.0;
-        int tie = INT_MAX;
-        const int i = rrow;
-        if (rlane) {
-          const double v = colE[i];
-          sm.fcol[par][i] = -v;
-          if (i < m) {
-            double r = sm.rhs[i];
-            if (pend) {
-              const double prr = sm.prow_rhs;
-              r = (i == l_prev) ? prr : __fma_rn(sm.fcol[par ^ 1][i], prr, r);
-              sm.rhs[i] = r;
-            }
-            if (!drive) {
-              val = v > a.eps_piv;
-              bool slow;
-              ratio = div_fast(r, val ? v : 1.0, slow);
-              if (slow) ratio = __ddiv_rn(r, val ? v : 1.0);  // rare: outside the fast range
-              tie = bland ? sm.bkey[i] : i;
-            }
+      const int ri = rrow;
+      bool rval = false;
+      double ratio = 0.0;
+      int rtie = INT_MAX;
+      if (rlane) {
+        const double v = colE[ri];
+        sm.fcol[par][ri] = -v;
+        if (ri < m) {
+          double r = sm.rhs[ri];
+          if (pend) {
+            r = (ri == l_prev) ? prr_prev : __fma_rn(sm.fcol[par ^ 1][ri], prr_prev, r);
+            sm.rhs[ri] = r;
+          }
+          if (!drive) {
+            rval = v > a.eps_piv;
+            bool slow;
+            ratio = div_fast(r, rval ? v : 1.0, slow);
+            if (slow) ratio = __ddiv_rn(r, rval ? v : 1.0);  // rare: outside the fast range
+            rtie = bland ? sm.bkey[ri] : ri;
           }
         }
-        if (!drive) {
-          const int wl = warp_argmin(val, okey(ratio), ikey(tie));
-          Part pw{0.0, INT_MAX, -1};
-          if (wl >= 0) {
-            pw.v = __shfl_sync(FULL, ratio, wl);
-            pw.tie = __shfl_sync(FULL, tie, wl);
-            pw.idx = __shfl_sync(FULL, i, wl);
-          }
-          if (lane == 0) sm.part[w] = pw;
+      }
+      int lw = -1;
+      double thw = 0.0;
+      int tiew = INT_MAX;
+      if (!drive) {
+        const int wl = warp_argmin(rval, okey(ratio), ikey(rtie));
+        if (wl >= 0) {
+          lw = __shfl_sync(FULL, ri, wl);
+          thw = __shfl_sync(FULL, ratio, wl);
+          tiew = __shfl_sync(FULL, rtie, wl);
         }
+      } else if ((l % TR) / RPW == w) {
+        lw = l;  // the drive-out row belongs to this warp
       }
-      LPB_PROF_MARK(2)
-      gsync<NT>();  // barrier 1
-      LPB_PROF_MARK(3)
-      double theta = 0.0;
-      if (!drive) {  // Step 2c: argmin over the warp partials, in every warp
-        const Part q = (lane < NWARP) ? sm.part[lane] : Part{0.0, INT_MAX, -1};
-        const int ql = warp_argmin(q.idx >= 0, okey(q.v), ikey(q.tie));
-        if (ql < 0) { st = (phase == 2) ? ST_UNBOUNDED : ST_NUMERICAL; break; }
-        l = __shfl_sync(FULL, q.idx, ql);
-        theta = __shfl_sync(FULL, q.v, ql);
-      }
-
-      LPB_PROF_MARK(4)
-      // Step 3: pivot row / PE by the owners of row l
-      const double pe = colE[l];
-      if (tid == 0) {
-        const int lv = sm.bkey[l];
-        sm.bkey[l] = evar;
-        sm.nbvar[e] = lv >= 0 ? lv : DEADV;
-        sm.leaving = lv;
-        sm.fcol[par][l] = 1.0;  // the pivot row: fma(1, prow, 0) = prow
-      }
-      const int ltr = l % TR, al = l / TR;
-      if (tr == ltr) {
+      __syncwarp();  // the lazily updated rhs[lw] is visible to the warp
+      // Step 3 (speculative): the thread-row holding lw scales it by PE
+      if (lw >= 0 && tr == lw % TR) {
+        const double pe = colE[lw];
+        const int al = lw / TR;
+        double* ps = sm.pslot[par][w];
 #define LPB_PROW(x)                                                                 \
   case x:                                                                           \
     if constexpr ((x) < A) {                                                        \
       bool slow_any = false;                                                        \
       double q[BC];                                                                 \
       _Pragma("unroll") for (int b = 0; b < BC; ++b) {                              \
-        const int p = tc + TC * b;                                                  \
         bool sl;                                                                    \
-        q[b] = div_fast(p == e ? 1.0 : T[x][b], pe, sl);                            \
+        q[b] = div_fast(tc + TC * b == e ? 1.0 : T[x][b], pe, sl);                  \
         slow_any |= sl;                                                             \
       }                                                                             \
       if (slow_any) {                                                               \
         _Pragma("unroll") for (int b = 0; b < BC; ++b)                              \
           q[b] = __ddiv_rn(tc + TC * b == e ? 1.0 : T[x][b], pe);                   \
       }                                                                             \
-      _Pragma("unroll") for (int b = 0; b < BC; ++b) {                              \
-        sm.prow[tc + TC * b] = q[b];                                                \
-        T[x][b] = 0.0;                                                              \
-      }                                                                             \
+      _Pragma("unroll") for (int b = 0; b < BC; ++b) ps[tc + TC * b] = q[b];        \
     }                                                                               \
     break;
         switch (al) { LPB_CASES(LPB_PROW) default: break; }
 #undef LPB_PROW
         if (tc == 0) {
           bool sl;
-          const double q = div_fast(sm.rhs[l], pe, sl);
-          sm.prow_rhs = sl ? __ddiv_rn(sm.rhs[l], pe) : q;
+          const double q = div_fast(sm.rhs[lw], pe, sl);
+          sm.prr[par][w] = sl ? __ddiv_rn(sm.rhs[lw], pe) : q;
         }
       }
+      if (lane == 0) sm.part[par][w] = Part{thw, tiew, lw, lw >= 0 ? sm.bkey[lw] : 0, 0};
+      LPB_PROF_MARK(2)
+      gsync<NT>();  // the pivot's only block barrier
+      LPB_PROF_MARK(3)
+      // Step 2c: the winning warp partial (argmin of the ratios), read by every warp
+      double theta = 0.0;
+      int ww, leaving;
+      if (!drive) {
+        const Part q = (lane < NWARP) ? sm.part[par][lane] : Part{0.0, INT_MAX, -1, 0, 0};
+        const int ql = warp_argmin(q.idx >= 0, okey(q.v), ikey(q.tie));
+        if (ql < 0) { st = (phase == 2) ? ST_UNBOUNDED : ST_NUMERICAL; break; }
+        ww = ql;
+        l = __shfl_sync(FULL, q.idx, ql);
+        theta = __shfl_sync(FULL, q.v, ql);
+        leaving = __shfl_sync(FULL, q.leave, ql);
+      } else {
+        ww = (l % TR) / RPW;
+        leaving = sm.part[par][ww].leave;
+      }
+      LPB_PROF_MARK(4)
+      // bookkeeping: per-warp nbvar copy; the winning warp owns row l (bkey, fcol, zeroing)
+      if (lane == 0) nbv[e] = leaving >= 0 ? leaving : DEADV;
+      const int ltr = l % TR, al = l / TR;
+      if (w == ww) {
+        if (lane == 0) {
+          sm.bkey[l] = evar;
+          sm.fcol[par][l] = 1.0;  // the pivot row: fma(1, prow, 0) = prow
+        }
+        if (tr == ltr) {
+#define LPB_ROWZ(x)                                                                    \
+  case x:                                                                              \
+    if constexpr ((x) < A) {                                                           \
+      _Pragma("unroll") for (int b = 0; b < BC; ++b) T[x][b] = 0.0;                    \
+    }                                                                                  \
+    break;
+          switch (al) { LPB_CASES(LPB_ROWZ) default: break; }
+#undef LPB_ROWZ
+        }
+      }
+      __syncwarp();
       LPB_PROF_MARK(5)
-      gsync<NT>();  // barrier 2
-      LPB_PROF_MARK(6)
       {
-        const double prr = sm.prow_rhs;
-        const int leaving = sm.leaving;
+        const double* pslw = sm.pslot[par][ww];
+        const double prr = sm.prr[par][ww];
         double pv[BC];
 #pragma unroll
-        for (int b = 0; b < BC; ++b) pv[b] = sm.prow[tc + TC * b];
+        for (int b = 0; b < BC; ++b) pv[b] = pslw[tc + TC * b];
         const double f2 = -sm.fobj[par][0];
         const bool upd1 = TWO && phase == 1;
         const double f1 = TWO ? -sm.fobj[par][1] : 0.0;
@@ -528,9 +566,8 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
         if constexpr (TWO) {
           if (upd1) z1 = __fma_rn(f1, prr, z1);
         }
-        // Row l and position e were zeroed when they were read (Step 2a / Step 3), so one
-        // fma per element yields the pivot row (f_l = 1: fma(1, prow, 0) = prow) and the
-        // leaving variable's column (fma(-f_i, rl, 0)) without any per-element branch.
+        // Row l and position e were zeroed, so one fma per element yields the pivot row
+        // (f_l = 1) and the leaving variable's column (fma(-f_i, rl, 0)) with no branch.
 #pragma unroll
         for (int ai = 0; ai < A; ++ai) {
           const double fi = sm.fcol[par][tr + TR * ai];
@@ -548,7 +585,9 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
           switch (be) { LPB_CASES(LPB_DEAD) default: break; }
 #undef LPB_DEAD
         }
+        prr_prev = prr;
       }
+      LPB_PROF_MARK(6)
       pend = true;
       l_prev = l;
       par ^= 1;
@@ -564,9 +603,8 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
     // ---- extract (R10) ----
     gsync<NT>();
     if (st == ST_OPTIMAL && pend) {  // apply the last pending RHS update
-      const double prr = sm.prow_rhs;
       for (int i = tid; i < m; i += NT)
-        sm.rhs[i] = (i == l_prev) ? prr : __fma_rn(sm.fcol[par ^ 1][i], prr, sm.rhs[i]);
+        sm.rhs[i] = (i == l_prev) ? prr_prev : __fma_rn(sm.fcol[par ^ 1][i], prr_prev, sm.rhs[i]);
     }
     if (tid == 0) {
       a.status[lp] = st;
