@@ -8,9 +8,13 @@ __global__ void div_check(const double* a, const double* b, double* q, int64_t n
                           unsigned long long* cnt) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    bool slow;
+    bool slow, slow2;
     double f = lpb::div_fast(a[i], b[i], slow);
     if (slow) f = __ddiv_rn(a[i], b[i]);
+    // the split form used for pivot rows: one reciprocal, many dividends
+    double g = lpb::div_with(a[i], b[i], lpb::recip_of(b[i]), slow2);
+    if (slow2) g = __ddiv_rn(a[i], b[i]);
+    if (__double_as_longlong(g) != __double_as_longlong(f)) atomicAdd(cnt, 1ull);
     const double r = __ddiv_rn(a[i], b[i]);
     q[i] = f;
     if (__double_as_longlong(f) != __double_as_longlong(r)) atomicAdd(cnt, 1ull);

@@ -162,12 +162,13 @@ __device__ __forceinline__ void pivot_local(const Smem& s, int S, int Wa, int nr
                                             bool own, int jloc, int ent_var) {
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const double pe = s.colE[l];
+  const double rpe = recip_of(pe);
   for (int j = tid; j < Wa; j += NT) {
     const bool sw = own && j == jloc;
     double* tl = s.T + l * S + j;
     const double num = sw ? 1.0 : *tl;
     bool slow;
-    double q = div_fast(num, pe, slow);
+    double q = div_with(num, pe, rpe, slow);
     if (slow) q = __ddiv_rn(num, pe);
     s.prow[j] = q;
     *tl = 0.0;

@@ -478,6 +478,7 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
       // Step 3 (speculative): the thread-row holding lw scales it by PE
       if (lw >= 0 && tr == lw % TR) {
         const double pe = colE[lw];
+        const double rpe = recip_of(pe);  // one MUFU op for the whole row
         const int al = lw / TR;
         double* ps = sm.pslot[par][w];
 #define LPB_PROW(x)                                                                 \
@@ -487,7 +488,7 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
       double q[BC];                                                                 \
       _Pragma("unroll") for (int b = 0; b < BC; ++b) {                              \
         bool sl;                                                                    \
-        q[b] = div_fast(tc + TC * b == e ? 1.0 : T[x][b], pe, sl);                  \
+        q[b] = div_with(tc + TC * b == e ? 1.0 : T[x][b], pe, rpe, sl);             \
         slow_any |= sl;                                                             \
       }                                                                             \
       if (slow_any) {                                                               \
@@ -501,7 +502,7 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
 #undef LPB_PROW
         if (tc == 0) {
           bool sl;
-          const double q = div_fast(sm.rhs[lw], pe, sl);
+          const double q = div_with(sm.rhs[lw], pe, rpe, sl);
           sm.prr[par][w] = sl ? __ddiv_rn(sm.rhs[lw], pe) : q;
         }
       }
