@@ -81,6 +81,14 @@ __device__ __forceinline__ int warp_argmin(bool valid, unsigned long long k, uns
   return __ffs(__ballot_sync(FULL, c2 && tie == mt)) - 1;
 }
 
+// st.shared through inline PTX: keeps a store inside its switch case (the compiler would
+// otherwise sink identical stores out of the cases and insert register copies to merge them)
+__device__ __forceinline__ void sts64(double* p, double v) {
+  asm volatile("st.shared.f64 [%0], %1;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(p))),
+               "d"(v)
+               : "memory");
+}
+
 // Barrier of the LP's thread group.
 template <int NT>
 __device__ __forceinline__ void gsync() {
@@ -417,23 +425,38 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
       const int be = e / TC, etc = e - be * TC;
       double* colE = sm.colE[par];
       if (tc == etc) {
+        double* cE = colE + tr;
 #define LPB_PUB(x)                                                                    \
   case x:                                                                             \
     if constexpr ((x) < BC) {                                                         \
       _Pragma("unroll") for (int ai = 0; ai < A; ++ai) {                             \
-        colE[tr + TR * ai] = T[ai][x];                                                \
+        sts64(cE + TR * ai, T[ai][x]);                                                \
         T[ai][x] = 0.0;                                                               \
       }                                                                               \
-      if (tr == 0) {                                                                  \
-        sm.fobj[par][0] = d2[x];                                                      \
-        if constexpr (TWO) sm.fobj[par][1] = d1[x];                                   \
-      }                                                                               \
-      d2[x] = 0.0;                                                                    \
-      if constexpr (TWO) d1[x] = 0.0;                                                 \
     }                                                                                 \
     break;
         switch (be) { LPB_CASES(LPB_PUB) default: break; }
 #undef LPB_PUB
+        // objective-row entries of column e (register selects, no dynamic indexing)
+        if (tr == 0) {
+          double v2 = d2[0], v1 = TWO ? d1[0] : 0.0;
+#pragma unroll
+          for (int b = 1; b < BC; ++b) {
+            v2 = (b == be) ? d2[b] : v2;
+            if constexpr (TWO) v1 = (b == be) ? d1[TWO ? b : 0] : v1;
+          }
+          sm.fobj[par][0] = v2;
+          if constexpr (TWO) sm.fobj[par][1] = v1;
+        }
+      }
+      {  // zero position e in the replicas (owner lanes) so the update swaps the column in
+        const bool own_e = (tc == etc);
+#pragma unroll
+        for (int b = 0; b < BC; ++b) {
+          const bool z = own_e && (b == be);
+          d2[b] = z ? 0.0 : d2[b];
+          if constexpr (TWO) d1[TWO ? b : 0] = z ? 0.0 : d1[TWO ? b : 0];
+        }
       }
       __syncwarp();
       LPB_PROF_MARK(1)
@@ -480,30 +503,35 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
         const double pe = colE[lw];
         const double rpe = recip_of(pe);  // one MUFU op for the whole row
         const int al = lw / TR;
-        double* ps = sm.pslot[par][w];
+        double* ps = sm.pslot[par][w] + tc;
+        bool slow_any = false;
 #define LPB_PROW(x)                                                                 \
   case x:                                                                           \
     if constexpr ((x) < A) {                                                        \
-      bool slow_any = false;                                                        \
-      double q[BC];                                                                 \
       _Pragma("unroll") for (int b = 0; b < BC; ++b) {                              \
         bool sl;                                                                    \
-        q[b] = div_with(tc + TC * b == e ? 1.0 : T[x][b], pe, rpe, sl);             \
+        sts64(ps + TC * b, div_with(tc + TC * b == e ? 1.0 : T[x][b], pe, rpe, sl)); \
         slow_any |= sl;                                                             \
       }                                                                             \
-      if (slow_any) {                                                               \
-        _Pragma("unroll") for (int b = 0; b < BC; ++b)                              \
-          q[b] = __ddiv_rn(tc + TC * b == e ? 1.0 : T[x][b], pe);                   \
-      }                                                                             \
-      _Pragma("unroll") for (int b = 0; b < BC; ++b) ps[tc + TC * b] = q[b];        \
     }                                                                               \
     break;
         switch (al) { LPB_CASES(LPB_PROW) default: break; }
 #undef LPB_PROW
+        if (slow_any) {  // rare: a quotient outside the fast range -> IEEE slow path
+#define LPB_PROWS(x)                                                                \
+  case x:                                                                           \
+    if constexpr ((x) < A) {                                                        \
+      _Pragma("unroll") for (int b = 0; b < BC; ++b)                                \
+        sts64(ps + TC * b, __ddiv_rn(tc + TC * b == e ? 1.0 : T[x][b], pe));        \
+    }                                                                               \
+    break;
+          switch (al) { LPB_CASES(LPB_PROWS) default: break; }
+#undef LPB_PROWS
+        }
         if (tc == 0) {
           bool sl;
-          const double q = div_with(sm.rhs[lw], pe, rpe, sl);
-          sm.prr[par][w] = sl ? __ddiv_rn(sm.rhs[lw], pe) : q;
+          const double q0 = div_with(sm.rhs[lw], pe, rpe, sl);
+          sm.prr[par][w] = sl ? __ddiv_rn(sm.rhs[lw], pe) : q0;
         }
       }
       if (lane == 0) sm.part[par][w] = Part{thw, tiew, lw, lw >= 0 ? sm.bkey[lw] : 0, 0};
