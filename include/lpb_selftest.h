@@ -19,9 +19,8 @@ extern "C" {
 int lpb_selftest_div(const double* a, const double* b, double* q, int64_t n, int64_t* out);
 
 /* lpb_set_profile_buffer: diagnostics for the register-resident simplex kernel.  dev_buf is a
- * device array of (grid CTAs x 8) int64 cycle counters, zeroed by the caller, or NULL (off).
- * Warp 0 of each CTA accumulates clock64() time per pivot phase: 0 Step 1, 1 publish column,
- * 2 ratio test, 3 barrier-1 wait, 4 partial reduce, 5 pivot row, 6 barrier-2 wait, 7 update.
+ * device array of (grid CTAs x 12) int64 cycle counters, zeroed by the caller, or NULL (off).
+ * Warp 0 of each CTA accumulates clock64() time per pivot phase (see csrc/simplex_reg.cu).
  * The context pointer type is the opaque lpb_ctx of lpb.h.  Returns LPB_OK / LPB_EINVAL. */
 struct lpb_ctx;
 int lpb_set_profile_buffer(struct lpb_ctx* c, long long* dev_buf);

@@ -154,7 +154,7 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
   const bool rlane = lane < RPW * A;
   const int m = a.m, n = a.n;
   const bool prof_on = a.prof != nullptr && w == 0;
-  long long pacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long pacc[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   long long pt = clock64();
 
   double T[A][BC];
@@ -484,6 +484,7 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
           }
         }
       }
+      LPB_PROF_MARK(8)
       int lw = -1;
       double thw = 0.0;
       int tiew = INT_MAX;
@@ -497,6 +498,7 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
       } else if ((l % TR) / RPW == w) {
         lw = l;  // the drive-out row belongs to this warp
       }
+      LPB_PROF_MARK(9)
       __syncwarp();  // the lazily updated rhs[lw] is visible to the warp
       // Step 3 (speculative): the thread-row holding lw scales it by PE
       if (lw >= 0 && tr == lw % TR) {
@@ -534,6 +536,7 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
           sm.prr[par][w] = sl ? __ddiv_rn(sm.rhs[lw], pe) : q0;
         }
       }
+      LPB_PROF_MARK(10)
       if (lane == 0) sm.part[par][w] = Part{thw, tiew, lw, lw >= 0 ? sm.bkey[lw] : 0, 0};
       LPB_PROF_MARK(2)
       gsync<NT>();  // the pivot's only block barrier
@@ -656,7 +659,7 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
     gsync<NT>();
   }
   if (prof_on && lane == 0)
-    for (int q = 0; q < 8; ++q) atomicAdd((unsigned long long*)&a.prof[blockIdx.x * 8 + q], (unsigned long long)pacc[q]);
+    for (int q = 0; q < 12; ++q) atomicAdd((unsigned long long*)&a.prof[blockIdx.x * 12 + q], (unsigned long long)pacc[q]);
 }
 
 struct RegCfg {

@@ -11,15 +11,15 @@ A, b, c = lpgen.make_config(name, int(B))
 At, bt, ct = (torch.from_numpy(v).cuda() for v in (A, b, c))
 s = lpb.Solver(*A.shape, lpb.GENERAL, kernel_class='R')
 s.solve_device(At, bt, ct, sync=True)
-buf = torch.zeros(4096 * 8, dtype=torch.int64, device='cuda')
+buf = torch.zeros(4096 * 12, dtype=torch.int64, device='cuda')
 lpb._lib.lpb_set_profile_buffer(s._ctx, ctypes.c_void_p(buf.data_ptr()))
 s.solve_device(At, bt, ct, sync=True)
 ms = s.timing()[0]
 r = s.device_results()
 piv = r['iters'].sum().item()
-p = buf.view(-1, 8).sum(0).cpu().numpy().astype(float)
-names = ['step1', 'publish', 'ratio', 'bar1', 'reduce', 'prow', 'bar2', 'update+build']
-ctas = (buf.view(-1, 8).sum(1) > 0).sum().item()
+p = buf.view(-1, 12).sum(0).cpu().numpy().astype(float)
+names = ['step1', 'publish', 'part_write', 'barrier', 'reduce', 'bookkeep', 'update', 'loophead', 'ratio_lanes', 'ratio_argmin', 'spec_prow', '-']
+ctas = (buf.view(-1, 12).sum(1) > 0).sum().item()
 print(f'{name} B={B} ms={ms:.3f} pivots={piv} ctas={ctas}')
 tot = p.sum()
 for nm, v in zip(names, p):
