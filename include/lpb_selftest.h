@@ -30,6 +30,10 @@ int lpb_set_profile_buffer(struct lpb_ctx* c, long long* dev_buf);
  * [1] 5-round shuffle argmax, [2] div_fast, [3] DFMA, [4] __syncthreads, [5] SHFL,
  * [6] REDUX, [7] DSETP+select scan step; out[8] is a checksum.  Returns LPB_OK / LPB_ECUDA. */
 int lpb_selftest_latency(int threads, long long* out9);
+
+/* lpb_selftest_prow: cycles per iteration of the pivot-row scaling step in three forms
+ * (switch + inline-PTX stores, select chain, divisions only).  Returns LPB_OK / LPB_ECUDA. */
+int lpb_selftest_prow(long long* out3);
 #ifdef __cplusplus
 }
 #endif

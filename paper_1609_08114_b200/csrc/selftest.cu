@@ -141,3 +141,79 @@ extern "C" int lpb_selftest_latency(int threads, long long* out9) {
   cudaFree(d_out);
   return e == cudaSuccess ? LPB_OK : LPB_ECUDA;
 }
+
+// ---- micro-benchmark of the speculative pivot-row step (switch on a row slot + 7 divisions)
+namespace {
+#define MB_CASES(BODY) BODY(0) BODY(1) BODY(2) BODY(3) BODY(4) BODY(5) BODY(6) BODY(7) BODY(8) \
+  BODY(9) BODY(10) BODY(11) BODY(12)
+__device__ __forceinline__ void mb_sts64(double* p, double v) {
+  asm volatile("st.shared.f64 [%0], %1;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(p))),
+               "d"(v) : "memory");
+}
+template <int VARIANT>
+__global__ void prow_bench(const double* in, long long* out, int iters) {
+  __shared__ double ps[16 * 8];
+  double T[13][7];
+#pragma unroll
+  for (int a = 0; a < 13; ++a)
+#pragma unroll
+    for (int b = 0; b < 7; ++b) T[a][b] = in[(a * 7 + b) & 127] + a + b;
+  const int tc = threadIdx.x & 15;
+  double pe = 1.7 + in[0];
+  long long t0 = clock64();
+  for (int it = 0; it < iters; ++it) {
+    const int al = __shfl_sync(0xffffffffu, it % 13, 0);
+    const double rpe = lpb::recip_of(pe);
+    bool slow_any = false;
+    if (VARIANT == 0) {  // switch + asm stores (the kernel's form)
+#define MB_PROW(x) case x: { _Pragma("unroll") for (int b = 0; b < 7; ++b) { bool sl; \
+      mb_sts64(ps + tc + 16 * b, lpb::div_with(T[x][b], pe, rpe, sl)); slow_any |= sl; } } break;
+      switch (al) { MB_CASES(MB_PROW) default: break; }
+#undef MB_PROW
+    } else if (VARIANT == 1) {  // select chain, plain stores
+      double q[7];
+#pragma unroll
+      for (int b = 0; b < 7; ++b) {
+        double v = T[0][b];
+#pragma unroll
+        for (int a = 1; a < 13; ++a) v = (a == al) ? T[a][b] : v;
+        bool sl;
+        q[b] = lpb::div_with(v, pe, rpe, sl);
+        slow_any |= sl;
+      }
+#pragma unroll
+      for (int b = 0; b < 7; ++b) ps[tc + 16 * b] = q[b];
+    } else {  // divisions only (no row selection)
+#pragma unroll
+      for (int b = 0; b < 7; ++b) {
+        bool sl;
+        ps[tc + 16 * b] = lpb::div_with(T[3][b], pe, rpe, sl);
+        slow_any |= sl;
+      }
+    }
+    if (slow_any) ps[0] = 0.0;
+    __syncwarp();
+    pe = pe + ps[(tc + it) & 127] * 1e-30;
+#pragma unroll
+    for (int b = 0; b < 7; ++b) T[it % 13 == 5 ? 5 : 6][b] += 1e-300;  // keep T live
+  }
+  long long t1 = clock64();
+  if (threadIdx.x == 0) out[VARIANT] = (t1 - t0) / iters;
+  if (threadIdx.x == 1) out[8 + VARIANT] = (long long)(pe + T[5][3]);
+}
+}  // namespace
+
+extern "C" int lpb_selftest_prow(long long* out3) {
+  double* d_in = nullptr;
+  long long* d_out = nullptr;
+  if (cudaMalloc(&d_in, 128 * sizeof(double)) != cudaSuccess) return LPB_ECUDA;
+  cudaMalloc(&d_out, 16 * sizeof(long long));
+  cudaMemset(d_in, 0, 128 * sizeof(double));
+  prow_bench<0><<<1, 128>>>(d_in, d_out, 500);
+  prow_bench<1><<<1, 128>>>(d_in, d_out, 500);
+  prow_bench<2><<<1, 128>>>(d_in, d_out, 500);
+  const cudaError_t e = cudaMemcpy(out3, d_out, 3 * sizeof(long long), cudaMemcpyDeviceToHost);
+  cudaFree(d_in);
+  cudaFree(d_out);
+  return e == cudaSuccess ? LPB_OK : LPB_ECUDA;
+}

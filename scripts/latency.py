@@ -7,3 +7,6 @@ for th in (32, 128, 256):
     out = (ctypes.c_longlong * 9)()
     rc = lpb._lib.lpb_selftest_latency(th, out)
     print(th, rc, {k: out[i] for i, k in enumerate(names)})
+lpb._lib.lpb_selftest_prow.argtypes = [ctypes.POINTER(ctypes.c_longlong)]
+out = (ctypes.c_longlong * 3)()
+print('prow switch/select/divonly', lpb._lib.lpb_selftest_prow(out), list(out))
