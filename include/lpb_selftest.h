@@ -34,6 +34,10 @@ int lpb_selftest_latency(int threads, long long* out9);
 /* lpb_selftest_prow: cycles per iteration of the pivot-row scaling step in three forms
  * (switch + inline-PTX stores, select chain, divisions only).  Returns LPB_OK / LPB_ECUDA. */
 int lpb_selftest_prow(long long* out3);
+
+/* lpb_selftest_fp64_peak: measured FP64 FMA throughput (TFLOP/s, 2 flop per DFMA) and
+ * MUFU.RCP64H throughput (G ops/s) on the current device.  Returns LPB_OK / LPB_ECUDA. */
+int lpb_selftest_fp64_peak(double* dfma_tflops, double* rcp_gops);
 #ifdef __cplusplus
 }
 #endif

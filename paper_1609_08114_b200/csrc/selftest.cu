@@ -217,3 +217,65 @@ extern "C" int lpb_selftest_prow(long long* out3) {
   cudaFree(d_out);
   return e == cudaSuccess ? LPB_OK : LPB_ECUDA;
 }
+
+// ---- FP64 pipe throughput (DFMA) and MUFU.RCP64H throughput, measured with events ----
+namespace {
+__global__ void dfma_tput(double* out, int iters) {
+  double a0 = threadIdx.x * 1e-3, a1 = a0 + 1, a2 = a0 + 2, a3 = a0 + 3, a4 = a0 + 4,
+         a5 = a0 + 5, a6 = a0 + 6, a7 = a0 + 7;
+  const double m = 0.999999, c = 1e-7;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      a0 = __fma_rn(a0, m, c); a1 = __fma_rn(a1, m, c); a2 = __fma_rn(a2, m, c);
+      a3 = __fma_rn(a3, m, c); a4 = __fma_rn(a4, m, c); a5 = __fma_rn(a5, m, c);
+      a6 = __fma_rn(a6, m, c); a7 = __fma_rn(a7, m, c);
+    }
+  }
+  if (a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7 == 12345.0) out[0] = a0;
+}
+__global__ void rcp_tput(double* out, int iters) {
+  double a0 = 1.5 + threadIdx.x * 1e-3, a1 = a0 + 1, a2 = a0 + 2, a3 = a0 + 3;
+  for (int i = 0; i < iters; ++i) {
+    double r0, r1, r2, r3;
+    asm volatile("rcp.approx.ftz.f64 %0, %1;" : "=d"(r0) : "d"(a0));
+    asm volatile("rcp.approx.ftz.f64 %0, %1;" : "=d"(r1) : "d"(a1));
+    asm volatile("rcp.approx.ftz.f64 %0, %1;" : "=d"(r2) : "d"(a2));
+    asm volatile("rcp.approx.ftz.f64 %0, %1;" : "=d"(r3) : "d"(a3));
+    a0 = r0 + 1.0; a1 = r1 + 1.0; a2 = r2 + 1.0; a3 = r3 + 1.0;
+  }
+  if (a0 + a1 + a2 + a3 == 12345.0) out[0] = a0;
+}
+}  // namespace
+
+extern "C" int lpb_selftest_fp64_peak(double* dfma_tflops, double* rcp_gops) {
+  double* d = nullptr;
+  if (cudaMalloc(&d, 64) != cudaSuccess) return LPB_ECUDA;
+  int sms = 0, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const int blocks = sms * 4, threads = 512, iters = 4096;
+  dfma_tput<<<blocks, threads>>>(d, 64);  // warm up
+  cudaEventRecord(e0);
+  dfma_tput<<<blocks, threads>>>(d, iters);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  *dfma_tflops = 2.0 * 32.0 * iters * (double)blocks * threads / (ms * 1e-3) / 1e12;
+  rcp_tput<<<blocks, threads>>>(d, 64);
+  cudaEventRecord(e0);
+  rcp_tput<<<blocks, threads>>>(d, iters);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  cudaEventElapsedTime(&ms, e0, e1);
+  *rcp_gops = 4.0 * iters * (double)blocks * threads / (ms * 1e-3) / 1e9;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  const cudaError_t err = cudaGetLastError();
+  cudaFree(d);
+  return err == cudaSuccess ? LPB_OK : LPB_ECUDA;
+}

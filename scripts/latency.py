@@ -10,3 +10,6 @@ for th in (32, 128, 256):
 lpb._lib.lpb_selftest_prow.argtypes = [ctypes.POINTER(ctypes.c_longlong)]
 out = (ctypes.c_longlong * 3)()
 print('prow switch/select/divonly', lpb._lib.lpb_selftest_prow(out), list(out))
+lpb._lib.lpb_selftest_fp64_peak.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]
+a, b = ctypes.c_double(), ctypes.c_double()
+print('fp64 peak', lpb._lib.lpb_selftest_fp64_peak(ctypes.byref(a), ctypes.byref(b)), 'DFMA TFLOP/s', a.value, 'RCP64H Gops', b.value)
