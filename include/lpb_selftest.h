@@ -28,7 +28,8 @@ int lpb_set_profile_buffer(struct lpb_ctx* c, long long* dev_buf);
 /* lpb_selftest_latency: one CTA of `threads` threads times dependent chains of the kernels'
  * building blocks with clock64 (cycles per step): out[0] REDUX (value,tie) warp argmax,
  * [1] 5-round shuffle argmax, [2] div_fast, [3] DFMA, [4] __syncthreads, [5] SHFL,
- * [6] REDUX, [7] DSETP+select scan step; out[8] is a checksum.  Returns LPB_OK / LPB_ECUDA. */
+ * [6] REDUX, [7] DSETP+select scan step, [9] recip_of, [10] MUFU.RCP64H+DADD; out[8] is a
+ * checksum (out must hold 11 values).  Returns LPB_OK / LPB_ECUDA. */
 int lpb_selftest_latency(int threads, long long* out9);
 
 /* lpb_selftest_prow: cycles per iteration of the pivot-row scaling step in three forms

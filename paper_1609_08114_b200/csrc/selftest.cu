@@ -125,7 +125,23 @@ __global__ void lat_kernel(const double* in, long long* out, int iters) {
   for (int i = 0; i < iters; ++i) { const double c = z + (double)i; bv2 = (c > bv2) ? c : bv2 * 0.5; }
   t1 = clock64();
   if (threadIdx.x == 0) out[7] = (t1 - t0) / iters;
-  if (threadIdx.x == 0) out[8] = acc + s + (int)r + (int)bv2 + (int)z;
+  // 8: dependent recip_of (MUFU.RCP64H + 4 DFMA)
+  t0 = clock64();
+  double rr = 1.5 + z * 1e-300;
+  for (int i = 0; i < iters; ++i) rr = lpb::recip_of(rr) + 1.0;
+  t1 = clock64();
+  if (threadIdx.x == 0) out[9] = (t1 - t0) / iters;
+  // 10: dependent MUFU.RCP64H alone
+  t0 = clock64();
+  double r0 = rr;
+  for (int i = 0; i < iters; ++i) {
+    double o;
+    asm volatile("rcp.approx.ftz.f64 %0, %1;" : "=d"(o) : "d"(r0));
+    r0 = o + 1.0;
+  }
+  t1 = clock64();
+  if (threadIdx.x == 0) out[10] = (t1 - t0) / iters;
+  if (threadIdx.x == 0) out[8] = acc + s + (int)r + (int)bv2 + (int)z + (int)rr + (int)r0;
 }
 }  // namespace
 
@@ -136,7 +152,7 @@ extern "C" int lpb_selftest_latency(int threads, long long* out9) {
   cudaMalloc(&d_out, 16 * sizeof(long long));
   cudaMemset(d_in, 0, 1024 * sizeof(double));
   lat_kernel<<<1, threads>>>(d_in, d_out, 1000);
-  const cudaError_t e = cudaMemcpy(out9, d_out, 9 * sizeof(long long), cudaMemcpyDeviceToHost);
+  const cudaError_t e = cudaMemcpy(out9, d_out, 11 * sizeof(long long), cudaMemcpyDeviceToHost);
   cudaFree(d_in);
   cudaFree(d_out);
   return e == cudaSuccess ? LPB_OK : LPB_ECUDA;

@@ -2,9 +2,9 @@ import ctypes, sys
 sys.path.insert(0, '.')
 from paper_1609_08114_b200 import lpb
 lpb._lib.lpb_selftest_latency.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_longlong)]
-names = ['redux_argmax', 'shfl_argmax', 'div_fast', 'dfma', 'syncthreads', 'shfl', 'redux', 'dsetp_sel']
+names = ['redux_argmax', 'shfl_argmax', 'div_fast', 'dfma', 'syncthreads', 'shfl', 'redux', 'dsetp_sel', 'chk', 'recip_of', 'rcp64h']
 for th in (32, 128, 256):
-    out = (ctypes.c_longlong * 9)()
+    out = (ctypes.c_longlong * 11)()
     rc = lpb._lib.lpb_selftest_latency(th, out)
     print(th, rc, {k: out[i] for i, k in enumerate(names)})
 lpb._lib.lpb_selftest_prow.argtypes = [ctypes.POINTER(ctypes.c_longlong)]
