@@ -102,8 +102,11 @@ __device__ __forceinline__ void gsync() {
   BODY(20) BODY(21) BODY(22) BODY(23) BODY(24) BODY(25) BODY(26) BODY(27) BODY(28)         \
   BODY(29) BODY(30) BODY(31)
 
-struct Part {  // a (value, tie, index) reduction partial
+struct Part {  // a (value, tie, index) reduction partial of the ratio test
   double v;
+  double pe;   // pivot element candidate colE[idx]
+  double rcp;  // its refined reciprocal (shared by every division of the pivot row)
+  double rhs;  // rhs[idx] (lazily updated)
   int tie;
   int idx;
   int leave;  // basis key of row idx (the leaving variable if idx wins)
@@ -118,8 +121,7 @@ struct RegSmem {
   double fobj[2][2];     // pivot-column entries of the phase-II / phase-I rows
   double rhs[RCAP];      // RHS column (lazily updated)
   double prow[CCAP];     // scratch for the phase-I row at build
-  double pslot[2][NWARP][CCAP];  // each warp's speculative scaled pivot row (its candidate)
-  double prr[2][NWARP];          // ... and its RHS / PE
+  double pslot[2][NWARP][CCAP];  // each warp's candidate pivot row (unscaled)
   int bkey[RCAP];        // row -> basic variable key (>= 0 real, < 0 artificial)
   int nbvar[NWARP][CCAP];  // position -> nonbasic variable index, one copy per warp
   int negrows[RCAP];     // ascending rows with b_i < 0
@@ -464,7 +466,7 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
       // also writes its row's update multiplier f_i = -colE_i
       const int ri = rrow;
       bool rval = false;
-      double ratio = 0.0;
+      double ratio = 0.0, rrhs = 0.0, rpe = 1.0, rrcp = 1.0;
       int rtie = INT_MAX;
       if (rlane) {
         const double v = colE[ri];
@@ -475,87 +477,69 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
             r = (ri == l_prev) ? prr_prev : __fma_rn(sm.fcol[par ^ 1][ri], prr_prev, r);
             sm.rhs[ri] = r;
           }
+          rrhs = r;
+          rpe = v;
+          rrcp = recip_of(v);
           if (!drive) {
             rval = v > a.eps_piv;
             bool slow;
-            ratio = div_fast(r, rval ? v : 1.0, slow);
-            if (slow) ratio = __ddiv_rn(r, rval ? v : 1.0);  // rare: outside the fast range
+            ratio = div_with(r, v, rrcp, slow);
+            if (slow || !rval) ratio = __ddiv_rn(r, rval ? v : 1.0);  // rare / non-candidate
             rtie = bland ? sm.bkey[ri] : ri;
           }
         }
       }
       LPB_PROF_MARK(8)
       int lw = -1;
-      double thw = 0.0;
-      int tiew = INT_MAX;
       if (!drive) {
         const int wl = warp_argmin(rval, okey(ratio), ikey(rtie));
         if (wl >= 0) {
           lw = __shfl_sync(FULL, ri, wl);
-          thw = __shfl_sync(FULL, ratio, wl);
-          tiew = __shfl_sync(FULL, rtie, wl);
+          if (lane == wl)  // the winning lane publishes the warp's partial itself
+            sm.part[par][w] = Part{ratio, rpe, rrcp, rrhs, rtie, ri, sm.bkey[ri], 0};
+        } else if (lane == 0) {
+          sm.part[par][w] = Part{0.0, 1.0, 1.0, 0.0, INT_MAX, -1, 0, 0};
         }
       } else if ((l % TR) / RPW == w) {
         lw = l;  // the drive-out row belongs to this warp
+        if (rlane && ri == l) sm.part[par][w] = Part{0.0, rpe, rrcp, rrhs, 0, l, sm.bkey[l], 0};
       }
       LPB_PROF_MARK(9)
-      __syncwarp();  // the lazily updated rhs[lw] is visible to the warp
-      // Step 3 (speculative): the thread-row holding lw scales it by PE
+      // Step 3 (speculative part): the thread-row holding lw publishes its row (unscaled;
+      // the winning row is divided by PE after the barrier, by every thread for its own
+      // positions)
       if (lw >= 0 && tr == lw % TR) {
-        const double pe = colE[lw];
-        const double rpe = recip_of(pe);  // one MUFU op for the whole row
         const int al = lw / TR;
         double* ps = sm.pslot[par][w] + tc;
-        bool slow_any = false;
-#define LPB_PROW(x)                                                                 \
-  case x:                                                                           \
-    if constexpr ((x) < A) {                                                        \
-      _Pragma("unroll") for (int b = 0; b < BC; ++b) {                              \
-        bool sl;                                                                    \
-        sts64(ps + TC * b, div_with(tc + TC * b == e ? 1.0 : T[x][b], pe, rpe, sl)); \
-        slow_any |= sl;                                                             \
-      }                                                                             \
-    }                                                                               \
-    break;
-        switch (al) { LPB_CASES(LPB_PROW) default: break; }
-#undef LPB_PROW
-        if (slow_any) {  // rare: a quotient outside the fast range -> IEEE slow path
-#define LPB_PROWS(x)                                                                \
+#define LPB_ROWPUB(x)                                                               \
   case x:                                                                           \
     if constexpr ((x) < A) {                                                        \
       _Pragma("unroll") for (int b = 0; b < BC; ++b)                                \
-        sts64(ps + TC * b, __ddiv_rn(tc + TC * b == e ? 1.0 : T[x][b], pe));        \
+        sts64(ps + TC * b, tc + TC * b == e ? 1.0 : T[x][b]);                       \
     }                                                                               \
     break;
-          switch (al) { LPB_CASES(LPB_PROWS) default: break; }
-#undef LPB_PROWS
-        }
-        if (tc == 0) {
-          bool sl;
-          const double q0 = div_with(sm.rhs[lw], pe, rpe, sl);
-          sm.prr[par][w] = sl ? __ddiv_rn(sm.rhs[lw], pe) : q0;
-        }
+        switch (al) { LPB_CASES(LPB_ROWPUB) default: break; }
+#undef LPB_ROWPUB
       }
       LPB_PROF_MARK(10)
-      if (lane == 0) sm.part[par][w] = Part{thw, tiew, lw, lw >= 0 ? sm.bkey[lw] : 0, 0};
       LPB_PROF_MARK(2)
       gsync<NT>();  // the pivot's only block barrier
       LPB_PROF_MARK(3)
       // Step 2c: the winning warp partial (argmin of the ratios), read by every warp
       double theta = 0.0;
-      int ww, leaving;
+      int ww;
       if (!drive) {
-        const Part q = (lane < NWARP) ? sm.part[par][lane] : Part{0.0, INT_MAX, -1, 0, 0};
+        const Part q = (lane < NWARP) ? sm.part[par][lane] : Part{0.0, 1.0, 1.0, 0.0, INT_MAX, -1, 0, 0};
         const int ql = warp_argmin(q.idx >= 0, okey(q.v), ikey(q.tie));
         if (ql < 0) { st = (phase == 2) ? ST_UNBOUNDED : ST_NUMERICAL; break; }
         ww = ql;
-        l = __shfl_sync(FULL, q.idx, ql);
-        theta = __shfl_sync(FULL, q.v, ql);
-        leaving = __shfl_sync(FULL, q.leave, ql);
       } else {
         ww = (l % TR) / RPW;
-        leaving = sm.part[par][ww].leave;
       }
+      const Part& win = sm.part[par][ww];  // broadcast SMEM reads of the winning partial
+      l = win.idx;
+      theta = win.v;
+      const int leaving = win.leave;
       LPB_PROF_MARK(4)
       // bookkeeping: per-warp nbvar copy; the winning warp owns row l (bkey, fcol, zeroing)
       if (lane == 0) nbv[e] = leaving >= 0 ? leaving : DEADV;
@@ -579,11 +563,23 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
       __syncwarp();
       LPB_PROF_MARK(5)
       {
-        const double* pslw = sm.pslot[par][ww];
-        const double prr = sm.prr[par][ww];
+        // the pivot row divided by PE (IEEE, one shared reciprocal)
+        const double* pslw = sm.pslot[par][ww] + tc;
         double pv[BC];
+        bool slow_any = false;
 #pragma unroll
-        for (int b = 0; b < BC; ++b) pv[b] = pslw[tc + TC * b];
+        for (int b = 0; b < BC; ++b) {
+          bool sl;
+          pv[b] = div_with(pslw[TC * b], win.pe, win.rcp, sl);
+          slow_any |= sl;
+        }
+        if (slow_any) {  // rare: outside the fast range -> IEEE slow path
+#pragma unroll
+          for (int b = 0; b < BC; ++b) pv[b] = __ddiv_rn(pslw[TC * b], win.pe);
+        }
+        bool slr;
+        double prr = div_with(win.rhs, win.pe, win.rcp, slr);
+        if (slr) prr = __ddiv_rn(win.rhs, win.pe);
         const double f2 = -sm.fobj[par][0];
         const bool upd1 = TWO && phase == 1;
         const double f1 = TWO ? -sm.fobj[par][1] : 0.0;
