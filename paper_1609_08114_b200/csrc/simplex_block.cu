@@ -30,6 +30,7 @@
 
 #include "lpb_fp64.cuh"
 #include "lpb_internal.cuh"
+#include "lpb_reduce.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -58,17 +59,21 @@ __device__ __forceinline__ bool better(const Cand& a, const Cand& b) {
   return a.v < b.v || (a.v == b.v && a.key < b.key);
 }
 
+// Warp (value, key) reduction over the lanes' candidates (pos < 0: none), identical result
+// in every lane; REDUX-based (lpb_reduce.cuh) with the MODE's order.
 template <int MODE>
 __device__ __forceinline__ Cand warp_reduce(Cand c) {
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) {
-    Cand o;
-    o.v = __shfl_xor_sync(FULL, c.v, off);
-    o.key = __shfl_xor_sync(FULL, c.key, off);
-    o.pos = __shfl_xor_sync(FULL, c.pos, off);
-    if (better<MODE>(o, c)) c = o;
-  }
-  return c;
+  const bool valid = c.pos >= 0;
+  int wl;
+  if (MODE == MAX_V) wl = warp_argmax(valid, okey(c.v), (unsigned)c.key);
+  else if (MODE == MIN_KEY) wl = warp_argmin(valid, 0ull, ikey(c.key));
+  else wl = warp_argmin(valid, okey(c.v), ikey(c.key));
+  if (wl < 0) return Cand{0.0, 0, -1};
+  Cand r;
+  r.v = __shfl_sync(FULL, c.v, wl);
+  r.key = __shfl_sync(FULL, c.key, wl);
+  r.pos = __shfl_sync(FULL, c.pos, wl);
+  return r;
 }
 
 struct Ctl {

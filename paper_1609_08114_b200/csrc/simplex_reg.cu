@@ -27,6 +27,7 @@
 #include "lpb_async.cuh"
 #include "lpb_fp64.cuh"
 #include "lpb_internal.cuh"
+#include "lpb_reduce.cuh"
 
 namespace lpb {
 namespace {
@@ -37,49 +38,6 @@ constexpr int DEADV = INT_MAX;
 __device__ __forceinline__ double neg_inf() { return __longlong_as_double(0xfff0000000000000ll); }
 __device__ __forceinline__ double pos_inf() { return __longlong_as_double(0x7ff0000000000000ll); }
 __device__ __forceinline__ double qnan() { return __longlong_as_double(0x7ff8000000000000ll); }
-
-// Order-preserving 64-bit key of a double; -0.0 is folded to +0.0 first so that IEEE
-// equality (-0 == +0) remains a tie, as in the oracle's comparisons.
-__device__ __forceinline__ unsigned long long okey(double d) {
-  const unsigned long long u = (unsigned long long)__double_as_longlong(__dadd_rn(d, 0.0));
-  return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
-}
-__device__ __forceinline__ unsigned ikey(int t) { return (unsigned)t ^ 0x80000000u; }
-
-// Warp argmax of (key desc, tie asc) over lanes with `valid`; returns the winner lane or -1.
-// Must be called by all 32 lanes.  Fast path: one REDUX on the key's high word; only when
-// several lanes share it (rare for real-valued data) are the low word and the tie key
-// reduced as well.
-__device__ __forceinline__ int warp_argmax(bool valid, unsigned long long k, unsigned tie) {
-  const unsigned hi = valid ? (unsigned)(k >> 32) : 0u;
-  const unsigned mhi = __reduce_max_sync(FULL, hi);
-  const bool c1 = valid && hi == mhi;
-  const unsigned b1 = __ballot_sync(FULL, c1);
-  if (b1 == 0u) return -1;
-  if ((b1 & (b1 - 1u)) == 0u) return __ffs(b1) - 1;
-  const unsigned lo = c1 ? (unsigned)k : 0u;
-  const unsigned mlo = __reduce_max_sync(FULL, lo);
-  const bool c2 = c1 && (unsigned)k == mlo;
-  const unsigned t = c2 ? tie : 0xffffffffu;
-  const unsigned mt = __reduce_min_sync(FULL, t);
-  return __ffs(__ballot_sync(FULL, c2 && tie == mt)) - 1;
-}
-
-// Warp argmin of (key asc, tie asc) over lanes with `valid`; returns the winner lane or -1.
-__device__ __forceinline__ int warp_argmin(bool valid, unsigned long long k, unsigned tie) {
-  const unsigned hi = valid ? (unsigned)(k >> 32) : 0xffffffffu;
-  const unsigned mhi = __reduce_min_sync(FULL, hi);
-  const bool c1 = valid && hi == mhi;
-  const unsigned b1 = __ballot_sync(FULL, c1);
-  if (b1 == 0u) return -1;
-  if ((b1 & (b1 - 1u)) == 0u) return __ffs(b1) - 1;
-  const unsigned lo = c1 ? (unsigned)k : 0xffffffffu;
-  const unsigned mlo = __reduce_min_sync(FULL, lo);
-  const bool c2 = c1 && (unsigned)k == mlo;
-  const unsigned t = c2 ? tie : 0xffffffffu;
-  const unsigned mt = __reduce_min_sync(FULL, t);
-  return __ffs(__ballot_sync(FULL, c2 && tie == mt)) - 1;
-}
 
 // st.shared through inline PTX: keeps a store inside its switch case (the compiler would
 // otherwise sink identical stores out of the cases and insert register copies to merge them)
@@ -165,11 +123,13 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
   // the next LP's A is prefetched into SMEM (one bulk async copy) while this LP is solved
   extern __shared__ __align__(16) double abuf[];
   const bool pf = a.prefetch != 0;
+  const bool direct = a.ticket == nullptr;
   const uint32_t abytes = (uint32_t)((int64_t)m * n * 8);
   uint32_t mphase = 0;
   if (tid == 0) {
     mbar_init(&sm.mbar, 1);
-    const int t = atomicAdd(a.ticket, 1);
+    // direct mode (grid = batch, no ticket): CTA b solves LP b
+    const int t = direct ? (int)blockIdx.x : atomicAdd(a.ticket, 1);
     sm.lp = t;
     if (pf && t < a.batch) bulk_load(abuf, a.A + (int64_t)t * m * n, abytes, &sm.mbar);
   }
@@ -178,20 +138,28 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
   for (;;) {
     const int64_t lp = sm.lp;
     if (lp >= a.batch) break;
+    const double* __restrict__ bk = a.b + lp * (int64_t)m;
+    const double* __restrict__ ck = a.c + lp * (int64_t)n;
+    // issue the b and c loads before waiting for A (overlapping DRAM round trips)
+    const double b_pre = (tid < m) ? __ldg(bk + tid) : 0.0;
+    double c_pre[BC];
+#pragma unroll
+    for (int b = 0; b < BC; ++b) {
+      const int p = tc + TC * b;
+      c_pre[b] = (p < n) ? __ldg(ck + p) : 0.0;
+    }
     if (pf) {
       mbar_wait(&sm.mbar, mphase);
       mphase ^= 1u;
     }
     const double* __restrict__ Ak = pf ? abuf : a.A + lp * (int64_t)m * n;
-    const double* __restrict__ bk = a.b + lp * (int64_t)m;
-    const double* __restrict__ ck = a.c + lp * (int64_t)n;
 
     // ---- build: negated rows (ascending), basis keys, |b|_inf, RHS (R7) ----
     int k = 0;
     double binf = 0.0;
     for (int base = 0; base < m; base += NT) {
       const int i = base + tid;
-      const double bi = (i < m) ? __ldg(bk + i) : 0.0;
+      const double bi = (i < m) ? (base == 0 ? b_pre : __ldg(bk + i)) : 0.0;
       const bool neg = (i < m) && (bi < 0.0);
       binf = fmax(binf, fabs(bi));
       const unsigned bal = __ballot_sync(FULL, neg);
@@ -252,7 +220,7 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
 #pragma unroll
     for (int b = 0; b < BC; ++b) {
       const int p = tc + TC * b;
-      d2[b] = (p < n) ? __ldg(ck + p) : (p < npos ? 0.0 : neg_inf());
+      d2[b] = (p < n) ? c_pre[b] : (p < npos ? 0.0 : neg_inf());
     }
     double z2 = 0.0, z1 = 0.0;
     if constexpr (TWO) {
@@ -285,7 +253,7 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
     }
     gsync<NT>();  // A has been consumed: the buffer may be refilled with the next LP
     if (tid == 0) {
-      const int t = atomicAdd(a.ticket, 1);
+      const int t = direct ? (int)a.batch : atomicAdd(a.ticket, 1);
       sm.lp = t;
       if (pf && t < a.batch) bulk_load(abuf, a.A + (int64_t)t * m * n, abytes, &sm.mbar);
     }
@@ -690,10 +658,15 @@ cudaError_t launch_one(const SimplexArgs& a, int grid_override, cudaStream_t s, 
     cached_dsm = dsm;
   }
   int64_t grid = (int64_t)(per_sm < 1 ? 1 : per_sm) * device_sm_count();
+  SimplexArgs d = a;
+  if (a.batch <= grid && grid_override <= 0) {
+    d.ticket = nullptr;  // one resident wave: CTA b solves LP b, no ticket round trips
+    grid = a.batch;
+  }
   if (grid > a.batch) grid = a.batch;
   if (grid_override > 0) grid = grid_override;
   if (ctas) *ctas = (int)grid;
-  kern<<<(unsigned)grid, TR * TC, dsm, s>>>(a);
+  kern<<<(unsigned)grid, TR * TC, dsm, s>>>(d);
   return cudaGetLastError();
 }
 
