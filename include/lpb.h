@@ -90,8 +90,9 @@ typedef struct {
                           stream); NULL -> a non-blocking stream owned by the context          */
   int32_t n_chunks;    /* host-pointer pipeline depth; 0 -> 10 if batch > 100 else 1
                           (the paper's stream count)                            */
-  int32_t kernel_class;/* 0 auto; 1 S (thread/LP), 2 M (block/LP), 3 L (2-CTA cluster/LP),
-                          4 R (block/LP, register-resident tableau); for tests / benches     */
+  int32_t kernel_class;/* 0 auto; 1 S (thread/LP, m,n <= 8), 2 M (block/LP, SMEM tableau),
+                          3 L (2/4-CTA cluster/LP, DSMEM), 4 R (block or warp/LP, register-
+                          resident tableau); for tests / benches                           */
   int32_t grid_ctas;   /* 0 auto; persistent grid size override (scheduling-invariance tests) */
 } lpb_options;
 

@@ -111,8 +111,8 @@ extern "C" const char* lpb_last_error(lpb_ctx* c) { return c ? c->err : ""; }
 
 // Size-class capacity check at the best case (no artificial rows).
 static bool general_fits_any(int m, int n) {
-  return reg_fits(m, n, 0) || block_fits(1, m, n, 0) || block_fits(2, m, n, 0) ||
-         block_fits(4, m, n, 0);
+  return thread_fits(m, n) || reg_fits(m, n, 0) || block_fits(1, m, n, 0) ||
+         block_fits(2, m, n, 0) || block_fits(4, m, n, 0);
 }
 
 extern "C" int lpb_create(lpb_ctx** out, int64_t batch, int32_t m, int32_t n, int32_t kind,
@@ -205,7 +205,7 @@ static int choose_class(const lpb_ctx* c, int kmax, int* cl) {
   const int m = c->m, n = c->n;
   const int forced = c->opt.kernel_class;
   *cl = 1;
-  if (forced == CLASS_R || forced == CLASS_S) return reg_fits(m, n, kmax) ? CLASS_R : -1;
+  if (forced == CLASS_R) return reg_fits(m, n, kmax) ? CLASS_R : -1;
   if (forced == CLASS_M) return block_fits(1, m, n, kmax) ? CLASS_M : -1;
   if (forced == CLASS_L) {
     for (int q : {2, 4})
@@ -257,8 +257,23 @@ static int run_general(lpb_ctx* c, cudaStream_t s, int64_t lp0, int64_t cnt, con
                        int* ticket, int* launches) {
   int kmax = kmax_known;
   const int forced = c->opt.kernel_class;
+  if (forced == CLASS_S || (forced == CLASS_AUTO && thread_fits(c->m, c->n))) {
+    if (!thread_fits(c->m, c->n)) return LPB_ETOOBIG;
+    SimplexArgs a;  // worst-case width reserved: no prepass
+    fill_args(c, a, lp0, cnt, A, b, cv, nox, c->m, ticket);
+    const bool timed = (s == c->stream);
+    if (timed) LPB_CUDA(c, cudaEventRecord(c->kev0, s));
+    LPB_CUDA(c, launch_simplex_thread(a, s));
+    if (timed) {
+      LPB_CUDA(c, cudaEventRecord(c->kev1, s));
+      c->kev_valid = true;
+    }
+    *launches += 1;
+    c->last_class = CLASS_S;
+    return LPB_OK;
+  }
   const bool r_ok_worst = reg_fits(c->m, c->n, c->m);
-  if (kmax < 0 && r_ok_worst && (forced == CLASS_AUTO || forced == CLASS_R || forced == CLASS_S))
+  if (kmax < 0 && r_ok_worst && (forced == CLASS_AUTO || forced == CLASS_R))
     kmax = c->m;  // worst-case capacity, no prepass
   if (kmax < 0) {  // device prepass: kmax over the chunk (one tiny kernel + 4-byte D2H)
     LPB_CUDA(c, launch_count_art(b, cnt, c->m, c->d_kmax, s));

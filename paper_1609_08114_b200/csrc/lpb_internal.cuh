@@ -51,6 +51,10 @@ bool block_fits(int cl, int m, int n, int kmax);
 cudaError_t launch_simplex_block(int cl, const SimplexArgs& a, int grid_override,
                                  cudaStream_t s, int* ctas_out);
 
+// ---- S class: one LP per thread (tiny LPs), tableau in a thread-private SMEM slice ----
+bool thread_fits(int m, int n);
+cudaError_t launch_simplex_thread(const SimplexArgs& a, cudaStream_t s);
+
 // ---- R class: one LP per CTA (one warp for small LPs), tableau resident in registers ----
 bool reg_fits(int m, int n, int kmax);
 cudaError_t launch_simplex_reg(const SimplexArgs& a, int grid_override, cudaStream_t s,

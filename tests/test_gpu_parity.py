@@ -16,7 +16,7 @@ from gpu_util import compare, gpu_solve
 pytestmark = pytest.mark.gpu
 
 GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "lp_fixtures.json")))
-CLASSES = ["R", "M", "L"]
+CLASSES = ["S", "R", "M", "L"]
 
 
 def _reg_fits(m, n, k):
@@ -40,7 +40,7 @@ def test_golden_fixtures(klass):
 
 @pytest.mark.parametrize("klass", CLASSES)
 def test_klee_minty_and_chvatal(klass):
-    for n in range(2, 10):
+    for n in range(2, 9 if klass == "S" else 10):
         A, b, c = lpgen.klee_minty(n)
         A, b, c = A[None], b[None], c[None]
         g = gpu_solve(A, b, c, kernel_class=klass)
@@ -82,6 +82,8 @@ def test_random_batches(klass, gen, m, n, B):
     A, b, c = _gen(gen, B, m, n, 1000 + 7 * m + n)
     if klass == "R" and not _reg_fits(m, n, int((b < 0).sum(axis=1).max())):
         pytest.skip("no register layout for this size")
+    if klass == "S" and (m > 8 or n > 8):
+        pytest.skip("the thread-per-LP class holds m, n <= 8")
     o = oracle.solve(A, b, c)
     g = gpu_solve(A, b, c, kernel_class=klass)
     compare(A, b, c, g, o)
@@ -121,6 +123,7 @@ def test_scheduling_invariance_grid_and_class():
     A, b, c = lpgen.status_mix(1500, 16, 16, 6, infeasible_start=True)
     ref = gpu_solve(A, b, c, kernel_class="M")
     for kw in (dict(kernel_class="M", grid_ctas=1), dict(kernel_class="M", grid_ctas=37),
+               dict(kernel_class="R"), dict(kernel_class="R", grid_ctas=5),
                dict(kernel_class="L"), dict(kernel_class="L", grid_ctas=3)):
         g = gpu_solve(A, b, c, **kw)
         for k in ("status", "iters"):
