@@ -257,7 +257,11 @@ static int run_general(lpb_ctx* c, cudaStream_t s, int64_t lp0, int64_t cnt, con
                        int* ticket, int* launches) {
   int kmax = kmax_known;
   const int forced = c->opt.kernel_class;
-  if (forced == CLASS_S || (forced == CLASS_AUTO && thread_fits(c->m, c->n))) {
+  // S (thread per LP) wins on throughput once every SM has a few warps of LPs (measured: 3-4x
+  // over the warp-per-LP register layout at 1e5-1e6 LPs of 5x5); below that the warp-per-LP
+  // layout has the shorter per-LP latency (cfg1: 1000 LPs).
+  const bool s_auto = forced == CLASS_AUTO && thread_fits(c->m, c->n) && cnt >= 8192;
+  if (forced == CLASS_S || s_auto) {
     if (!thread_fits(c->m, c->n)) return LPB_ETOOBIG;
     SimplexArgs a;  // worst-case width reserved: no prepass
     fill_args(c, a, lp0, cnt, A, b, cv, nox, c->m, ticket);
