@@ -265,15 +265,21 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
     // SMEM traffic is warp-local (colE, fcol, rhs, bkey of a row are touched only by the
     // warp owning that row; nbvar has one copy per warp).
     int it1 = 0, it2 = 0, stall = 0, phase = (TWO && k > 0) ? 1 : 2;
-    int par = 0, l_prev = -1, dl = 0;
-    double prr_prev = 0.0;
-    bool pend = false, drive = false;
+    int par = 0, dl = 0;
+    bool drive = false;
+    bool have_e = false;  // Step 1 of this pivot was already done, fused into the last update
+    int e_next = -1, evar_next = 0;
     int* nbv = sm.nbvar[w];
     while (st < 0) {
       const bool bland = a.bland_K > 0 && stall >= a.bland_K;
       const bool p1 = TWO && phase == 1;
       int e = -1, evar = 0, l = -1;
-      if (drive) {
+      if (!drive && have_e) {
+        have_e = false;
+        if (it1 + it2 >= a.max_iter) { st = ST_ITER_LIMIT; break; }
+        e = e_next;
+        evar = evar_next;
+      } else if (drive) {
         // phase switch (R9): drive the next basic artificial out on max |T[l][p]|
         while (dl < m && sm.bkey[dl] >= 0) ++dl;
         if (dl >= m) {
@@ -430,8 +436,8 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
       }
       __syncwarp();
       LPB_PROF_MARK(1)
-      // Step 2b: lane-parallel lazy RHS update + ratio test over the warp's rows; each lane
-      // also writes its row's update multiplier f_i = -colE_i
+      // Step 2b: lane-parallel ratio test over the warp's rows; each lane also writes its
+      // row's update multiplier f_i = -colE_i
       const int ri = rrow;
       bool rval = false;
       double ratio = 0.0, rrhs = 0.0, rpe = 1.0, rrcp = 1.0;
@@ -440,11 +446,7 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
         const double v = colE[ri];
         sm.fcol[par][ri] = -v;
         if (ri < m) {
-          double r = sm.rhs[ri];
-          if (pend) {
-            r = (ri == l_prev) ? prr_prev : __fma_rn(sm.fcol[par ^ 1][ri], prr_prev, r);
-            sm.rhs[ri] = r;
-          }
+          const double r = sm.rhs[ri];  // current: updated right after the previous pivot
           rrhs = r;
           rpe = v;
           rrcp = recip_of(v);
@@ -562,14 +564,6 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
         if constexpr (TWO) {
           if (upd1) z1 = __fma_rn(f1, prr, z1);
         }
-        // Row l and position e were zeroed, so one fma per element yields the pivot row
-        // (f_l = 1) and the leaving variable's column (fma(-f_i, rl, 0)) with no branch.
-#pragma unroll
-        for (int ai = 0; ai < A; ++ai) {
-          const double fi = sm.fcol[par][tr + TR * ai];
-#pragma unroll
-          for (int b = 0; b < BC; ++b) T[ai][b] = __fma_rn(fi, pv[b], T[ai][b]);
-        }
         if (leaving < 0 && tc == etc) {  // an artificial left: position e is dead (rare)
 #define LPB_DEAD(x)                            \
   case x:                                      \
@@ -581,27 +575,70 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
           switch (be) { LPB_CASES(LPB_DEAD) default: break; }
 #undef LPB_DEAD
         }
-        prr_prev = prr;
+        if (drive) ++it1;
+        else if (phase == 1) ++it1;
+        else ++it2;
+        if (!drive) stall = (theta > 0.0) ? 0 : stall + 1;
+        // Step 1 of the NEXT pivot, fused with this update (software pipelining): the argmax
+        // over the freshly updated objective replica is issued before the tableau update so
+        // that its reduction latency overlaps the DFMAs.  Fast path only (unique maximum, no
+        // in-thread tie, Dantzig mode); anything else is redone by the full Step 1 at the top.
+        const bool fuse = !drive && !(a.bland_K > 0 && stall >= a.bland_K);
+        double bv = neg_inf();
+        int bb = 0;
+        {
+          double v[BC];
+#pragma unroll
+          for (int b = 0; b < BC; ++b) v[b] = p1 ? d1[TWO ? b : 0] : d2[b];
+          // first maximum (lowest b on ties) by a balanced tree
+          double tv[BC];
+          int tb[BC];
+#pragma unroll
+          for (int b = 0; b < BC; ++b) { tv[b] = v[b]; tb[b] = b; }
+#pragma unroll
+          for (int step = 1; step < BC; step *= 2) {
+#pragma unroll
+            for (int b = 0; b + step < BC; b += 2 * step) {
+              const bool take = tv[b + step] > tv[b];
+              tv[b] = take ? tv[b + step] : tv[b];
+              tb[b] = take ? tb[b + step] : tb[b];
+            }
+          }
+          bv = tv[0];
+          bb = tb[0];
+        }
+        const bool fval = fuse && bv > a.eps_enter;
+        bool ftie = false;
+#pragma unroll
+        for (int b = 0; b < BC; ++b) ftie |= (b != bb) && ((p1 ? d1[TWO ? b : 0] : d2[b]) == bv);
+        const unsigned fhi = fval ? (unsigned)(okey(bv) >> 32) : 0u;
+        const unsigned fmhi = __reduce_max_sync(FULL, fhi);
+        // Row l and position e were zeroed, so one fma per element yields the pivot row
+        // (f_l = 1) and the leaving variable's column (fma(-f_i, rl, 0)) with no branch.
+#pragma unroll
+        for (int ai = 0; ai < A; ++ai) {
+          const double fi = sm.fcol[par][tr + TR * ai];
+#pragma unroll
+          for (int b = 0; b < BC; ++b) T[ai][b] = __fma_rn(fi, pv[b], T[ai][b]);
+        }
+        const unsigned fb1 = __ballot_sync(FULL, fval && fhi == fmhi);
+        const bool fany_tie = __any_sync(FULL, fval && ftie);
+        const int fwl = (fb1 != 0u) ? (__ffs(fb1) - 1) : 0;
+        const unsigned fvar = (unsigned)nbv[tc + TC * bb];
+        e_next = __shfl_sync(FULL, tc + TC * bb, fwl);
+        evar_next = (int)__shfl_sync(FULL, fvar, fwl);
+        have_e = fuse && fb1 != 0u && (fb1 & (fb1 - 1u)) == 0u && !fany_tie;
+        // RHS column update (the lane serving row i; the pivot row gets RHS / PE)
+        if (rlane && ri < m)
+          sm.rhs[ri] = (ri == l) ? prr : __fma_rn(sm.fcol[par][ri], prr, sm.rhs[ri]);
       }
       LPB_PROF_MARK(6)
-      pend = true;
-      l_prev = l;
       par ^= 1;
-      if (drive) {
-        ++it1;
-        gsync<NT>();  // the next drive-out scan reads bkey
-      } else {
-        if (phase == 1) ++it1; else ++it2;
-        stall = (theta > 0.0) ? 0 : stall + 1;
-      }
+      if (drive) gsync<NT>();  // the next drive-out scan reads bkey
     }
 
     // ---- extract (R10) ----
     gsync<NT>();
-    if (st == ST_OPTIMAL && pend) {  // apply the last pending RHS update
-      for (int i = tid; i < m; i += NT)
-        sm.rhs[i] = (i == l_prev) ? prr_prev : __fma_rn(sm.fcol[par ^ 1][i], prr_prev, sm.rhs[i]);
-    }
     if (tid == 0) {
       a.status[lp] = st;
       a.iters[2 * lp] = it1;
