@@ -3,6 +3,11 @@
     python paper_1609_08114_b200/build.py [--verbose] [--force]
 (run it by path: importing the package first would load a possibly stale liblpb.so)
 
+Development variants (never the product library):
+    python paper_1609_08114_b200/build.py --variant ab/prof -DLPB_PROFILE
+builds a copy of the package under ab/prof/paper_1609_08114_b200/ with extra defines
+(scripts/phase_prof.py and scripts/ab_time.py import it from there).
+
 Every .cu under csrc/ is compiled to an object with
     -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -fmad=false
 (-fmad=false: no implicit multiply-add contraction; the kernels write the FMAs the method
@@ -36,7 +41,9 @@ def _stale(obj: str, deps: list[str]) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
+def build(verbose: bool = False, force: bool = False, defines: list[str] | None = None,
+          out: str = OUT, obj: str = OBJ) -> str:
+    OUT, OBJ = out, obj
     os.makedirs(OBJ, exist_ok=True)
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
     hdrs = sorted(glob.glob(os.path.join(CSRC, "*.cuh"))) + [os.path.join(ROOT, "include", "lpb.h")]
@@ -46,7 +53,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
         o = os.path.join(OBJ, os.path.basename(s)[:-3] + ".o")
         objs.append(o)
         if force or _stale(o, [s] + hdrs):
-            cmd = [NVCC, *ARCH, *FLAGS, "-c", s, "-o", o]
+            cmd = [NVCC, *ARCH, *FLAGS, *(defines or []), "-c", s, "-o", o]
             if verbose:
                 cmd.insert(1, "-Xptxas=-v")
             jobs.append(cmd)
@@ -69,4 +76,15 @@ def build(verbose: bool = False, force: bool = False) -> str:
 
 
 if __name__ == "__main__":
-    print(build(verbose="--verbose" in sys.argv, force="--force" in sys.argv))
+    defs = [a for a in sys.argv[1:] if a.startswith("-D")]
+    if "--variant" in sys.argv:
+        import shutil
+        vdir = os.path.join(os.path.abspath(sys.argv[sys.argv.index("--variant") + 1]),
+                            os.path.basename(HERE))
+        os.makedirs(vdir, exist_ok=True)
+        for f in glob.glob(os.path.join(HERE, "*.py")):
+            shutil.copy(f, vdir)
+        print(build(verbose="--verbose" in sys.argv, force=True, defines=defs,
+                    out=os.path.join(vdir, "liblpb.so"), obj=os.path.join(vdir, "build_obj")))
+    else:
+        print(build(verbose="--verbose" in sys.argv, force="--force" in sys.argv, defines=defs))

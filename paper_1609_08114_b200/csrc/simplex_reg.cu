@@ -39,14 +39,6 @@ __device__ __forceinline__ double neg_inf() { return __longlong_as_double(0xfff0
 __device__ __forceinline__ double pos_inf() { return __longlong_as_double(0x7ff0000000000000ll); }
 __device__ __forceinline__ double qnan() { return __longlong_as_double(0x7ff8000000000000ll); }
 
-// st.shared through inline PTX: keeps a store inside its switch case (the compiler would
-// otherwise sink identical stores out of the cases and insert register copies to merge them)
-__device__ __forceinline__ void sts64(double* p, double v) {
-  asm volatile("st.shared.f64 [%0], %1;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(p))),
-               "d"(v)
-               : "memory");
-}
-
 // Barrier of the LP's thread group.
 template <int NT>
 __device__ __forceinline__ void gsync() {
@@ -60,15 +52,10 @@ __device__ __forceinline__ void gsync() {
   BODY(20) BODY(21) BODY(22) BODY(23) BODY(24) BODY(25) BODY(26) BODY(27) BODY(28)         \
   BODY(29) BODY(30) BODY(31)
 
-struct Part {  // a (value, tie, index) reduction partial of the ratio test
+struct Part {  // a (value, tie, index) reduction partial
   double v;
-  double pe;   // pivot element candidate colE[idx]
-  double rcp;  // its refined reciprocal (shared by every division of the pivot row)
-  double rhs;  // rhs[idx] (lazily updated)
   int tie;
   int idx;
-  int leave;  // basis key of row idx (the leaving variable if idx wins)
-  int pad;
 };
 
 template <int TR, int TC, int A, int BC>
@@ -78,27 +65,31 @@ struct RegSmem {
   double fcol[2][RCAP];  // update multipliers: -colE, and +1 for the pivot row
   double fobj[2][2];     // pivot-column entries of the phase-II / phase-I rows
   double rhs[RCAP];      // RHS column (lazily updated)
-  double prow[CCAP];     // scratch for the phase-I row at build
-  double pslot[2][NWARP][CCAP];  // each warp's candidate pivot row (unscaled)
+  double prow[CCAP];     // new pivot row (positions); scratch for the phase-I row at build
   int bkey[RCAP];        // row -> basic variable key (>= 0 real, < 0 artificial)
-  int nbvar[NWARP][CCAP];  // position -> nonbasic variable index, one copy per warp
+  int nbvar[CCAP];       // position -> nonbasic variable index (DEADV: dead / padding)
   int negrows[RCAP];     // ascending rows with b_i < 0
   int wcount[NWARP];
-  Part part[2][NWARP];   // ratio-test partial per warp (double-buffered by pivot parity)
+  Part part[NWARP];      // ratio-test partial per warp
+  double prow_rhs;
   uint64_t mbar;         // completes when the prefetched A of LP `lp` has landed
   int lp;
+  int leaving;
 };
 
-// Optional phase profiler (SimplexArgs::prof != nullptr): warp 0 of every CTA accumulates
-// clock64() deltas per pivot phase into prof[blockIdx.x * 8 + phase]: 7 build/loop head,
-// 0 Step 1, 1 publish column, 2 ratio + speculative pivot row, 3 barrier wait, 4 partial
-// reduce, 5 bookkeeping, 6 update.  Off by default.
+// Optional phase profiler, compiled in only with -DLPB_PROFILE (scripts/phase_prof.py builds
+// that variant): warp 0 of every CTA accumulates clock64() deltas per pivot phase into
+// prof[blockIdx.x * 12 + phase] when SimplexArgs::prof is set.
+#ifdef LPB_PROFILE
 #define LPB_PROF_MARK(ph)                                                 \
   if (prof_on) {                                                          \
     const long long t_ = clock64();                                       \
     pacc[ph] += t_ - pt;                                                  \
     pt = t_;                                                              \
   }
+#else
+#define LPB_PROF_MARK(ph)
+#endif
 
 template <int TR, int TC, int A, int BC, bool TWO, int MINB>
 __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs a) {
@@ -113,9 +104,11 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
   const int rrow = (w * RPW + lane % RPW) + TR * (lane / RPW);
   const bool rlane = lane < RPW * A;
   const int m = a.m, n = a.n;
+#ifdef LPB_PROFILE
   const bool prof_on = a.prof != nullptr && w == 0;
   long long pacc[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   long long pt = clock64();
+#endif
 
   double T[A][BC];
   double d2[BC];
@@ -182,17 +175,14 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
     }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) binf = fmax(binf, __shfl_xor_sync(FULL, binf, off));
-    if (lane == 0) sm.part[0][w].v = binf;
+    if (lane == 0) sm.part[w].v = binf;
     gsync<NT>();
 #pragma unroll
-    for (int q = 0; q < NWARP; ++q) binf = fmax(binf, sm.part[0][q].v);
+    for (int q = 0; q < NWARP; ++q) binf = fmax(binf, sm.part[q].v);
     const int npos = n + k;
     int st = (m > RCAP || npos > CCAP || (!TWO && k > 0)) ? ST_NUMERICAL : -1;
-    for (int p = tid; p < CCAP; p += NT) {
-      const int v = (p < n) ? p : (p < npos ? n + sm.negrows[p - n] : DEADV);
-#pragma unroll
-      for (int q = 0; q < NWARP; ++q) sm.nbvar[q][p] = v;
-    }
+    for (int p = tid; p < CCAP; p += NT)
+      sm.nbvar[p] = (p < n) ? p : (p < npos ? n + sm.negrows[p - n] : DEADV);
     for (int i = m + tid; i < RCAP; i += NT) sm.rhs[i] = 0.0;
 
 #pragma unroll
@@ -259,27 +249,14 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
     }
 
     // ---- Steps 1-3, two phases ----
-    // ONE block barrier per pivot: every warp scales its own ratio-test winner row
-    // speculatively (a warp's candidate row always lies in the warp's own thread-rows), and
-    // after the barrier every warp reads the winning warp's scaled pivot row.  All other
-    // SMEM traffic is warp-local (colE, fcol, rhs, bkey of a row are touched only by the
-    // warp owning that row; nbvar has one copy per warp).
     int it1 = 0, it2 = 0, stall = 0, phase = (TWO && k > 0) ? 1 : 2;
-    int par = 0, dl = 0;
-    bool drive = false;
-    bool have_e = false;  // Step 1 of this pivot was already done, fused into the last update
-    int e_next = -1, evar_next = 0;
-    int* nbv = sm.nbvar[w];
+    int par = 0, l_prev = -1, dl = 0;
+    bool pend = false, drive = false;
     while (st < 0) {
       const bool bland = a.bland_K > 0 && stall >= a.bland_K;
       const bool p1 = TWO && phase == 1;
       int e = -1, evar = 0, l = -1;
-      if (!drive && have_e) {
-        have_e = false;
-        if (it1 + it2 >= a.max_iter) { st = ST_ITER_LIMIT; break; }
-        e = e_next;
-        evar = evar_next;
-      } else if (drive) {
+      if (drive) {
         // phase switch (R9): drive the next basic artificial out on max |T[l][p]|
         while (dl < m && sm.bkey[dl] >= 0) ++dl;
         if (dl >= m) {
@@ -303,7 +280,7 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
             v = fabs(v);
             if (d2[b] != neg_inf() && v > a.eps_piv) {  // live position
               const int p = tc + TC * b;
-              const unsigned var = (unsigned)nbv[p];
+              const unsigned var = (unsigned)sm.nbvar[p];
               if (!val || v > bv || (v == bv && var < bvar)) {
                 val = true;
                 bv = v;
@@ -314,15 +291,15 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
           }
         }
         const int wl = warp_argmax(val, okey(bv), bvar);
-        Part pw{0.0, INT_MAX, -1, 0, 0};
+        Part pw{0.0, INT_MAX, -1};
         if (wl >= 0) {
           pw.v = __shfl_sync(FULL, bv, wl);
           pw.tie = (int)__shfl_sync(FULL, bvar, wl);
           pw.idx = __shfl_sync(FULL, bp, wl);
         }
-        if (lane == 0) sm.part[par][w] = pw;
+        if (lane == 0) sm.part[w] = pw;
         gsync<NT>();
-        const Part q = (lane < NWARP) ? sm.part[par][lane] : Part{0.0, INT_MAX, -1, 0, 0};
+        const Part q = (lane < NWARP) ? sm.part[lane] : Part{0.0, INT_MAX, -1};
         const int ql = warp_argmax(q.idx >= 0, okey(q.v), (unsigned)q.tie);
         gsync<NT>();
         if (ql < 0) continue;  // redundant row: the artificial stays basic at 0
@@ -350,13 +327,13 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
             const double v = p1 ? d1[TWO ? b : 0] : d2[b];
             tie |= (b != bb) && (v == bv);
           }
-          bvar = val ? (unsigned)nbv[tc + TC * bb] : 0u;
+          bvar = val ? (unsigned)sm.nbvar[tc + TC * bb] : 0u;
           if (__any_sync(FULL, val && tie)) {  // rare: exact tie inside a thread -> var index
             if (val && tie) {
 #pragma unroll
               for (int b = 0; b < BC; ++b) {
                 const double v = p1 ? d1[TWO ? b : 0] : d2[b];
-                const unsigned var = (unsigned)nbv[tc + TC * b];
+                const unsigned var = (unsigned)sm.nbvar[tc + TC * b];
                 if (v == bv && var < bvar) {
                   bvar = var;
                   bb = b;
@@ -371,7 +348,7 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
           for (int b = 0; b < BC; ++b) {
             const double v = p1 ? d1[TWO ? b : 0] : d2[b];
             if (v > a.eps_enter) {
-              const unsigned var = (unsigned)nbv[tc + TC * b];
+              const unsigned var = (unsigned)sm.nbvar[tc + TC * b];
               if (var < bvar) {
                 bvar = var;
                 bb = b;
@@ -387,169 +364,137 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
           if (z1 > a.eps_phase1 * fmax(1.0, binf)) { st = ST_INFEASIBLE; break; }
           drive = true;  // phase-I optimum with w* ~ 0
           dl = 0;
-          gsync<NT>();  // the drive-out scan reads bkey written by other warps
           continue;
         }
         if (it1 + it2 >= a.max_iter) { st = ST_ITER_LIMIT; break; }
         e = __shfl_sync(FULL, tc + TC * bb, wl);
         evar = (int)__shfl_sync(FULL, bvar, wl);
       }
-      LPB_PROF_MARK(0)
 
-      // Step 2a: the owners of position e publish column e (+ objective-row entries) and
-      // zero it (so the update produces the leaving variable's column)
+      LPB_PROF_MARK(0)
+      // Step 2a: the owners of position e publish column e (+ objective-row entries)
       const int be = e / TC, etc = e - be * TC;
       double* colE = sm.colE[par];
       if (tc == etc) {
-        double* cE = colE + tr;
 #define LPB_PUB(x)                                                                    \
   case x:                                                                             \
     if constexpr ((x) < BC) {                                                         \
       _Pragma("unroll") for (int ai = 0; ai < A; ++ai) {                             \
-        sts64(cE + TR * ai, T[ai][x]);                                                \
+        colE[tr + TR * ai] = T[ai][x];                                                \
         T[ai][x] = 0.0;                                                               \
       }                                                                               \
+      if (tr == 0) {                                                                  \
+        sm.fobj[par][0] = d2[x];                                                      \
+        if constexpr (TWO) sm.fobj[par][1] = d1[x];                                   \
+      }                                                                               \
+      d2[x] = 0.0;                                                                    \
+      if constexpr (TWO) d1[x] = 0.0;                                                 \
     }                                                                                 \
     break;
         switch (be) { LPB_CASES(LPB_PUB) default: break; }
 #undef LPB_PUB
-        // objective-row entries of column e (register selects, no dynamic indexing)
-        if (tr == 0) {
-          double v2 = d2[0], v1 = TWO ? d1[0] : 0.0;
-#pragma unroll
-          for (int b = 1; b < BC; ++b) {
-            v2 = (b == be) ? d2[b] : v2;
-            if constexpr (TWO) v1 = (b == be) ? d1[TWO ? b : 0] : v1;
-          }
-          sm.fobj[par][0] = v2;
-          if constexpr (TWO) sm.fobj[par][1] = v1;
-        }
-      }
-      {  // zero position e in the replicas (owner lanes) so the update swaps the column in
-        const bool own_e = (tc == etc);
-#pragma unroll
-        for (int b = 0; b < BC; ++b) {
-          const bool z = own_e && (b == be);
-          d2[b] = z ? 0.0 : d2[b];
-          if constexpr (TWO) d1[TWO ? b : 0] = z ? 0.0 : d1[TWO ? b : 0];
-        }
       }
       __syncwarp();
       LPB_PROF_MARK(1)
-      // Step 2b: lane-parallel ratio test over the warp's rows; each lane also writes its
-      // row's update multiplier f_i = -colE_i
-      const int ri = rrow;
-      bool rval = false;
-      double ratio = 0.0, rrhs = 0.0, rpe = 1.0, rrcp = 1.0;
-      int rtie = INT_MAX;
-      if (rlane) {
-        const double v = colE[ri];
-        sm.fcol[par][ri] = -v;
-        if (ri < m) {
-          const double r = sm.rhs[ri];  // current: updated right after the previous pivot
-          rrhs = r;
-          rpe = v;
-          rrcp = recip_of(v);
-          if (!drive) {
-            rval = v > a.eps_piv;
-            bool slow;
-            ratio = div_with(r, v, rrcp, slow);
-            if (slow || !rval) ratio = __ddiv_rn(r, rval ? v : 1.0);  // rare / non-candidate
-            rtie = bland ? sm.bkey[ri] : ri;
+      // Step 2b: lane-parallel lazy RHS update + ratio test over the warp's rows; each lane
+      // also writes its row's update multiplier f_i = -colE_i
+      {
+        bool val = false;
+        double ratio = 0.0;
+        int tie = INT_MAX;
+        const int i = rrow;
+        if (rlane) {
+          const double v = colE[i];
+          sm.fcol[par][i] = -v;
+          if (i < m) {
+            double r = sm.rhs[i];
+            if (pend) {
+              const double prr = sm.prow_rhs;
+              r = (i == l_prev) ? prr : __fma_rn(sm.fcol[par ^ 1][i], prr, r);
+              sm.rhs[i] = r;
+            }
+            if (!drive) {
+              val = v > a.eps_piv;
+              bool slow;
+              ratio = div_fast(r, val ? v : 1.0, slow);
+              if (slow) ratio = __ddiv_rn(r, val ? v : 1.0);  // rare: outside the fast range
+              tie = bland ? sm.bkey[i] : i;
+            }
           }
         }
-      }
-      LPB_PROF_MARK(8)
-      int lw = -1;
-      if (!drive) {
-        const int wl = warp_argmin(rval, okey(ratio), ikey(rtie));
-        if (wl >= 0) {
-          lw = __shfl_sync(FULL, ri, wl);
-          if (lane == wl)  // the winning lane publishes the warp's partial itself
-            sm.part[par][w] = Part{ratio, rpe, rrcp, rrhs, rtie, ri, sm.bkey[ri], 0};
-        } else if (lane == 0) {
-          sm.part[par][w] = Part{0.0, 1.0, 1.0, 0.0, INT_MAX, -1, 0, 0};
+        if (!drive) {
+          const int wl = warp_argmin(val, okey(ratio), ikey(tie));
+          Part pw{0.0, INT_MAX, -1};
+          if (wl >= 0) {
+            pw.v = __shfl_sync(FULL, ratio, wl);
+            pw.tie = __shfl_sync(FULL, tie, wl);
+            pw.idx = __shfl_sync(FULL, i, wl);
+          }
+          if (lane == 0) sm.part[w] = pw;
         }
-      } else if ((l % TR) / RPW == w) {
-        lw = l;  // the drive-out row belongs to this warp
-        if (rlane && ri == l) sm.part[par][w] = Part{0.0, rpe, rrcp, rrhs, 0, l, sm.bkey[l], 0};
       }
-      LPB_PROF_MARK(9)
-      // Step 3 (speculative part): the thread-row holding lw publishes its row (unscaled;
-      // the winning row is divided by PE after the barrier, by every thread for its own
-      // positions)
-      if (lw >= 0 && tr == lw % TR) {
-        const int al = lw / TR;
-        double* ps = sm.pslot[par][w] + tc;
-#define LPB_ROWPUB(x)                                                               \
-  case x:                                                                           \
-    if constexpr ((x) < A) {                                                        \
-      _Pragma("unroll") for (int b = 0; b < BC; ++b)                                \
-        sts64(ps + TC * b, tc + TC * b == e ? 1.0 : T[x][b]);                       \
-    }                                                                               \
-    break;
-        switch (al) { LPB_CASES(LPB_ROWPUB) default: break; }
-#undef LPB_ROWPUB
-      }
-      LPB_PROF_MARK(10)
       LPB_PROF_MARK(2)
-      gsync<NT>();  // the pivot's only block barrier
+      gsync<NT>();  // barrier 1
       LPB_PROF_MARK(3)
-      // Step 2c: the winning warp partial (argmin of the ratios), read by every warp
       double theta = 0.0;
-      int ww;
-      if (!drive) {
-        const Part q = (lane < NWARP) ? sm.part[par][lane] : Part{0.0, 1.0, 1.0, 0.0, INT_MAX, -1, 0, 0};
+      if (!drive) {  // Step 2c: argmin over the warp partials, in every warp
+        const Part q = (lane < NWARP) ? sm.part[lane] : Part{0.0, INT_MAX, -1};
         const int ql = warp_argmin(q.idx >= 0, okey(q.v), ikey(q.tie));
         if (ql < 0) { st = (phase == 2) ? ST_UNBOUNDED : ST_NUMERICAL; break; }
-        ww = ql;
-      } else {
-        ww = (l % TR) / RPW;
+        l = __shfl_sync(FULL, q.idx, ql);
+        theta = __shfl_sync(FULL, q.v, ql);
       }
-      const Part& win = sm.part[par][ww];  // broadcast SMEM reads of the winning partial
-      l = win.idx;
-      theta = win.v;
-      const int leaving = win.leave;
+
       LPB_PROF_MARK(4)
-      // bookkeeping: per-warp nbvar copy; the winning warp owns row l (bkey, fcol, zeroing)
-      if (lane == 0) nbv[e] = leaving >= 0 ? leaving : DEADV;
+      // Step 3: pivot row / PE by the owners of row l
+      const double pe = colE[l];
+      if (tid == 0) {
+        const int lv = sm.bkey[l];
+        sm.bkey[l] = evar;
+        sm.nbvar[e] = lv >= 0 ? lv : DEADV;
+        sm.leaving = lv;
+        sm.fcol[par][l] = 1.0;  // the pivot row: fma(1, prow, 0) = prow
+      }
       const int ltr = l % TR, al = l / TR;
-      if (w == ww) {
-        if (lane == 0) {
-          sm.bkey[l] = evar;
-          sm.fcol[par][l] = 1.0;  // the pivot row: fma(1, prow, 0) = prow
-        }
-        if (tr == ltr) {
-#define LPB_ROWZ(x)                                                                    \
-  case x:                                                                              \
-    if constexpr ((x) < A) {                                                           \
-      _Pragma("unroll") for (int b = 0; b < BC; ++b) T[x][b] = 0.0;                    \
-    }                                                                                  \
+      if (tr == ltr) {
+#define LPB_PROW(x)                                                                 \
+  case x:                                                                           \
+    if constexpr ((x) < A) {                                                        \
+      bool slow_any = false;                                                        \
+      double q[BC];                                                                 \
+      _Pragma("unroll") for (int b = 0; b < BC; ++b) {                              \
+        const int p = tc + TC * b;                                                  \
+        bool sl;                                                                    \
+        q[b] = div_fast(p == e ? 1.0 : T[x][b], pe, sl);                            \
+        slow_any |= sl;                                                             \
+      }                                                                             \
+      if (slow_any) {                                                               \
+        _Pragma("unroll") for (int b = 0; b < BC; ++b)                              \
+          q[b] = __ddiv_rn(tc + TC * b == e ? 1.0 : T[x][b], pe);                   \
+      }                                                                             \
+      _Pragma("unroll") for (int b = 0; b < BC; ++b) {                              \
+        sm.prow[tc + TC * b] = q[b];                                                \
+        T[x][b] = 0.0;                                                              \
+      }                                                                             \
+    }                                                                               \
     break;
-          switch (al) { LPB_CASES(LPB_ROWZ) default: break; }
-#undef LPB_ROWZ
+        switch (al) { LPB_CASES(LPB_PROW) default: break; }
+#undef LPB_PROW
+        if (tc == 0) {
+          bool sl;
+          const double q = div_fast(sm.rhs[l], pe, sl);
+          sm.prow_rhs = sl ? __ddiv_rn(sm.rhs[l], pe) : q;
         }
       }
-      __syncwarp();
       LPB_PROF_MARK(5)
+      gsync<NT>();  // barrier 2
+      LPB_PROF_MARK(6)
       {
-        // the pivot row divided by PE (IEEE, one shared reciprocal)
-        const double* pslw = sm.pslot[par][ww] + tc;
+        const double prr = sm.prow_rhs;
+        const int leaving = sm.leaving;
         double pv[BC];
-        bool slow_any = false;
 #pragma unroll
-        for (int b = 0; b < BC; ++b) {
-          bool sl;
-          pv[b] = div_with(pslw[TC * b], win.pe, win.rcp, sl);
-          slow_any |= sl;
-        }
-        if (slow_any) {  // rare: outside the fast range -> IEEE slow path
-#pragma unroll
-          for (int b = 0; b < BC; ++b) pv[b] = __ddiv_rn(pslw[TC * b], win.pe);
-        }
-        bool slr;
-        double prr = div_with(win.rhs, win.pe, win.rcp, slr);
-        if (slr) prr = __ddiv_rn(win.rhs, win.pe);
+        for (int b = 0; b < BC; ++b) pv[b] = sm.prow[tc + TC * b];
         const double f2 = -sm.fobj[par][0];
         const bool upd1 = TWO && phase == 1;
         const double f1 = TWO ? -sm.fobj[par][1] : 0.0;
@@ -564,6 +509,15 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
         if constexpr (TWO) {
           if (upd1) z1 = __fma_rn(f1, prr, z1);
         }
+        // Row l and position e were zeroed when they were read (Step 2a / Step 3), so one
+        // fma per element yields the pivot row (f_l = 1: fma(1, prow, 0) = prow) and the
+        // leaving variable's column (fma(-f_i, rl, 0)) without any per-element branch.
+#pragma unroll
+        for (int ai = 0; ai < A; ++ai) {
+          const double fi = sm.fcol[par][tr + TR * ai];
+#pragma unroll
+          for (int b = 0; b < BC; ++b) T[ai][b] = __fma_rn(fi, pv[b], T[ai][b]);
+        }
         if (leaving < 0 && tc == etc) {  // an artificial left: position e is dead (rare)
 #define LPB_DEAD(x)                            \
   case x:                                      \
@@ -575,70 +529,27 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
           switch (be) { LPB_CASES(LPB_DEAD) default: break; }
 #undef LPB_DEAD
         }
-        if (drive) ++it1;
-        else if (phase == 1) ++it1;
-        else ++it2;
-        if (!drive) stall = (theta > 0.0) ? 0 : stall + 1;
-        // Step 1 of the NEXT pivot, fused with this update (software pipelining): the argmax
-        // over the freshly updated objective replica is issued before the tableau update so
-        // that its reduction latency overlaps the DFMAs.  Fast path only (unique maximum, no
-        // in-thread tie, Dantzig mode); anything else is redone by the full Step 1 at the top.
-        const bool fuse = !drive && !(a.bland_K > 0 && stall >= a.bland_K);
-        double bv = neg_inf();
-        int bb = 0;
-        {
-          double v[BC];
-#pragma unroll
-          for (int b = 0; b < BC; ++b) v[b] = p1 ? d1[TWO ? b : 0] : d2[b];
-          // first maximum (lowest b on ties) by a balanced tree
-          double tv[BC];
-          int tb[BC];
-#pragma unroll
-          for (int b = 0; b < BC; ++b) { tv[b] = v[b]; tb[b] = b; }
-#pragma unroll
-          for (int step = 1; step < BC; step *= 2) {
-#pragma unroll
-            for (int b = 0; b + step < BC; b += 2 * step) {
-              const bool take = tv[b + step] > tv[b];
-              tv[b] = take ? tv[b + step] : tv[b];
-              tb[b] = take ? tb[b + step] : tb[b];
-            }
-          }
-          bv = tv[0];
-          bb = tb[0];
-        }
-        const bool fval = fuse && bv > a.eps_enter;
-        bool ftie = false;
-#pragma unroll
-        for (int b = 0; b < BC; ++b) ftie |= (b != bb) && ((p1 ? d1[TWO ? b : 0] : d2[b]) == bv);
-        const unsigned fhi = fval ? (unsigned)(okey(bv) >> 32) : 0u;
-        const unsigned fmhi = __reduce_max_sync(FULL, fhi);
-        // Row l and position e were zeroed, so one fma per element yields the pivot row
-        // (f_l = 1) and the leaving variable's column (fma(-f_i, rl, 0)) with no branch.
-#pragma unroll
-        for (int ai = 0; ai < A; ++ai) {
-          const double fi = sm.fcol[par][tr + TR * ai];
-#pragma unroll
-          for (int b = 0; b < BC; ++b) T[ai][b] = __fma_rn(fi, pv[b], T[ai][b]);
-        }
-        const unsigned fb1 = __ballot_sync(FULL, fval && fhi == fmhi);
-        const bool fany_tie = __any_sync(FULL, fval && ftie);
-        const int fwl = (fb1 != 0u) ? (__ffs(fb1) - 1) : 0;
-        const unsigned fvar = (unsigned)nbv[tc + TC * bb];
-        e_next = __shfl_sync(FULL, tc + TC * bb, fwl);
-        evar_next = (int)__shfl_sync(FULL, fvar, fwl);
-        have_e = fuse && fb1 != 0u && (fb1 & (fb1 - 1u)) == 0u && !fany_tie;
-        // RHS column update (the lane serving row i; the pivot row gets RHS / PE)
-        if (rlane && ri < m)
-          sm.rhs[ri] = (ri == l) ? prr : __fma_rn(sm.fcol[par][ri], prr, sm.rhs[ri]);
       }
-      LPB_PROF_MARK(6)
+      LPB_PROF_MARK(8)
+      pend = true;
+      l_prev = l;
       par ^= 1;
-      if (drive) gsync<NT>();  // the next drive-out scan reads bkey
+      if (drive) {
+        ++it1;
+        gsync<NT>();  // the next drive-out scan reads bkey
+      } else {
+        if (phase == 1) ++it1; else ++it2;
+        stall = (theta > 0.0) ? 0 : stall + 1;
+      }
     }
 
     // ---- extract (R10) ----
     gsync<NT>();
+    if (st == ST_OPTIMAL && pend) {  // apply the last pending RHS update
+      const double prr = sm.prow_rhs;
+      for (int i = tid; i < m; i += NT)
+        sm.rhs[i] = (i == l_prev) ? prr : __fma_rn(sm.fcol[par ^ 1][i], prr, sm.rhs[i]);
+    }
     if (tid == 0) {
       a.status[lp] = st;
       a.iters[2 * lp] = it1;
@@ -659,8 +570,11 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
     }
     gsync<NT>();
   }
+#ifdef LPB_PROFILE
   if (prof_on && lane == 0)
-    for (int q = 0; q < 12; ++q) atomicAdd((unsigned long long*)&a.prof[blockIdx.x * 12 + q], (unsigned long long)pacc[q]);
+    for (int q = 0; q < 12; ++q)
+      atomicAdd((unsigned long long*)&a.prof[blockIdx.x * 12 + q], (unsigned long long)pacc[q]);
+#endif
 }
 
 struct RegCfg {

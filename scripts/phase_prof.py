@@ -1,7 +1,11 @@
 """Per-phase cycle breakdown of the R-class kernel (warp 0 of each CTA):
 python scripts/phase_prof.py cfg2:20000"""
-import ctypes, sys
-sys.path.insert(0, '.')
+import ctypes, os, sys
+# the profiler is compiled in only with -DLPB_PROFILE: use (or build) that variant
+if not os.path.exists('ab/prof/paper_1609_08114_b200/liblpb.so'):
+    os.system(f'{sys.executable} paper_1609_08114_b200/build.py --variant ab/prof -DLPB_PROFILE')
+sys.path.insert(0, 'ab/prof')
+sys.path.insert(1, '.')
 import numpy as np, torch
 import lpgen
 from paper_1609_08114_b200 import lpb
@@ -18,7 +22,7 @@ ms = s.timing()[0]
 r = s.device_results()
 piv = r['iters'].sum().item()
 p = buf.view(-1, 12).sum(0).cpu().numpy().astype(float)
-names = ['step1', 'publish', 'part_write', 'barrier', 'reduce', 'bookkeep', 'update', 'loophead', 'ratio_lanes', 'ratio_argmin', 'spec_prow', '-']
+names = ['step1', 'publish', 'ratio_part', 'barrier1', 'reduce', 'prow', 'barrier2', 'loophead', 'update', '-', '-', '-']
 ctas = (buf.view(-1, 12).sum(1) > 0).sum().item()
 print(f'{name} B={B} ms={ms:.3f} pivots={piv} ctas={ctas}')
 tot = p.sum()
