@@ -58,9 +58,9 @@ struct Part {  // a (value, tie, index) reduction partial
   int idx;
 };
 
-template <int TR, int TC, int A, int BC>
+template <int TR, int TC, int AT, int BC>
 struct RegSmem {
-  static constexpr int RCAP = TR * A, CCAP = TC * BC, NWARP = (TR * TC) / 32;
+  static constexpr int RCAP = TR * AT, CCAP = TC * BC, NWARP = (TR * TC) / 32;
   double colE[2][RCAP];  // pivot column (constraint rows), double-buffered by pivot parity
   double fcol[2][RCAP];  // update multipliers: -colE, and +1 for the pivot row
   double fobj[2][2];     // pivot-column entries of the phase-II / phase-I rows
@@ -91,18 +91,23 @@ struct RegSmem {
 #define LPB_PROF_MARK(ph)
 #endif
 
-template <int TR, int TC, int A, int BC, bool TWO, int MINB>
+// AS > 0: each thread also owns AS more rows (i = tr + TR*(A+s)) kept in a thread-private
+// SMEM slice (double2 pairs of positions, thread-interleaved: conflict-free 128-bit accesses),
+// so that three LPs fit one SM (registers + SMEM) instead of two (registers only).
+template <int TR, int TC, int A, int AS, int BC, bool TWO, int MINB>
 __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs a) {
-  constexpr int NT = TR * TC, RCAP = TR * A, CCAP = TC * BC, NWARP = NT / 32;
+  constexpr int AT = A + AS;  // rows per thread-row
+  constexpr int NT = TR * TC, RCAP = TR * AT, CCAP = TC * BC, NWARP = NT / 32;
   constexpr int RPW = 32 / TC;  // thread-rows per warp
-  static_assert(NT % 32 == 0 && 32 % TC == 0 && TR <= 32 && A <= 32 && BC <= 32, "layout");
-  static_assert(RPW * A <= 32, "the warp's rows must fit its lanes");
-  __shared__ RegSmem<TR, TC, A, BC> sm;
+  constexpr int BH = (BC + 1) / 2;  // double2 pairs per SMEM row
+  static_assert(NT % 32 == 0 && 32 % TC == 0 && TR <= 32 && AT <= 32 && BC <= 32, "layout");
+  static_assert(RPW * AT <= 32, "the warp's rows must fit its lanes");
+  __shared__ RegSmem<TR, TC, AT, BC> sm;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int tr = tid / TC, tc = tid - (tid / TC) * TC;
   // the row this lane serves in the warp-parallel ratio test
   const int rrow = (w * RPW + lane % RPW) + TR * (lane / RPW);
-  const bool rlane = lane < RPW * A;
+  const bool rlane = lane < RPW * AT;
   const int m = a.m, n = a.n;
 #ifdef LPB_PROFILE
   const bool prof_on = a.prof != nullptr && w == 0;
@@ -114,8 +119,14 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
   double d2[BC];
   double d1[TWO ? BC : 1];
   // the next LP's A is prefetched into SMEM (one bulk async copy) while this LP is solved
+  // (register-only layouts); with AS > 0 the dynamic SMEM holds the SMEM rows instead
   extern __shared__ __align__(16) double abuf[];
-  const bool pf = a.prefetch != 0;
+  double2* const Ts2 = reinterpret_cast<double2*>(abuf) + tid;  // [(s*BH + h) * NT]
+  double* const Ts1 = abuf + 2 * tid;                             // scalar view: [s][b]
+  auto ts = [&](int s_, int b_) -> double& {
+    return Ts1[(size_t)((s_ * BH + (b_ >> 1)) * NT) * 2 + (b_ & 1)];
+  };
+  const bool pf = AS == 0 && a.prefetch != 0;
   const bool direct = a.ticket == nullptr;
   const uint32_t abytes = (uint32_t)((int64_t)m * n * 8);
   uint32_t mphase = 0;
@@ -205,6 +216,26 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
         T[ai][b] = v;
       }
     }
+#pragma unroll
+    for (int s_ = 0; s_ < AS; ++s_) {
+      const int i = tr + TR * (A + s_);
+      const bool rowok = (i < m) && st < 0;
+      const bool neg = rowok && sm.bkey[i] < 0;
+#pragma unroll
+      for (int b = 0; b < BC; ++b) {
+        const int p = tc + TC * b;
+        double v = 0.0;
+        if (rowok && p < npos) {
+          if (p < n) {
+            v = Ak[i * n + p];
+            v = neg ? -v : v;
+          } else {
+            v = (i == sm.negrows[p - n]) ? -1.0 : (neg ? -0.0 : 0.0);
+          }
+        }
+        ts(s_, b) = v;
+      }
+    }
     // padding positions (and, later, dead artificial positions) hold -inf in the objective
     // replicas: never a Step-1 candidate, and fma(f, p, -inf) keeps them -inf
 #pragma unroll
@@ -277,6 +308,7 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
             double v = T[0][b];
 #pragma unroll
             for (int ai = 1; ai < A; ++ai) v = (ai == al) ? T[ai][b] : v;
+            if (AS > 0 && al >= A) v = ts(al - A, b);
             v = fabs(v);
             if (d2[b] != neg_inf() && v > a.eps_piv) {  // live position
               const int p = tc + TC * b;
@@ -393,6 +425,12 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
     break;
         switch (be) { LPB_CASES(LPB_PUB) default: break; }
 #undef LPB_PUB
+#pragma unroll
+        for (int s_ = 0; s_ < AS; ++s_) {  // SMEM rows: dynamic position index
+          double& t = ts(s_, be);
+          colE[tr + TR * (A + s_)] = t;
+          t = 0.0;
+        }
       }
       __syncwarp();
       LPB_PROF_MARK(1)
@@ -480,6 +518,26 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
     break;
         switch (al) { LPB_CASES(LPB_PROW) default: break; }
 #undef LPB_PROW
+        if (AS > 0 && al >= A) {  // pivot row in SMEM
+          const int s_ = al - A;
+          bool slow_any = false;
+          double q[BC];
+#pragma unroll
+          for (int b = 0; b < BC; ++b) {
+            bool sl;
+            q[b] = div_fast(tc + TC * b == e ? 1.0 : ts(s_, b), pe, sl);
+            slow_any |= sl;
+          }
+          if (slow_any) {
+#pragma unroll
+            for (int b = 0; b < BC; ++b) q[b] = __ddiv_rn(tc + TC * b == e ? 1.0 : ts(s_, b), pe);
+          }
+#pragma unroll
+          for (int b = 0; b < BC; ++b) {
+            sm.prow[tc + TC * b] = q[b];
+            ts(s_, b) = 0.0;
+          }
+        }
         if (tc == 0) {
           bool sl;
           const double q = div_fast(sm.rhs[l], pe, sl);
@@ -517,6 +575,17 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
           const double fi = sm.fcol[par][tr + TR * ai];
 #pragma unroll
           for (int b = 0; b < BC; ++b) T[ai][b] = __fma_rn(fi, pv[b], T[ai][b]);
+        }
+#pragma unroll
+        for (int s_ = 0; s_ < AS; ++s_) {  // SMEM rows, two positions per 128-bit access
+          const double fi = sm.fcol[par][tr + TR * (A + s_)];
+#pragma unroll
+          for (int h = 0; h < BH; ++h) {
+            double2 v = Ts2[(s_ * BH + h) * NT];
+            v.x = __fma_rn(fi, pv[2 * h], v.x);
+            if (2 * h + 1 < BC) v.y = __fma_rn(fi, pv[(2 * h + 1 < BC) ? 2 * h + 1 : 0], v.y);
+            Ts2[(s_ * BH + h) * NT] = v;
+          }
         }
         if (leaving < 0 && tc == etc) {  // an artificial left: position e is dead (rare)
 #define LPB_DEAD(x)                            \
@@ -581,20 +650,23 @@ struct RegCfg {
   int rcap, ccap, two, id;
 };
 
-// Instantiated layouts: {id, TR, TC, A, BC, TWO, MINB}
-#define LPB_REG_CONFIGS(X)           \
-  X(0, 8, 4, 1, 3, true, 16)         \
-  X(1, 8, 4, 2, 6, true, 12)         \
-  X(2, 8, 4, 4, 8, true, 6)          \
-  X(3, 16, 8, 4, 8, true, 2)         \
-  X(6, 8, 16, 13, 7, false, 2)       \
-  X(4, 16, 16, 7, 7, false, 1)       \
-  X(5, 16, 16, 7, 7, true, 1)
+// Instantiated layouts: {id, TR, TC, A (register rows), AS (SMEM rows), BC, TWO, MINB}.
+// (An AS > 0 layout with 3 LPs/SM, {8,16,7,6,7,false,3}, is correct but measured 15% slower
+// than {8,16,13,0,7} on cfg2: 1.63e6 vs 1.92e6 LPs/s; none is instantiated by default.)
+#define LPB_REG_CONFIGS(X)              \
+  X(0, 8, 4, 1, 0, 3, true, 16)         \
+  X(1, 8, 4, 2, 0, 6, true, 12)         \
+  X(2, 8, 4, 4, 0, 8, true, 6)          \
+  X(3, 16, 8, 4, 0, 8, true, 2)         \
+  X(6, 8, 16, 13, 0, 7, false, 2)       \
+  X(4, 16, 16, 7, 0, 7, false, 1)       \
+  X(5, 16, 16, 7, 0, 7, true, 1)
 
-template <int TR, int TC, int A, int BC, bool TWO, int MINB>
+template <int TR, int TC, int A, int AS, int BC, bool TWO, int MINB>
 cudaError_t launch_one(const SimplexArgs& a, int grid_override, cudaStream_t s, int* ctas) {
-  auto kern = simplex_reg_kernel<TR, TC, A, BC, TWO, MINB>;
-  const size_t dsm = a.prefetch ? (size_t)a.m * a.n * 8 : 0;
+  auto kern = simplex_reg_kernel<TR, TC, A, AS, BC, TWO, MINB>;
+  const size_t dsm = AS > 0 ? (size_t)AS * ((BC + 1) / 2) * TR * TC * 16
+                            : (a.prefetch ? (size_t)a.m * a.n * 8 : 0);
   // attribute + occupancy queries are host round trips: cache them per (device, smem size)
   static int cached_dev = -1, per_sm = 0;
   static size_t cached_dsm = (size_t)-1;
@@ -624,7 +696,7 @@ cudaError_t launch_one(const SimplexArgs& a, int grid_override, cudaStream_t s, 
 }  // namespace
 
 static const RegCfg kCfgs[] = {
-#define X(id, TR, TC, A, BC, TWO, MINB) {TR * A, TC * BC, TWO ? 1 : 0, id},
+#define X(id, TR, TC, A, AS, BC, TWO, MINB) {TR * (A + AS), TC * BC, TWO ? 1 : 0, id},
     LPB_REG_CONFIGS(X)
 #undef X
 };
@@ -649,8 +721,8 @@ bool reg_fits(int m, int n, int kmax) { return pick_cfg(m, n, kmax) >= 0; }
 cudaError_t launch_simplex_reg(const SimplexArgs& a, int grid_override, cudaStream_t s,
                                int* ctas_out) {
   switch (pick_cfg(a.m, a.n, a.kmax)) {
-#define X(id, TR, TC, A, BC, TWO, MINB) \
-  case id: return launch_one<TR, TC, A, BC, TWO, MINB>(a, grid_override, s, ctas_out);
+#define X(id, TR, TC, A, AS, BC, TWO, MINB) \
+  case id: return launch_one<TR, TC, A, AS, BC, TWO, MINB>(a, grid_override, s, ctas_out);
     LPB_REG_CONFIGS(X)
 #undef X
     default: return cudaErrorInvalidValue;
