@@ -76,6 +76,15 @@ __device__ __forceinline__ Cand warp_reduce(Cand c) {
   return r;
 }
 
+// One CTA's speculative pivot proposal: its best local entering candidate and the ratio-test
+// result on that column (the global winner is one of the CL proposals).
+struct Rec {
+  Cand ce;
+  double theta;
+  int l;
+  int pad;
+};
+
 struct Ctl {
   double theta;
   double binf;
@@ -84,6 +93,10 @@ struct Ctl {
   int k;
   int pad;
 };
+
+// Tableau row stride (doubles): even, so rows are 128-bit pair arrays, with S/2 odd so that a
+// column read by 32 consecutive rows spreads over the banks.
+__host__ __device__ __forceinline__ int row_stride(int Q) { return 2 * (((Q + 2) >> 1) | 1); }
 
 struct Smem {
   double* T;      // rows x S
@@ -96,6 +109,8 @@ struct Smem {
   int* wcount;    // NW ints
   Cand* wslots;   // 2 x NW
   Cand* cslots;   // 2 x CL
+  Rec* rec;       // 2 x CL proposals (parity-buffered), written by every CTA of the cluster
+  double* colC;   // 2 x CL x RC proposal columns (parity-buffered)
   Ctl* ctl;
 };
 
@@ -163,10 +178,10 @@ __device__ __forceinline__ Cand cluster_reduce(Cand c, const Smem& s, int& par,
 // the pivot row (fma(1, prow, 0)), the swapped column (fma(-f_i, rl, 0)) and every other
 // element -- no per-element branch.  Warps walk rows, lanes walk columns (conflict-free
 // SMEM rows, odd stride), the lane's prow values stay in registers.
-__device__ __forceinline__ void pivot_local(const Smem& s, int S, int Wa, int nrow, int l,
-                                            bool own, int jloc, int ent_var) {
+__device__ __forceinline__ void pivot_local(const Smem& s, const double* colE, int S, int Wa,
+                                            int nrow, int l, bool own, int jloc, int ent_var) {
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const double pe = s.colE[l];
+  const double pe = colE[l];
   const double rpe = recip_of(pe);
   for (int j = tid; j < Wa; j += NT) {
     const bool sw = own && j == jloc;
@@ -179,29 +194,57 @@ __device__ __forceinline__ void pivot_local(const Smem& s, int S, int Wa, int nr
     *tl = 0.0;
   }
   for (int i = tid; i < nrow; i += NT) {
-    s.fcol[i] = (i == l) ? 1.0 : -s.colE[i];
+    s.fcol[i] = (i == l) ? 1.0 : -colE[i];
     if (own) s.T[i * S + jloc] = 0.0;
   }
   if (tid == 0) {
     const int leaving = s.bkey[l];
     s.bkey[l] = ent_var;
     if (own) s.nbvar[jloc] = leaving < 0 ? DEAD : leaving;
+    if (Wa & 1) s.prow[Wa] = 0.0;  // pad of the last pair (Wa + 1 <= S)
   }
   __syncthreads();
-  constexpr int MAXC = 8;  // Wa <= 256 local columns per CTA
-  double pr[MAXC];
+  // 128-bit pairs of columns: lane handles pairs lane + 32c (Wa <= 256 -> <= 4 chunks)
+  constexpr int MAXC = 4;
+  const int Wa2 = (Wa + 1) >> 1, S2 = S >> 1;
+  const double2* prow2 = reinterpret_cast<const double2*>(s.prow);
+  double2 pr[MAXC];
 #pragma unroll
   for (int c = 0; c < MAXC; ++c) {
     const int j = lane + 32 * c;
-    pr[c] = (j < Wa) ? s.prow[j] : 0.0;
+    pr[c] = (j < Wa2) ? prow2[j] : make_double2(0.0, 0.0);
   }
-  const int nch = (Wa + 31) >> 5;
-  for (int i = w; i < nrow; i += NW) {
-    const double f = s.fcol[i];
-    double* row = s.T + i * S + lane;
+  double2* T2 = reinterpret_cast<double2*>(s.T);
+  if (Wa2 <= 64) {  // the common case: two chunks
+    for (int i = w; i < nrow; i += NW) {
+      const double f = s.fcol[i];
+      double2* row = T2 + i * S2 + lane;
+      if (lane < Wa2) {
+        double2 v0 = row[0];
+        v0.x = __fma_rn(f, pr[0].x, v0.x);
+        v0.y = __fma_rn(f, pr[0].y, v0.y);
+        row[0] = v0;
+      }
+      if (lane + 32 < Wa2) {
+        double2 v1 = row[32];
+        v1.x = __fma_rn(f, pr[1].x, v1.x);
+        v1.y = __fma_rn(f, pr[1].y, v1.y);
+        row[32] = v1;
+      }
+    }
+  } else {
+    for (int i = w; i < nrow; i += NW) {
+      const double f = s.fcol[i];
+      double2* row = T2 + i * S2 + lane;
 #pragma unroll
-    for (int c = 0; c < MAXC; ++c) {
-      if (c < nch && lane + 32 * c < Wa) row[32 * c] = __fma_rn(f, pr[c], row[32 * c]);
+      for (int c = 0; c < MAXC; ++c) {
+        if (lane + 32 * c < Wa2) {
+          double2 v = row[32 * c];
+          v.x = __fma_rn(f, pr[c].x, v.x);
+          v.y = __fma_rn(f, pr[c].y, v.y);
+          row[32 * c] = v;
+        }
+      }
     }
   }
   __syncthreads();
@@ -214,7 +257,7 @@ __global__ void __launch_bounds__(NT) simplex_block_kernel(SimplexArgs a) {
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int m = a.m, n = a.n;
   const int Q = (n + a.kmax + CL - 1) / CL;  // nonbasic positions per CTA (capacity)
-  const int S = (Q + 1) | 1;                 // odd row stride: conflict-free column reads
+  const int S = row_stride(Q);  // even (128-bit rows), S/2 odd (spread column reads)
   const int RC = m + 2;
 
   Smem s;
@@ -222,7 +265,7 @@ __global__ void __launch_bounds__(NT) simplex_block_kernel(SimplexArgs a) {
   s.colE = s.T + (size_t)RC * S;
   s.fcol = s.colE + RC;
   s.prow = s.fcol + RC;
-  s.nbvar = reinterpret_cast<int*>(s.prow + (Q + 1));
+  s.nbvar = reinterpret_cast<int*>(s.prow + S);
   s.bkey = s.nbvar + (Q + 1);
   s.negrows = s.bkey + m;
   s.wcount = s.negrows + m;
@@ -230,7 +273,9 @@ __global__ void __launch_bounds__(NT) simplex_block_kernel(SimplexArgs a) {
   p = (p + 15) & ~uintptr_t(15);
   s.wslots = reinterpret_cast<Cand*>(p);
   s.cslots = s.wslots + 2 * NW;
-  s.ctl = reinterpret_cast<Ctl*>(s.cslots + 2 * CL);
+  s.rec = reinterpret_cast<Rec*>(s.cslots + 2 * CL);
+  s.colC = reinterpret_cast<double*>(s.rec + 2 * CL);
+  s.ctl = reinterpret_cast<Ctl*>(s.colC + 2 * CL * RC);
 
   int par = 0;
   for (;;) {
@@ -279,16 +324,19 @@ __global__ void __launch_bounds__(NT) simplex_block_kernel(SimplexArgs a) {
     int st = -1, it1 = 0, it2 = 0;
     const int cnt = max(0, min(Q, n + k - cl.rank * Q));  // live local positions
     const int Wa = cnt + 1;                               // + RHS at local column cnt
+    const int Wp = (Wa + 1) & ~1;                         // whole 128-bit pairs
     const int g0 = cl.rank * Q;
     if (k > a.kmax) st = ST_NUMERICAL;  // cannot happen: kmax comes from the prepass
 
     if (st < 0) {
       for (int i = w; i < m; i += NW) {
         const bool neg = s.bkey[i] < 0;
-        for (int j = lane; j < Wa; j += 32) {
+        for (int j = lane; j < Wp; j += 32) {
           const int gp = g0 + j;
           double v;
-          if (j == cnt) {
+          if (j >= Wa) {
+            v = 0.0;  // pad column of the last 128-bit pair
+          } else if (j == cnt) {
             v = __ldg(bk + i);
             v = neg ? -v : v;
           } else if (gp < n) {
@@ -300,14 +348,14 @@ __global__ void __launch_bounds__(NT) simplex_block_kernel(SimplexArgs a) {
           s.T[i * S + j] = v;
         }
       }
-      for (int j = tid; j < Wa; j += NT) {
+      for (int j = tid; j < Wp; j += NT) {
         const int gp = g0 + j;
         s.T[m * S + j] = (j < cnt && gp < n) ? __ldg(ck + gp) : 0.0;
         if (j < cnt) s.nbvar[j] = gp < n ? gp : n + s.negrows[gp - n];
       }
       __syncthreads();
       if (k > 0) {  // phase-I row: ascending-row sums of the negated rows (R7)
-        for (int j = tid; j < Wa; j += NT) {
+        for (int j = tid; j < Wp; j += NT) {
           double acc = 0.0;
           for (int t = 0; t < k; ++t) acc = __dadd_rn(acc, s.T[s.negrows[t] * S + j]);
           s.T[(m + 1) * S + j] = acc;
@@ -317,12 +365,14 @@ __global__ void __launch_bounds__(NT) simplex_block_kernel(SimplexArgs a) {
     }
 
     // ---- Steps 1-3 loop, two phases ----
-    int phase = (k > 0) ? 1 : 2, stall = 0;
+    int phase = (k > 0) ? 1 : 2, stall = 0, pp = 0;
     while (st < 0) {
       const int objrow = (phase == 1) ? m + 1 : m;
       const int nrow = (phase == 1) ? m + 2 : m + 1;
       const bool bland = a.bland_K > 0 && stall >= a.bland_K;
-      // Step 1: entering variable (LPC/Dantzig, lowest variable index on ties; Bland)
+      // Step 1: this CTA's entering candidate (LPC/Dantzig, lowest variable index on ties;
+      // Bland), then Step 2 on that candidate column, speculatively: the global winner is
+      // one of the CL proposals, so ONE cluster barrier per pivot publishes them all.
       Cand ce{0.0, 0, -1};
       for (int j = tid; j < cnt; j += NT) {
         const int var = s.nbvar[j];
@@ -332,8 +382,45 @@ __global__ void __launch_bounds__(NT) simplex_block_kernel(SimplexArgs a) {
           if (bland ? better<MIN_KEY>(cd, ce) : better<MAX_V>(cd, ce)) ce = cd;
         }
       }
-      ce = bland ? cluster_reduce<MIN_KEY, CL>(ce, s, par, cl)
-                 : cluster_reduce<MAX_V, CL>(ce, s, par, cl);
+      ce = bland ? block_reduce<MIN_KEY>(ce, s.wslots) : block_reduce<MAX_V>(ce, s.wslots);
+      Cand cr{0.0, 0, -1};
+      const int jc = ce.pos - g0;  // local column of the proposal
+      if (ce.pos >= 0) {
+        for (int i = tid; i < m; i += NT) {
+          const double ai = s.T[i * S + jc];
+          if (ai > a.eps_piv) {
+            bool slow;
+            double r = div_fast(s.T[i * S + cnt], ai, slow);
+            if (slow) r = __ddiv_rn(s.T[i * S + cnt], ai);
+            const Cand cc{r, bland ? s.bkey[i] : i, i};
+            if (better<MIN_V>(cc, cr)) cr = cc;
+          }
+        }
+      }
+      cr = block_reduce<MIN_V>(cr, s.wslots + NW);
+      double* const myc = s.colC + (size_t)(pp * CL + cl.rank) * RC;
+      if (ce.pos >= 0)
+        for (int i = tid; i < nrow; i += NT) {
+          const double v = s.T[i * S + jc];
+#pragma unroll
+          for (int q = 0; q < CL; ++q) cl.remote(myc, q)[i] = v;
+        }
+      if (tid == 0) {
+        const Rec r{ce, cr.v, cr.pos, 0};
+#pragma unroll
+        for (int q = 0; q < CL; ++q) *cl.remote(s.rec + pp * CL + cl.rank, q) = r;
+      }
+      cl.sync();
+      int win = 0;
+      ce = s.rec[pp * CL].ce;
+#pragma unroll
+      for (int q = 1; q < CL; ++q) {
+        const Cand o = s.rec[pp * CL + q].ce;
+        if (bland ? better<MIN_KEY>(o, ce) : better<MAX_V>(o, ce)) {
+          ce = o;
+          win = q;
+        }
+      }
       if (ce.pos < 0) {
         if (phase == 2) { st = ST_OPTIMAL; break; }
         // phase switch (R8, R9): infeasibility test, drive artificials out, drop phase-I row
@@ -360,50 +447,23 @@ __global__ void __launch_bounds__(NT) simplex_block_kernel(SimplexArgs a) {
             }
           }
           cl.sync();
-          pivot_local(s, S, Wa, m + 2, l, cl.rank == owner, jloc, cd.key);
+          pivot_local(s, s.colE, S, Wa, m + 2, l, cl.rank == owner, jloc, cd.key);
           ++it1;
         }
         phase = 2;
         stall = 0;
+        pp ^= 1;  // the proposal slots of this round may still be read by a peer CTA
         continue;
       }
       if (it1 + it2 >= a.max_iter) { st = ST_ITER_LIMIT; break; }
-      // Step 2: ratio test on the owner CTA (RHS is replicated), sentinel = no candidate
-      const int owner = ce.pos / Q, jloc = ce.pos - owner * Q;
-      if (cl.rank == owner) {
-        Cand cr{0.0, 0, -1};
-        for (int i = tid; i < m; i += NT) {
-          const double ai = s.T[i * S + jloc];
-          if (ai > a.eps_piv) {
-            bool slow;
-            double r = div_fast(s.T[i * S + cnt], ai, slow);
-            if (slow) r = __ddiv_rn(s.T[i * S + cnt], ai);
-            const Cand cc{r, bland ? s.bkey[i] : i, i};
-            if (better<MIN_V>(cc, cr)) cr = cc;
-          }
-        }
-        Cand* ws = s.wslots + par * NW;
-        par ^= 1;
-        cr = block_reduce<MIN_V>(cr, ws);
-        for (int i = tid; i < nrow; i += NT) {
-          const double v = s.T[i * S + jloc];
-          for (int q = 0; q < CL; ++q) cl.remote(s.colE, q)[i] = v;
-        }
-        if (tid == 0)
-          for (int q = 0; q < CL; ++q) {
-            Ctl* c = cl.remote(s.ctl, q);
-            c->l = cr.pos;
-            c->theta = cr.v;
-          }
-      } else {
-        par ^= 1;  // keep the slot parity identical in every CTA
-      }
-      cl.sync();
-      const int l = s.ctl->l;
-      const double theta = s.ctl->theta;
+      const int l = s.rec[pp * CL + win].l;
+      const double theta = s.rec[pp * CL + win].theta;
       if (l < 0) { st = (phase == 2) ? ST_UNBOUNDED : ST_NUMERICAL; break; }
-      // Step 3: pivot
-      pivot_local(s, S, Wa, nrow, l, cl.rank == owner, jloc, ce.key);
+      // Step 3: pivot (the winner's column is in this CTA's slot `win`)
+      const int jloc = ce.pos - win * Q;
+      pivot_local(s, s.colC + (size_t)(pp * CL + win) * RC, S, Wa, nrow, l, cl.rank == win, jloc,
+                  ce.key);
+      pp ^= 1;
       if (phase == 1) ++it1; else ++it2;
       stall = (theta > 0.0) ? 0 : stall + 1;
     }
@@ -439,11 +499,12 @@ __global__ void __launch_bounds__(NT) simplex_block_kernel(SimplexArgs a) {
 
 size_t block_smem_bytes(int cl, int m, int n, int kmax) {
   const int Q = (n + kmax + cl - 1) / cl;
-  const int S = (Q + 1) | 1;
-  size_t bytes = sizeof(double) * ((size_t)(m + 2) * S + 2 * (size_t)(m + 2) + (Q + 1));
+  const int S = row_stride(Q);
+  size_t bytes = sizeof(double) * ((size_t)(m + 2) * S + 2 * (size_t)(m + 2) + S);
   bytes += sizeof(int) * ((size_t)(Q + 1) + 2 * (size_t)m + NW);
   bytes = (bytes + 15) & ~size_t(15);
-  bytes += sizeof(Cand) * (2 * NW + 2 * cl) + sizeof(Ctl);
+  bytes += sizeof(Cand) * (2 * NW + 2 * cl) + sizeof(Rec) * 2 * cl +
+           sizeof(double) * 2 * (size_t)cl * (m + 2) + sizeof(Ctl);
   return bytes;
 }
 
