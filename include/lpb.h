@@ -74,7 +74,11 @@ enum { /* lpb_solve_batch flags */
   LPB_DEVICE_PTRS = 1u, /* A, b, c are device pointers (e.g. torch CUDA tensors)              */
   LPB_SHARED_BOX = 2u,  /* hyperbox: one box (2n entries of b) for the whole batch             */
   LPB_NO_X = 4u,        /* do not produce x (saves 8n bytes per LP of HBM / D2H traffic)       */
-  LPB_ASYNC = 8u        /* enqueue only; do not synchronize before returning                   */
+  LPB_ASYNC = 8u,       /* enqueue only; do not synchronize before returning                   */
+  LPB_SHARED_AB = 16u   /* general LPs: one constraint system (A: m x n, b: m) for the whole
+                           batch, only c varies per LP -- many objectives over one polytope,
+                           the support-function sampling of PAPER.md:313,330 (SURVEY §8(f)
+                           NEXT-1); A and b are read with stride 0                            */
 };
 
 typedef struct {

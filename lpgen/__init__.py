@@ -31,6 +31,7 @@ __all__ = [
     "degenerate",
     "klee_minty",
     "chvatal_cycling",
+    "shared_polytope",
     "CONFIGS",
     "make_config",
 ]
@@ -209,13 +210,26 @@ def chvatal_cycling():
     return A, b, c
 
 
-# BASELINE.json configs (SURVEY §8(d) "Configs as concrete runs"; seeds cfgK -> K).
+def shared_polytope(B: int, m: int, n: int, seed: int, gen: str = "G1"):
+    """Many objectives over ONE polytope (the support-function sampling
+    of PAPER.md:313,330 for a general polytope): A (m x n) and b (m) are LP 0 of G1 / G2 with
+    this seed, and the B objectives are c ~ U[-10,10)^{B x n} drawn from PCG64([seed, 1]).
+    Returns (A [m, n], b [m], c [B, n]) -- the LPB_SHARED_AB layout."""
+    A, b, _ = {"G1": signed_bounded, "G2": twophase_signed}[gen](1, m, n, seed)
+    c = np.random.Generator(np.random.PCG64([seed, 1])).uniform(-10.0, 10.0, size=(B, n))
+    return np.ascontiguousarray(A[0]), np.ascontiguousarray(b[0]), c
+
+
+# BASELINE.json configs (SURVEY §8(d) "Configs as concrete runs"; seeds cfgK -> K).  The
+# "s" configs are the NEXT-1 shared-constraint variants (one polytope, B objectives).
 CONFIGS = {
     "cfg1": dict(kind="general", gen="G1", B=1000, m=5, n=5, seed=1),
     "cfg2": dict(kind="general", gen="G1", B=50000, m=100, n=100, seed=2),
     "cfg3": dict(kind="general", gen="G2", B=10000, m=200, n=200, seed=3),
     "cfg4": dict(kind="hyperbox", gen="G3", B=4001000, n=5, seed=4),
     "cfg5": dict(kind="hyperbox", gen="G3", B=6003000, n=28, seed=5),
+    "cfg2s": dict(kind="general", gen="G1", B=50000, m=100, n=100, seed=2, shared=True),
+    "cfg3s": dict(kind="general", gen="G2", B=10000, m=200, n=200, seed=3, shared=True),
 }
 
 
@@ -226,6 +240,8 @@ def make_config(name: str, B: int | None = None):
     Bv = cfg["B"] if B is None else B
     if cfg["kind"] == "hyperbox":
         return hyperbox(Bv, cfg["n"], cfg["seed"])
+    if cfg.get("shared"):
+        return shared_polytope(Bv, cfg["m"], cfg["n"], cfg["seed"], cfg["gen"])
     gen = {"G1": signed_bounded, "G2": twophase_signed}[cfg["gen"]]
     return gen(Bv, cfg["m"], cfg["n"], cfg["seed"])
 
@@ -286,5 +302,11 @@ def make_config_shard(name: str, B: int, lo: int, hi: int):
     if cfg["kind"] == "hyperbox":
         lo_b, hi_b, dirs = hyperbox(B, cfg["n"], cfg["seed"])
         return lo_b, hi_b, np.ascontiguousarray(dirs[lo:hi])
+    if cfg.get("shared"):
+        A, b, _ = shared_polytope(1, cfg["m"], cfg["n"], cfg["seed"], cfg["gen"])
+        bg = np.random.PCG64([cfg["seed"], 1])
+        g = np.random.Generator(bg)
+        bg.advance(lo * cfg["n"])
+        return A, b, g.uniform(-10.0, 10.0, size=(hi - lo, cfg["n"]))
     f = {"G1": signed_bounded_shard, "G2": twophase_signed_shard}[cfg["gen"]]
     return f(B, cfg["m"], cfg["n"], cfg["seed"], lo, hi)

@@ -221,13 +221,15 @@ static int choose_class(const lpb_ctx* c, int kmax, int* cl) {
 
 static void fill_args(const lpb_ctx* c, SimplexArgs& a, int64_t lp0, int64_t cnt,
                       const double* A, const double* b, const double* cv, bool nox,
-                      int kmax, int* ticket) {
+                      int kmax, int* ticket, bool sab) {
   const int m = c->m, n = c->n;
   a.batch = cnt;
   a.m = m;
   a.n = n;
   a.A = A;
   a.b = b;
+  a.sA = sab ? 0 : (int64_t)c->m * c->n;
+  a.sb = sab ? 0 : (int64_t)c->m;
   a.c = cv;
   a.status = c->d_status + lp0;
   a.obj = c->d_obj + lp0;
@@ -253,7 +255,7 @@ static void fill_args(const lpb_ctx* c, SimplexArgs& a, int64_t lp0, int64_t cnt
 // when a register layout holds even the worst case k = m, no prepass is needed; otherwise
 // one tiny prepass kernel + a 4-byte D2H give kmax first.
 static int run_general(lpb_ctx* c, cudaStream_t s, int64_t lp0, int64_t cnt, const double* A,
-                       const double* b, const double* cv, bool nox, int kmax_known,
+                       const double* b, const double* cv, bool nox, bool sab, int kmax_known,
                        int* ticket, int* launches) {
   int kmax = kmax_known;
   const int forced = c->opt.kernel_class;
@@ -264,7 +266,7 @@ static int run_general(lpb_ctx* c, cudaStream_t s, int64_t lp0, int64_t cnt, con
   if (forced == CLASS_S || s_auto) {
     if (!thread_fits(c->m, c->n)) return LPB_ETOOBIG;
     SimplexArgs a;  // worst-case width reserved: no prepass
-    fill_args(c, a, lp0, cnt, A, b, cv, nox, c->m, ticket);
+    fill_args(c, a, lp0, cnt, A, b, cv, nox, c->m, ticket, sab);
     const bool timed = (s == c->stream);
     if (timed) LPB_CUDA(c, cudaEventRecord(c->kev0, s));
     LPB_CUDA(c, launch_simplex_thread(a, s));
@@ -280,7 +282,7 @@ static int run_general(lpb_ctx* c, cudaStream_t s, int64_t lp0, int64_t cnt, con
   if (kmax < 0 && r_ok_worst && (forced == CLASS_AUTO || forced == CLASS_R))
     kmax = c->m;  // worst-case capacity, no prepass
   if (kmax < 0) {  // device prepass: kmax over the chunk (one tiny kernel + 4-byte D2H)
-    LPB_CUDA(c, launch_count_art(b, cnt, c->m, c->d_kmax, s));
+    LPB_CUDA(c, launch_count_art(b, sab ? 1 : cnt, c->m, c->d_kmax, s));
     LPB_CUDA(c, cudaMemcpyAsync(c->h_kmax, c->d_kmax, sizeof(int), cudaMemcpyDeviceToHost, s));
     LPB_CUDA(c, cudaStreamSynchronize(s));
     kmax = *c->h_kmax;
@@ -290,7 +292,7 @@ static int run_general(lpb_ctx* c, cudaStream_t s, int64_t lp0, int64_t cnt, con
   const int klass = choose_class(c, kmax, &cl);
   if (klass < 0) return LPB_ETOOBIG;
   SimplexArgs a;
-  fill_args(c, a, lp0, cnt, A, b, cv, nox, kmax, ticket);
+  fill_args(c, a, lp0, cnt, A, b, cv, nox, kmax, ticket, sab);
   LPB_CUDA(c, cudaMemsetAsync(ticket, 0, sizeof(int), s));
   int ctas = 0;
   const bool timed = (s == c->stream);
@@ -362,6 +364,7 @@ static int solve_impl(lpb_ctx* c, const double* A, const double* b, const double
   if ((general && (!A || !b || !cv)) || (!general && (A || !b || !cv))) return LPB_EINVAL;
   const bool nox = (flags & LPB_NO_X) != 0;
   const bool shared = (flags & LPB_SHARED_BOX) != 0;
+  const bool sab = general && (flags & LPB_SHARED_AB) != 0;
   if (o_x && nox) return LPB_EINVAL;
   LPB_CUDA(c, cudaSetDevice(c->device));
   c->solved = false;
@@ -374,7 +377,7 @@ static int solve_impl(lpb_ctx* c, const double* A, const double* b, const double
   if (flags & LPB_DEVICE_PTRS) {
     c->host_path = false;
     LPB_CUDA(c, cudaEventRecord(c->ev0, c->stream));
-    int rc = general ? run_general(c, c->stream, 0, B, A, b, cv, nox, -1, c->d_ticket,
+    int rc = general ? run_general(c, c->stream, 0, B, A, b, cv, nox, sab, -1, c->d_ticket,
                                    &c->last_launches)
                      : run_hyperbox(c, c->stream, 0, B, cv, b, shared, nox, &c->last_launches);
     if (rc != LPB_OK) return rc;
@@ -398,7 +401,7 @@ static int solve_impl(lpb_ctx* c, const double* A, const double* b, const double
   int kmax = -1;
   if (general) {  // kmax from the host copy of b (no device round trip inside the pipeline)
     int best = 0;
-    for (int64_t k = 0; k < B; ++k) {
+    for (int64_t k = 0; k < (sab ? 1 : B); ++k) {
       int cnt = 0;
       const double* bk = b + k * m;
       for (int i = 0; i < m; ++i) cnt += (bk[i] < 0.0);
@@ -412,14 +415,22 @@ static int solve_impl(lpb_ctx* c, const double* A, const double* b, const double
     cudaStream_t s = c->chunk_streams[q];
     LPB_CUDA(c, cudaStreamWaitEvent(s, c->ev0, 0));
     if (general) {
-      LPB_CUDA(c, cudaMemcpyAsync(c->d_A + lp0 * m * (int64_t)n, A + lp0 * m * (int64_t)n,
-                                  8 * cnt * m * (int64_t)n, cudaMemcpyHostToDevice, s));
-      LPB_CUDA(c, cudaMemcpyAsync(c->d_b + lp0 * m, b + lp0 * m, 8 * cnt * m,
-                                  cudaMemcpyHostToDevice, s));
+      // shared constraints (LPB_SHARED_AB): A and b cross PCIe once, on the first chunk's
+      // stream; the other chunks wait for that copy
+      const int64_t sA = sab ? 0 : m * (int64_t)n, sb = sab ? 0 : m;
+      if (q == 0 || !sab) {
+        LPB_CUDA(c, cudaMemcpyAsync(c->d_A + lp0 * sA, A + lp0 * sA,
+                                    8 * (sab ? m * (int64_t)n : cnt * sA),
+                                    cudaMemcpyHostToDevice, s));
+        LPB_CUDA(c, cudaMemcpyAsync(c->d_b + lp0 * sb, b + lp0 * sb, 8 * (sab ? m : cnt * sb),
+                                    cudaMemcpyHostToDevice, s));
+      }
+      if (sab && q == 0) LPB_CUDA(c, cudaEventRecord(c->chunk_done[0], s));
+      if (sab && q > 0) LPB_CUDA(c, cudaStreamWaitEvent(s, c->chunk_done[0], 0));
       LPB_CUDA(c, cudaMemcpyAsync(c->d_c + lp0 * n, cv + lp0 * n, 8 * cnt * n,
                                   cudaMemcpyHostToDevice, s));
-      rc = run_general(c, s, lp0, cnt, c->d_A + lp0 * m * (int64_t)n, c->d_b + lp0 * m,
-                       c->d_c + lp0 * n, nox, kmax, c->d_ticket + q, &c->last_launches);
+      rc = run_general(c, s, lp0, cnt, c->d_A + lp0 * sA, c->d_b + lp0 * sb, c->d_c + lp0 * n,
+                       nox, sab, kmax, c->d_ticket + q, &c->last_launches);
     } else {
       const int64_t bstride = shared ? 0 : 2 * (int64_t)n;
       if (q == 0 || !shared)

@@ -18,8 +18,9 @@ enum : int32_t { CLASS_AUTO = 0, CLASS_S = 1, CLASS_M = 2, CLASS_L = 3, CLASS_R 
 struct SimplexArgs {
   int64_t batch;
   int m, n;
-  const double* A;  // batch x m x n
-  const double* b;  // batch x m
+  const double* A;  // batch x m x n (LP k at A + k * sA)
+  const double* b;  // batch x m     (LP k at b + k * sb)
+  int64_t sA, sb;   // per-LP strides in elements: m*n and m, or 0 (LPB_SHARED_AB)
   const double* c;  // batch x n
   int32_t* status;
   double* obj;

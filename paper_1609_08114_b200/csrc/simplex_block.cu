@@ -287,8 +287,8 @@ __global__ void __launch_bounds__(NT) simplex_block_kernel(SimplexArgs a) {
     const int64_t lp = s.ctl->lp;
     if (lp >= a.batch) break;
 
-    const double* __restrict__ Ak = a.A + lp * (int64_t)m * n;
-    const double* __restrict__ bk = a.b + lp * (int64_t)m;
+    const double* __restrict__ Ak = a.A + lp * a.sA;
+    const double* __restrict__ bk = a.b + lp * a.sb;
     const double* __restrict__ ck = a.c + lp * (int64_t)n;
 
     // ---- build (reading R7): negated rows, basis keys, |b|_inf ----

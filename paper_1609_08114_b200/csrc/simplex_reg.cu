@@ -135,14 +135,14 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
     // direct mode (grid = batch, no ticket): CTA b solves LP b
     const int t = direct ? (int)blockIdx.x : atomicAdd(a.ticket, 1);
     sm.lp = t;
-    if (pf && t < a.batch) bulk_load(abuf, a.A + (int64_t)t * m * n, abytes, &sm.mbar);
+    if (pf && t < a.batch) bulk_load(abuf, a.A + (int64_t)t * a.sA, abytes, &sm.mbar);
   }
   gsync<NT>();
 
   for (;;) {
     const int64_t lp = sm.lp;
     if (lp >= a.batch) break;
-    const double* __restrict__ bk = a.b + lp * (int64_t)m;
+    const double* __restrict__ bk = a.b + lp * a.sb;
     const double* __restrict__ ck = a.c + lp * (int64_t)n;
     // issue the b and c loads before waiting for A (overlapping DRAM round trips)
     const double b_pre = (tid < m) ? __ldg(bk + tid) : 0.0;
@@ -156,7 +156,7 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
       mbar_wait(&sm.mbar, mphase);
       mphase ^= 1u;
     }
-    const double* __restrict__ Ak = pf ? abuf : a.A + lp * (int64_t)m * n;
+    const double* __restrict__ Ak = pf ? abuf : a.A + lp * a.sA;
 
     // ---- build: negated rows (ascending), basis keys, |b|_inf, RHS (R7) ----
     int k = 0;
@@ -276,7 +276,7 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
     if (tid == 0) {
       const int t = direct ? (int)a.batch : atomicAdd(a.ticket, 1);
       sm.lp = t;
-      if (pf && t < a.batch) bulk_load(abuf, a.A + (int64_t)t * m * n, abytes, &sm.mbar);
+      if (pf && t < a.batch) bulk_load(abuf, a.A + (int64_t)t * a.sA, abytes, &sm.mbar);
     }
 
     // ---- Steps 1-3, two phases ----

@@ -40,8 +40,8 @@ __global__ void __launch_bounds__(S_NT) simplex_thread_kernel(SimplexArgs a) {
   auto bkey = [&](int i) -> int& { return ib[i * S_NT]; };
   auto nbv = [&](int p) -> int& { return ib[(S_MAXM + p) * S_NT]; };
   auto neg = [&](int t) -> int& { return ib[(S_MAXM + S_MAXM + S_MAXN + t) * S_NT]; };
-  const double* Ak = a.A + lp * (int64_t)m * n;
-  const double* bk = a.b + lp * (int64_t)m;
+  const double* Ak = a.A + lp * a.sA;
+  const double* bk = a.b + lp * a.sb;
   const double* ck = a.c + lp * (int64_t)n;
 
   // ---- build (R7) ----

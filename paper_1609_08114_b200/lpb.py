@@ -26,7 +26,7 @@ _lib = ctypes.CDLL(LIB_PATH)
 GENERAL, HYPERBOX = 0, 1
 OPTIMAL, UNBOUNDED, INFEASIBLE, ITER_LIMIT, NUMERICAL = range(5)
 OK, EINVAL, ENOMEM, ECUDA, ESTATE, ETOOBIG = 0, -1, -2, -3, -4, -5
-DEVICE_PTRS, SHARED_BOX, NO_X, ASYNC = 1, 2, 4, 8
+DEVICE_PTRS, SHARED_BOX, NO_X, ASYNC, SHARED_AB = 1, 2, 4, 8, 16
 CLASS_NAMES = {0: "auto", 1: "S", 2: "M", 3: "L", 4: "R", 5: "H"}
 CLASS_IDS = {v: k for k, v in CLASS_NAMES.items()}
 
@@ -172,18 +172,23 @@ class Solver:
             pass
 
     # -- solves --
-    def solve_device(self, A, b, c, *, shared_box=False, want_x=True, sync=False):
+    def solve_device(self, A, b, c, *, shared_box=False, shared_ab=False, want_x=True,
+                     sync=False):
         """Device tensors in; results stay in the context's device buffers (see
-        ``device_results``).  Asynchronous on the context's stream unless ``sync``."""
-        flags = DEVICE_PTRS | (SHARED_BOX if shared_box else 0) | (0 if want_x else NO_X)
+        ``device_results``).  Asynchronous on the context's stream unless ``sync``.
+        ``shared_ab``: A (m x n) and b (m) are one constraint system for the whole batch."""
+        flags = (DEVICE_PTRS | (SHARED_BOX if shared_box else 0) | (0 if want_x else NO_X) |
+                 (SHARED_AB if shared_ab else 0))
         if not sync:
             flags |= ASYNC
         _check(_lib.lpb_solve_batch(self._ctx, _dptr(A), _dptr(b), _dptr(c), flags), self._ctx)
 
-    def solve_host_into(self, A, b, c, status, obj, x=None, iters=None, *, shared_box=False):
+    def solve_host_into(self, A, b, c, status, obj, x=None, iters=None, *, shared_box=False,
+                        shared_ab=False):
         """End-to-end path: host arrays in (pinned for overlap), results copied into host
         arrays, chunk by chunk on the library's streams; returns when done."""
-        flags = (SHARED_BOX if shared_box else 0) | (0 if x is not None else NO_X)
+        flags = ((SHARED_BOX if shared_box else 0) | (0 if x is not None else NO_X) |
+                 (SHARED_AB if shared_ab else 0))
         _check(_lib.lpb_solve_batch_into(self._ctx, _hptr(A), _hptr(b), _hptr(c), flags,
                                          _hptr(status), _hptr(obj), _hptr(x), _hptr(iters)),
                self._ctx)
@@ -238,23 +243,29 @@ def _wrap_device(ptr, shape, dtype, device):
 
 def solve(A, b, c, *, want_x=True, **opts):
     """One-shot solve of max c.x s.t. A x <= b, x >= 0 for a batch.
+    A (B x m x n), b (B x m), c (B x n); or A (m x n) and b (m) shared by every LP (many
+    objectives over one polytope, LPB_SHARED_AB).
     torch CUDA tensors -> torch results (device path, synchronous);
     numpy arrays -> numpy results (host pipeline)."""
+    shared = len(A.shape) == 2
     if _is_torch(A):
-        B, m, n = A.shape
+        B, n = c.shape
+        m = A.shape[-2]
         s = Solver(B, m, n, GENERAL, **opts)
-        s.solve_device(A, b, c, want_x=want_x, sync=True)
+        s.solve_device(A, b, c, want_x=want_x, sync=True, shared_ab=shared)
         res = {k: v.clone() for k, v in s.device_results(want_x).items()}
         s.close()
         return res
     A = np.ascontiguousarray(A, np.float64)
     b = np.ascontiguousarray(b, np.float64)
     c = np.ascontiguousarray(c, np.float64)
-    B, m, n = A.shape
+    B, n = c.shape
+    m = A.shape[-2]
     s = Solver(B, m, n, GENERAL, **opts)
     out = dict(status=np.empty(B, np.int32), obj=np.empty(B), iters=np.empty((B, 2), np.int32))
     out["x"] = np.empty((B, n)) if want_x else None
-    s.solve_host_into(A, b, c, out["status"], out["obj"], out["x"], out["iters"])
+    s.solve_host_into(A, b, c, out["status"], out["obj"], out["x"], out["iters"],
+                      shared_ab=shared)
     s.close()
     return out
 

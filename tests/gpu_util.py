@@ -19,9 +19,11 @@ def gpu_solve(A, b, c, *, path="device", want_x=True, **opts):
         At = torch.from_numpy(np.ascontiguousarray(A)).cuda()
         bt = torch.from_numpy(np.ascontiguousarray(b)).cuda()
         ct = torch.from_numpy(np.ascontiguousarray(c)).cuda()
-        B, m, n = At.shape
+        shared = At.dim() == 2  # one constraint system for the batch (LPB_SHARED_AB)
+        B, n = ct.shape
+        m = At.shape[-2]
         s = lpb.Solver(B, m, n, lpb.GENERAL, **opts)
-        s.solve_device(At, bt, ct, want_x=want_x, sync=True)
+        s.solve_device(At, bt, ct, want_x=want_x, sync=True, shared_ab=shared)
         r = {k: v.cpu().numpy() for k, v in s.device_results(want_x).items()}
         r["launch"] = s.launch_info()
         s.close()

@@ -64,3 +64,18 @@ def test_binding_struct_matches_header():
     body = re.search(r"typedef struct \{(.*?)\} lpb_options;", src, re.S).group(1)
     fields = re.findall(r"(\w+)\s*;", body)
     assert fields == [f[0] for f in lpb.Options._fields_]
+
+
+def test_binding_enums_match_header():
+    """Every LPB_* enum constant of include/lpb.h has the same value in the Python binding."""
+    from paper_1609_08114_b200 import lpb
+    src = re.sub(r"/\*.*?\*/", "", open(HDR).read(), flags=re.S)
+    consts = dict((k, int(v.rstrip("u"))) for k, v in re.findall(r"\b(LPB_[A-Z0-9_]+)\s*=\s*(-?\d+u?)", src))
+    assert len(consts) >= 18
+    for k, v in consts.items():
+        name = k[4:]
+        if hasattr(lpb, name):
+            assert getattr(lpb, name) == v, k
+    for k in ("DEVICE_PTRS", "SHARED_BOX", "NO_X", "ASYNC", "SHARED_AB", "GENERAL", "HYPERBOX",
+              "OPTIMAL", "UNBOUNDED", "INFEASIBLE", "ITER_LIMIT", "NUMERICAL"):
+        assert getattr(lpb, k) == consts["LPB_" + k], k

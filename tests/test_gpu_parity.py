@@ -89,6 +89,33 @@ def test_random_batches(klass, gen, m, n, B):
     compare(A, b, c, g, o)
 
 
+SHARED_CASES = [("G1", 5, 5, 3000), ("G1", 100, 100, 300), ("G2", 8, 8, 2000),
+                ("G2", 60, 60, 200), ("G2", 200, 200, 12)]
+
+
+@pytest.mark.parametrize("klass", CLASSES)
+@pytest.mark.parametrize("gen,m,n,B", SHARED_CASES,
+                         ids=[f"{g}-{m}x{n}" for g, m, n, _ in SHARED_CASES])
+def test_shared_constraints(klass, gen, m, n, B):
+    """NEXT-1: many objectives over one polytope, A and b read with stride 0
+    (LPB_SHARED_AB), device and host paths, against the oracle on the broadcast batch."""
+    A, b, c = lpgen.shared_polytope(B, m, n, 900 + m, gen)
+    k = int((b < 0).sum())
+    if klass == "R" and not _reg_fits(m, n, k):
+        pytest.skip("no register layout for this size")
+    if klass == "S" and (m > 8 or n > 8):
+        pytest.skip("the thread-per-LP class holds m, n <= 8")
+    if klass != "L" and m >= 200:
+        pytest.skip("200x200 two-phase needs the cluster class")
+    Ab = np.ascontiguousarray(np.broadcast_to(A, (B, m, n)))
+    bb = np.ascontiguousarray(np.broadcast_to(b, (B, m)))
+    o = oracle.solve(Ab, bb, c)
+    g = gpu_solve(A, b, c, kernel_class=klass)
+    compare(Ab, bb, c, g, o)
+    gh = gpu_solve(A, b, c, path="host", kernel_class=klass, n_chunks=3)
+    compare(Ab, bb, c, gh, o)
+
+
 @pytest.mark.parametrize("K", [1, 3])
 def test_bland_coverage_degenerate(K):
     """G-deg with small Bland thresholds: exercises Bland mode and artificial drive-outs."""

@@ -67,3 +67,15 @@ def test_shards_equal_slices_of_the_full_batch():
                 assert np.array_equal(f[lo:hi], p)
     lo_b, hi_b, d = lpgen.make_config_shard("cfg4", 5000, 100, 300)
     assert np.array_equal(d, lpgen.hyperbox(5000, 5, 4)[2][100:300])
+
+
+def test_shared_polytope_layout_and_shards():
+    A, b, c = lpgen.shared_polytope(50, 12, 9, 4)
+    assert A.shape == (12, 9) and b.shape == (12,) and c.shape == (50, 9)
+    A1, b1, _ = lpgen.signed_bounded(1, 12, 9, 4)
+    assert np.array_equal(A, A1[0]) and np.array_equal(b, b1[0])
+    A2, b2, c2 = lpgen.make_config_shard("cfg2s", 200, 40, 90)
+    Af, bf, cf = lpgen.make_config("cfg2s", 200)
+    assert np.array_equal(A2, Af) and np.array_equal(b2, bf) and np.array_equal(c2, cf[40:90])
+    _, b3, _ = lpgen.shared_polytope(3, 40, 40, 3, "G2")
+    assert (b3 < 0).sum() == 10  # ceil(m/4) covering rows
