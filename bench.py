@@ -36,8 +36,10 @@ UNIT = "LPs/s"
 # Paper numbers for the exact workload (GeForce GTX 670): hyperbox only.
 PAPER_LPS = {"cfg4": 4001000 / 0.406, "cfg5": 6003000 / 2.388}
 # oracle sample per reference step (bounded CPU work)
-REF_SAMPLE = {"cfg1": 1000, "cfg2": 240, "cfg3": 8, "cfg4": 4001000, "cfg5": 1000000}
-CPU_SAMPLE = {"cfg1": 1000, "cfg2": 1200, "cfg3": 24, "cfg4": 4001000, "cfg5": 6003000}
+REF_SAMPLE = {"cfg1": 1000, "cfg2": 240, "cfg3": 8, "cfg4": 4001000, "cfg5": 1000000,
+              "cfg2s": 240, "cfg3s": 8}
+CPU_SAMPLE = {"cfg1": 1000, "cfg2": 1200, "cfg3": 24, "cfg4": 4001000, "cfg5": 6003000,
+              "cfg2s": 1200, "cfg3s": 24}
 L2_BYTES = 126 * 1024 * 1024
 
 
@@ -47,7 +49,21 @@ def describe(name):
         return (f"{name}: type-3 hyperbox, {c['B']} LPs of n={c['n']} (shared box, G3 seed "
                 f"{c['seed']})")
     t = "type-1 (b>=0)" if c["gen"] == "G1" else "type-2 (two-phase)"
+    if c.get("shared"):
+        return (f"{name}: {t}, {c['B']} objectives over one {c['m']}x{c['n']} polytope "
+                f"({c['gen']} seed {c['seed']}, shared A/b)")
     return f"{name}: {t}, {c['B']} LPs of {c['m']}x{c['n']} ({c['gen']} seed {c['seed']})"
+
+
+def general_sample(name, n_lp):
+    """First n_lp LPs of a general config as a full (B, m, n) batch (shared A/b broadcast)."""
+    cfg = lpgen.CONFIGS[name]
+    A, b, c = lpgen.make_config_shard(name, cfg["B"], 0, min(n_lp, cfg["B"]))
+    if A.ndim == 2:
+        B = c.shape[0]
+        A = np.ascontiguousarray(np.broadcast_to(A, (B,) + A.shape))
+        b = np.ascontiguousarray(np.broadcast_to(b, (B,) + b.shape))
+    return A, b, c
 
 
 def peaks():
@@ -131,7 +147,7 @@ def cpu_baseline(name, sample_n):
         dt = time.perf_counter() - t
         n_lp = dirs.shape[0]
     else:
-        A, b, c = lpgen.make_config_shard(name, cfg["B"], 0, min(sample_n, cfg["B"]))
+        A, b, c = general_sample(name, sample_n)
         t = time.perf_counter()
         r = oracle.solve(A, b, c)
         dt = time.perf_counter() - t
@@ -154,7 +170,7 @@ def run_reference(args):
         step = lambda: oracle.hyperbox(lo, hi, dirs)  # noqa: E731
         n_lp = dirs.shape[0]
     else:
-        A, b, c = lpgen.make_config_shard(name, cfg["B"], 0, min(n, cfg["B"]))
+        A, b, c = general_sample(name, n)
         step = lambda: oracle.solve(A, b, c)  # noqa: E731
         n_lp = A.shape[0]
     for _ in range(args.warmup):
@@ -210,6 +226,7 @@ def main():
     B = args.batch or cfg["B"]
     lo, hi = rank * B, (rank + 1) * B
     hyper = cfg["kind"] == "hyperbox"
+    sab = bool(cfg.get("shared"))
     if hyper:
         n = cfg["n"]
         lo_b, hi_b, dirs = lpgen.make_config_shard(name, B * world, lo, hi)
@@ -234,7 +251,7 @@ def main():
         flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
 
     def step():
-        solver.solve_device(d_A, d_b, d_c, shared_box=hyper)
+        solver.solve_device(d_A, d_b, d_c, shared_box=hyper, shared_ab=sab)
 
     for _ in range(args.warmup):
         step()
@@ -277,7 +294,7 @@ def main():
         iters_mean = None
     else:
         iters = res["iters"].cpu().numpy()
-        k = (host_in[1] < 0).sum(axis=1)
+        k = (np.broadcast_to(host_in[1], (B, m)) < 0).sum(axis=1)
         flops = algorithmic_flops(iters, k, m, n)
         achieved = flops / (kmean / 1e3) / 1e12
         roof = {"bound": "alu", "achieved": achieved, "peak": p["fp64_tflops"],
@@ -301,10 +318,12 @@ def main():
         out_x = lpb.pinned_empty((B, n))
         out_it = lpb.pinned_empty((B, 2), np.int32) if not hyper else None
         hs = lpb.Solver(B, m, n, kind)
-        hs.solve_host_into(*pin, out_st, out_obj, out_x, out_it, shared_box=hyper)  # warm
+        hs.solve_host_into(*pin, out_st, out_obj, out_x, out_it, shared_box=hyper,
+                           shared_ab=sab)  # warm
         e_ms = []
         for _ in range(args.e2e_steps):
-            hs.solve_host_into(*pin, out_st, out_obj, out_x, out_it, shared_box=hyper)
+            hs.solve_host_into(*pin, out_st, out_obj, out_x, out_it, shared_box=hyper,
+                               shared_ab=sab)
             e_ms.append(hs.timing()[1])
             launches_e2e = hs.launch_info()[0]
         e_tot = lpdist.max_over_ranks(float(sum(e_ms)), device=torch.device("cuda", local))
@@ -324,7 +343,7 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_ms / args.steps,
             "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": (value / world / PAPER_LPS[name]) if name in PAPER_LPS else None,
+            "vs_baseline": (value / PAPER_LPS[name]) if name in PAPER_LPS else None,
             "dtype": "f64", "data": "synthetic (seeded lpgen generators, DESIGN.md)",
             "config": {"workload": describe(name), "batch_per_gpu": B, "m": m, "n": n,
                        "kind": "hyperbox" if hyper else "general",

@@ -9,6 +9,8 @@ for cf in cfg2 cfg1 cfg4 cfg5; do
   timeout 900 python bench.py --config $cf > $OUT/bench_$cf.json 2> $OUT/bench_$cf.err
 done
 timeout 900 python bench.py --config cfg3 --steps 2 --warmup 1 --e2e-steps 1 > $OUT/bench_cfg3.json 2> $OUT/bench_cfg3.err
+timeout 900 python bench.py --config cfg2s > $OUT/bench_cfg2s.json 2> $OUT/bench_cfg2s.err
+timeout 900 python bench.py --config cfg3s --steps 2 --warmup 1 --e2e-steps 1 > $OUT/bench_cfg3s.json 2> $OUT/bench_cfg3s.err
 timeout 300 python bench.py --impl reference --config cfg2 --steps 3 --warmup 1 > $OUT/ref_cfg2.json 2>&1
 # launch lists (cold-cache, serialised: compare shares, not absolutes)
 for cf in cfg2 cfg5 cfg1; do
