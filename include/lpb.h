@@ -96,7 +96,8 @@ typedef struct {
                           (the paper's stream count)                            */
   int32_t kernel_class;/* 0 auto; 1 S (thread/LP, m,n <= 8), 2 M (block/LP, SMEM tableau),
                           3 L (2/4-CTA cluster/LP, DSMEM), 4 R (block or warp/LP, register-
-                          resident tableau); for tests / benches                           */
+                          resident tableau tiles), 6 T (block/LP, one register-resident row
+                          per thread); for tests / benches                                 */
   int32_t grid_ctas;   /* 0 auto; persistent grid size override (scheduling-invariance tests) */
 } lpb_options;
 

@@ -206,6 +206,7 @@ static int choose_class(const lpb_ctx* c, int kmax, int* cl) {
   const int forced = c->opt.kernel_class;
   *cl = 1;
   if (forced == CLASS_R) return reg_fits(m, n, kmax) ? CLASS_R : -1;
+  if (forced == CLASS_T) return row_fits(m, n, kmax) ? CLASS_T : -1;
   if (forced == CLASS_M) return block_fits(1, m, n, kmax) ? CLASS_M : -1;
   if (forced == CLASS_L) {
     for (int q : {2, 4})
@@ -299,6 +300,8 @@ static int run_general(lpb_ctx* c, cudaStream_t s, int64_t lp0, int64_t cnt, con
   if (timed) LPB_CUDA(c, cudaEventRecord(c->kev0, s));
   if (klass == CLASS_R) {
     LPB_CUDA(c, launch_simplex_reg(a, c->opt.grid_ctas, s, &ctas));
+  } else if (klass == CLASS_T) {
+    LPB_CUDA(c, launch_simplex_row(a, c->opt.grid_ctas, s, &ctas));
   } else {
     LPB_CUDA(c, launch_simplex_block(cl, a, c->opt.grid_ctas, s, &ctas));
   }

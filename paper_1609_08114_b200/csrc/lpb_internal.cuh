@@ -13,7 +13,7 @@ enum : int32_t { ST_OPTIMAL = 0, ST_UNBOUNDED = 1, ST_INFEASIBLE = 2, ST_ITER_LI
 
 // Size classes (lpb_options.kernel_class / lpb_last_launch_info).
 enum : int32_t { CLASS_AUTO = 0, CLASS_S = 1, CLASS_M = 2, CLASS_L = 3, CLASS_R = 4,
-                 CLASS_H = 5 };
+                 CLASS_H = 5, CLASS_T = 6 };
 
 struct SimplexArgs {
   int64_t batch;
@@ -55,6 +55,11 @@ cudaError_t launch_simplex_block(int cl, const SimplexArgs& a, int grid_override
 // ---- S class: one LP per thread (tiny LPs), tableau in a thread-private SMEM slice ----
 bool thread_fits(int m, int n);
 cudaError_t launch_simplex_thread(const SimplexArgs& a, cudaStream_t s);
+
+// ---- T class: one LP per CTA, one tableau row per thread, rows resident in registers ----
+bool row_fits(int m, int n, int kmax);
+cudaError_t launch_simplex_row(const SimplexArgs& a, int grid_override, cudaStream_t s,
+                               int* ctas_out);
 
 // ---- R class: one LP per CTA (one warp for small LPs), tableau resident in registers ----
 bool reg_fits(int m, int n, int kmax);

@@ -16,7 +16,21 @@ from gpu_util import compare, gpu_solve
 pytestmark = pytest.mark.gpu
 
 GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "lp_fixtures.json")))
-CLASSES = ["S", "R", "M", "L"]
+CLASSES = ["S", "R", "M", "L", "T"]
+
+
+def _row_fits(m, n, k):
+    # mirrors the instantiated row-per-thread layouts in csrc/simplex_row.cu
+    return m <= 128 and n + k <= 100
+
+
+def _skip_class(klass, m, n, k):
+    if klass == "R" and not _reg_fits(m, n, k):
+        pytest.skip("no register layout for this size")
+    if klass == "T" and not _row_fits(m, n, k):
+        pytest.skip("no row-per-thread layout for this size")
+    if klass == "S" and (m > 8 or n > 8):
+        pytest.skip("the thread-per-LP class holds m, n <= 8")
 
 
 def _reg_fits(m, n, k):
@@ -80,10 +94,7 @@ def _gen(gen, B, m, n, seed):
 @pytest.mark.parametrize("gen,m,n,B", CASES, ids=[f"{g}-{m}x{n}" for g, m, n, _ in CASES])
 def test_random_batches(klass, gen, m, n, B):
     A, b, c = _gen(gen, B, m, n, 1000 + 7 * m + n)
-    if klass == "R" and not _reg_fits(m, n, int((b < 0).sum(axis=1).max())):
-        pytest.skip("no register layout for this size")
-    if klass == "S" and (m > 8 or n > 8):
-        pytest.skip("the thread-per-LP class holds m, n <= 8")
+    _skip_class(klass, m, n, int((b < 0).sum(axis=1).max()))
     o = oracle.solve(A, b, c)
     g = gpu_solve(A, b, c, kernel_class=klass)
     compare(A, b, c, g, o)
@@ -101,10 +112,7 @@ def test_shared_constraints(klass, gen, m, n, B):
     (LPB_SHARED_AB), device and host paths, against the oracle on the broadcast batch."""
     A, b, c = lpgen.shared_polytope(B, m, n, 900 + m, gen)
     k = int((b < 0).sum())
-    if klass == "R" and not _reg_fits(m, n, k):
-        pytest.skip("no register layout for this size")
-    if klass == "S" and (m > 8 or n > 8):
-        pytest.skip("the thread-per-LP class holds m, n <= 8")
+    _skip_class(klass, m, n, k)
     if klass != "L" and m >= 200:
         pytest.skip("200x200 two-phase needs the cluster class")
     Ab = np.ascontiguousarray(np.broadcast_to(A, (B, m, n)))
