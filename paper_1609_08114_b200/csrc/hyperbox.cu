@@ -127,14 +127,44 @@ __global__ void __launch_bounds__(HB_NT) hyperbox_kernel(HyperboxArgs a) {
 // Shared-box fast path: tiles of LPT*256 directions stream HBM -> SMEM with bulk async copies
 // (cp.async.bulk, one per tile) through a STAGES-deep ring, so several tiles per SM are in
 // flight while the current one is evaluated (HBM latency x bandwidth needs ~44 KB in flight
-// per SM).  The tile stays dense in SMEM; x = h is produced in the coalesced store pass
-// directly from the sign of l (no write-back).
+// per SM).  Each thread evaluates its LPs from its SMEM row (128-bit reads when n is even)
+// and writes h back in place; x then leaves the SM as ONE bulk async store per tile
+// (cp.async.bulk shared -> global, TMA engine), so the SM issues no per-element global
+// stores.  The ragged tail (< one tile) is evaluated by the next CTA in round-robin order
+// straight from global memory, inside the same launch.
+__device__ __forceinline__ double hb_eval_row(double* row, int n, const double* blo,
+                                              const double* bhi, bool empty, bool wb) {
+  // acc = fma(l_i, h_i, acc) over i = 0..n-1 from 0 (the oracle's order); h written back
+  const double nan = __longlong_as_double(0x7ff8000000000000ll);
+  double acc = 0.0;
+  if ((n & 1) == 0) {
+    double2* r2 = reinterpret_cast<double2*>(row);
+    for (int i2 = 0; i2 < (n >> 1); ++i2) {
+      double2 v = r2[i2];
+      const double h0 = (v.x < 0.0) ? blo[2 * i2] : bhi[2 * i2];
+      acc = __fma_rn(v.x, h0, acc);
+      const double h1 = (v.y < 0.0) ? blo[2 * i2 + 1] : bhi[2 * i2 + 1];
+      acc = __fma_rn(v.y, h1, acc);
+      if (wb) r2[i2] = make_double2(empty ? nan : h0, empty ? nan : h1);
+    }
+  } else {
+    for (int i = 0; i < n; ++i) {
+      const double li = row[i];
+      const double h = (li < 0.0) ? blo[i] : bhi[i];
+      acc = __fma_rn(li, h, acc);
+      if (wb) row[i] = empty ? nan : h;
+    }
+  }
+  return acc;
+}
+
 __global__ void __launch_bounds__(HB_NT, 1)
-hyperbox_tma_kernel(HyperboxArgs a, int lpt, int stages) {
+hyperbox_tma_kernel(HyperboxArgs a, int lpt, int stages, int bulk_x) {
   extern __shared__ __align__(16) unsigned char hraw[];
   const int n = a.n, tid = threadIdx.x;
   const int tile_lps = lpt * HB_NT;
   const size_t tile_elems = (size_t)tile_lps * n;
+  const uint32_t tile_bytes = (uint32_t)(tile_elems * 8);
   uint64_t* mbar = reinterpret_cast<uint64_t*>(hraw);                 // [stages]
   double* blo = reinterpret_cast<double*>(hraw + 16 * 8);            // [n]
   double* bhi = blo + n;                                              // [n]
@@ -146,55 +176,87 @@ hyperbox_tma_kernel(HyperboxArgs a, int lpt, int stages) {
   }
   bool empty = false;
   for (int i = 0; i < n; ++i) empty |= (-a.box[n + i] > a.box[i]);
+  const double ninf = __longlong_as_double(0xfff0000000000000ll);
   const int64_t nfull = a.batch / tile_lps;  // full tiles go through the TMA ring
+  const int64_t G = gridDim.x;
   if (tid == 0) {
     for (int st = 0; st < stages; ++st) mbar_init(&mbar[st], 1);
     for (int st = 0; st < stages; ++st) {
-      const int64_t t = blockIdx.x + (int64_t)st * gridDim.x;
-      if (t < nfull)
-        bulk_load(buf + st * tile_elems, a.l + t * tile_elems, (uint32_t)(tile_elems * 8), &mbar[st]);
+      const int64_t t = blockIdx.x + (int64_t)st * G;
+      if (t < nfull) bulk_load(buf + st * tile_elems, a.l + t * tile_elems, tile_bytes, &mbar[st]);
     }
   }
   __syncthreads();
-  const int r0 = tid / n, j0 = tid - r0 * n;
-  const int dq = HB_NT / n, dr = HB_NT - dq * n;
+  const bool wx = a.x != nullptr;
+  const int j0 = tid % n, dr = HB_NT % n;
   int k = 0;
-  for (int64_t t = blockIdx.x; t < nfull; t += gridDim.x, ++k) {
+  for (int64_t t = blockIdx.x; t < nfull; t += G, ++k) {
     const int st = k % stages;
     mbar_wait(&mbar[st], (uint32_t)((k / stages) & 1));
-    const double* tb = buf + st * tile_elems;
+    double* tb = buf + st * tile_elems;
     const int64_t lp0 = t * tile_lps;
     for (int q = 0; q < lpt; ++q) {
       const int r = q * HB_NT + tid;
-      const double* row = tb + (size_t)r * n;
-      double acc = 0.0;
-      for (int i = 0; i < n; ++i) {
-        const double li = row[i];
-        acc = __fma_rn(li, (li < 0.0) ? blo[i] : bhi[i], acc);
-      }
+      const double acc = hb_eval_row(tb + (size_t)r * n, n, blo, bhi, empty, wx && bulk_x);
       __stcs(a.status + lp0 + r, empty ? ST_INFEASIBLE : ST_OPTIMAL);
-      __stcs(a.obj + lp0 + r, empty ? __longlong_as_double(0xfff0000000000000ll) : acc);
+      __stcs(a.obj + lp0 + r, empty ? ninf : acc);
     }
-    if (a.x) {
-      double* __restrict__ dst = a.x + lp0 * n;
-      const int total = tile_lps * n;
-      int j = j0;
-      for (int f = tid; f < total; f += HB_NT) {
-        const double li = tb[f];
-        __stcs(dst + f, empty ? __longlong_as_double(0x7ff8000000000000ll)
-                              : ((li < 0.0) ? blo[j] : bhi[j]));
-        j += dr;
-        if (j >= n) j -= n;
+    if (wx && bulk_x) {
+      fence_proxy_async_smem();  // the in-place h writes, before the async-proxy store reads
+      __syncthreads();
+      if (tid == 0) {
+        bulk_store(a.x + lp0 * n, tb, tile_bytes);
+        bulk_commit();
+        // the store of the previous tile has finished reading its stage: refill that stage
+        bulk_wait_read<1>();
+        if (k > 0) {
+          const int sp = (k - 1) % stages;
+          const int64_t tn = t - G + (int64_t)stages * G;
+          if (tn < nfull)
+            bulk_load(buf + sp * tile_elems, a.l + tn * tile_elems, tile_bytes, &mbar[sp]);
+        }
       }
-    }
-    __syncthreads();  // every read of this stage is done: refill it
-    if (tid == 0) {
-      const int64_t tn = t + (int64_t)stages * gridDim.x;
-      if (tn < nfull)
-        bulk_load(buf + st * tile_elems, a.l + tn * tile_elems, (uint32_t)(tile_elems * 8), &mbar[st]);
+    } else {
+      if (wx) {  // coalesced per-thread stores of x from the sign of l
+        double* __restrict__ dst = a.x + lp0 * n;
+        const int total = tile_lps * n;
+        int j = j0;
+        for (int f = tid; f < total; f += HB_NT) {
+          const double li = tb[f];
+          __stcs(dst + f, empty ? __longlong_as_double(0x7ff8000000000000ll)
+                                : ((li < 0.0) ? blo[j] : bhi[j]));
+          j += dr;
+          if (j >= n) j -= n;
+        }
+      }
+      __syncthreads();  // every read of this stage is done: refill it
+      if (tid == 0) {
+        const int64_t tn = t + (int64_t)stages * G;
+        if (tn < nfull) bulk_load(tb, a.l + tn * tile_elems, tile_bytes, &mbar[st]);
+      }
     }
   }
-  (void)r0; (void)dq;
+  if (wx && bulk_x && tid == 0) {
+    // the last tile's stage was never refilled; make every store complete before exit
+    bulk_wait_all();
+  }
+  // ragged tail (< one tile): the next CTA in round-robin order, straight from global memory
+  const int64_t done = nfull * tile_lps;
+  if (done < a.batch && blockIdx.x == nfull % G) {
+    const double nan = __longlong_as_double(0x7ff8000000000000ll);
+    for (int64_t lp = done + tid; lp < a.batch; lp += HB_NT) {
+      const double* li = a.l + lp * n;
+      double acc = 0.0;
+      for (int i = 0; i < n; ++i) {
+        const double l_i = __ldg(li + i);
+        const double h = (l_i < 0.0) ? blo[i] : bhi[i];
+        acc = __fma_rn(l_i, h, acc);
+        if (wx) a.x[lp * n + i] = empty ? nan : h;
+      }
+      a.status[lp] = empty ? ST_INFEASIBLE : ST_OPTIMAL;
+      a.obj[lp] = empty ? ninf : acc;
+    }
+  }
 }
 
 }  // namespace
@@ -238,6 +300,10 @@ cudaError_t launch_hyperbox(const HyperboxArgs& a, cudaStream_t s) {
   const int64_t tile_lps = (int64_t)lpt * HB_NT;
   const int64_t nfull = tma ? a.batch / tile_lps : 0;
   if (nfull > 0) {
+    // x leaves by bulk store when its tiles are 16-byte aligned (always for cudaMalloc'd x
+    // and tile-aligned chunks); otherwise by coalesced per-thread stores
+    const int bulk_x = (a.x != nullptr && (reinterpret_cast<uintptr_t>(a.x) & 15) == 0 &&
+                        getenv("LPB_NO_BULK_X") == nullptr) ? 1 : 0;
     const size_t smem = 16 * 8 + 16 * (size_t)((2 * n + 2 + 1) / 2) + 16 + stages * tile_bytes;
     static size_t cached_smem = (size_t)-1;
     static int cached_dev = -1;
@@ -252,9 +318,8 @@ cudaError_t launch_hyperbox(const HyperboxArgs& a, cudaStream_t s) {
     }
     int64_t grid = device_sm_count();
     if (grid > nfull) grid = nfull;
-    hyperbox_tma_kernel<<<(unsigned)grid, HB_NT, smem, s>>>(a, lpt, stages);
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
+    hyperbox_tma_kernel<<<(unsigned)grid, HB_NT, smem, s>>>(a, lpt, stages, bulk_x);
+    return cudaGetLastError();  // the ragged tail is handled inside the same launch
   }
   const int64_t done = nfull * tile_lps;
   if (done < a.batch) {

@@ -231,3 +231,32 @@ def test_hyperbox_per_lp_box_and_empty():
     assert np.array_equal(r["x"], o["x"], equal_nan=True)
     assert np.any(o["status"] == oracle.INFEASIBLE)
     s.close()
+
+
+@pytest.mark.parametrize("n,B", [(4, 70001), (5, 4099), (28, 9000), (3, 100000)])
+def test_hyperbox_no_x_empty_shared_box_and_misaligned_chunks(n, B):
+    """Shared-box kernel paths: NO_X (no x stores), an empty shared box (all INFEASIBLE, x NaN),
+    and host-pipeline chunks whose x slices are not 16-byte aligned (per-thread store path)."""
+    import torch
+
+    from paper_1609_08114_b200 import lpb
+    lo, hi, dirs = lpgen.hyperbox(B, n, 70 + n)
+    o = oracle.hyperbox(lo, hi, dirs)
+    s = lpb.Solver(B, 2 * n, n, lpb.HYPERBOX)
+    box = torch.from_numpy(np.concatenate([hi, -lo])).cuda()
+    s.solve_device(None, box, torch.from_numpy(dirs).cuda(), shared_box=True, want_x=False,
+                   sync=True)
+    r = s.device_results(want_x=False)
+    assert np.array_equal(r["obj"].cpu().numpy(), o["obj"])
+    assert np.array_equal(r["status"].cpu().numpy(), o["status"])
+    s.close()
+    hi_e = hi.copy()
+    hi_e[n // 2] = lo[n // 2] - 0.5  # empty box
+    oe = oracle.hyperbox(lo, hi_e, dirs)
+    ge = lpb.hyperbox(lo, hi_e, torch.from_numpy(dirs).cuda())
+    assert np.all(oe["status"] == oracle.INFEASIBLE)
+    assert np.array_equal(ge["status"].cpu().numpy(), oe["status"])
+    assert np.array_equal(ge["obj"].cpu().numpy(), oe["obj"])
+    assert np.array_equal(ge["x"].cpu().numpy(), oe["x"], equal_nan=True)
+    gh = lpb.hyperbox(lo, hi, dirs, n_chunks=7)  # odd chunk boundaries
+    assert np.array_equal(gh["obj"], o["obj"]) and np.array_equal(gh["x"], o["x"])
