@@ -39,6 +39,8 @@ typedef struct {
   double eps_phase1;  /* phase-I zero test (R8): w* > eps_phase1*max(1,|b|_inf) infeasible */
   int max_iter;       /* <= 0 -> 50(n+m)                                     */
   int bland_after;    /* 0 -> n+m ; < 0 -> never (pure Dantzig) (R6)                       */
+  int pivot_rule;     /* 0 LPC, 1 RPC (reading R15)             */
+  uint64_t rpc_seed;  /* RPC: seed of the counter-based choice (R15)                          */
 } oracle_opts;
 
 /* One LP's full tableau.  Rows 0..m-1 constraints, row m the phase-II (original objective)
@@ -138,6 +140,33 @@ static int entering(const tableau* t, int row, double eps, int bland) {
   return e;
 }
 
+/* SplitMix64 finaliser (R15): z += golden gamma; two xor-shift-multiply rounds; xor-shift. */
+static uint64_t mix64(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+/* Step 1 under RPC ("we choose a random index having a positive coefficient
+ * from the last row"; reading R15): every column j with reduced cost > eps_enter (artificials
+ * excluded, R7) draws the score u_j = mix64(mix64(mix64(seed ^ mix64(k)) ^ t) ^ j) >> 11 --
+ * k = the LP's index in the batch, t = pivots done so far -- and the largest score enters
+ * (ties to the lowest j).  Each candidate is equally likely to win. */
+static int entering_rpc(const tableau* t, int row, double eps, uint64_t seed, int64_t k,
+                        int pivots) {
+  const uint64_t base = mix64(mix64(seed ^ mix64((uint64_t)k)) ^ (uint64_t)pivots);
+  int e = -1;
+  uint64_t best = 0;
+  for (int j = 0; j < t->n + t->m; ++j) {
+    const double d = TT(t, row, j);
+    if (!(d > eps)) continue;
+    const uint64_t u = mix64(base ^ (uint64_t)j) >> 11;
+    if (e < 0 || u > best) { e = j; best = u; }
+  }
+  return e;
+}
+
 /* Step 2 ("minimum positive ratio ... a large positive number in place of
  * ratios that are negative or undefined"; readings R1, R2): rows with a_ie > eps_piv give
  * r_i = b_i / a_ie (IEEE division); other rows are excluded (the +inf sentinel); argmin r,
@@ -190,8 +219,8 @@ static void certs(const tableau* t, int status, int e_unb, double* y, double* ra
  * otherwise; R10); x[n] (basic values read from the RHS column, NaN when not OPTIMAL);
  * iters[2] = (phase-I pivots incl. drive-outs, phase-II pivots).  y[m], ray[n] optional. */
 int oracle_solve_lp(int m, int n, const double* A, const double* b, const double* c,
-                    const oracle_opts* o, int* status, double* obj, double* x, int* iters,
-                    double* y, double* ray, double* xb) {
+                    const oracle_opts* o, int64_t lp_index, int* status, double* obj,
+                    double* x, int* iters, double* y, double* ray, double* xb) {
   tableau tb;
   tableau* t = &tb;
   if (build(t, m, n, A, b, c) != 0) return -1;
@@ -204,7 +233,9 @@ int oracle_solve_lp(int m, int n, const double* A, const double* b, const double
     const int row = (phase == 1) ? m + 1 : m;
     const int nrow = (phase == 1) ? m + 2 : m + 1;
     const int bland = (K > 0 && stall >= K);
-    const int e = entering(t, row, o->eps_enter, bland);
+    const int e = (o->pivot_rule == 1 && !bland)
+                      ? entering_rpc(t, row, o->eps_enter, o->rpc_seed, lp_index, it[0] + it[1])
+                      : entering(t, row, o->eps_enter, bland);
     if (e < 0) {
       if (phase == 2) { st = OR_OPTIMAL; break; }
       /* Phase switch ("checked if the optimal solution ... is 0"; R8, R9). */
@@ -304,7 +335,7 @@ static void* batch_worker(void* arg) {
     if (k >= j->batch) break;
     const size_t mn = (size_t)j->m * (size_t)j->n;
     oracle_solve_lp(j->m, j->n, j->A + (size_t)k * mn, j->b + (size_t)k * j->m,
-                    j->c + (size_t)k * j->n, j->o, j->status + k, j->obj + k,
+                    j->c + (size_t)k * j->n, j->o, k, j->status + k, j->obj + k,
                     j->x + (size_t)k * j->n, j->iters + 2 * k,
                     j->y ? j->y + (size_t)k * j->m : NULL,
                     j->ray ? j->ray + (size_t)k * j->n : NULL,
