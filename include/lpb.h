@@ -99,7 +99,28 @@ typedef struct {
                           resident tableau tiles), 6 T (block/LP, one register-resident row
                           per thread); for tests / benches                                 */
   int32_t grid_ctas;   /* 0 auto; persistent grid size override (scheduling-invariance tests) */
+  int32_t cluster_ctas;/* L class cluster size: 0 auto (the smallest of 2/4/8/16 CTAs whose
+                          distributed SMEM holds the tableau); 2/4/8/16 forces that size when
+                          the tableau fits it (tests / benches); 16 is a non-portable size    */
+  int32_t pivot_rule;  /* Step 1 entering rule: LPB_RULE_LPC (0, default)
+                          = Largest Positive Coefficient (Dantzig); LPB_RULE_RPC (1) = Random
+                          Positive Coefficient.  Bland's rule still takes over after
+                          bland_after degenerate pivots under either rule.                   */
+  uint64_t rpc_seed;   /* RPC: seed of the counter-based choice (see LPB_RULE_RPC)            */
 } lpb_options;
+
+/* Entering rules (lpb_options.pivot_rule).
+ * LPB_RULE_RPC picks uniformly among the Step-1 candidates (reduced cost > eps_enter, never a
+ * left artificial) without a stored random state: with mix64 the SplitMix64 finaliser
+ * (z += 0x9E3779B97F4A7C15; z = (z^(z>>30))*0xBF58476D1CE4E5B9; z = (z^(z>>27))*
+ * 0x94D049BB133111EB; z ^= z>>31), candidate variable j (0..n-1 structural, n+i slack of row
+ * i) of LP k (its 0-based index in the lpb_solve_batch call) at pivot t (= phase-I + phase-II
+ * pivots done so far) scores  u = mix64(mix64(mix64(rpc_seed ^ mix64(k)) ^ t) ^ j) >> 11
+ * (an integer < 2^53), and the candidate with the largest u enters (ties: lowest j).  Every
+ * candidate is equally likely to win, the choice depends only on (seed, k, t, j) -- not on
+ * the storage order of a size class -- and identical seeds give identical pivot sequences.
+ * An undefined rule value is LPB_EINVAL at lpb_create. */
+enum { LPB_RULE_LPC = 0, LPB_RULE_RPC = 1 };
 
 /* Fill *o with the defaults above.  Returns LPB_EINVAL if o is NULL. */
 int lpb_default_options(lpb_options* o);
@@ -152,8 +173,13 @@ int lpb_last_timing(lpb_ctx* c, double* solve_ms, double* e2e_ms);
 int lpb_last_kernel_timing(lpb_ctx* c, double* kernel_ms);
 
 /* Number of kernel launches the last solve issued (for the bench's gpu_launches count),
- * and the size class it dispatched to (1 S, 2 M, 3 L, 4 R, 5 H). */
+ * and the size class it dispatched to (1 S, 2 M, 3 L, 4 R, 5 H, 6 T). */
 int lpb_last_launch_info(lpb_ctx* c, int32_t* launches, int32_t* kernel_class);
+
+/* Launch shape of the last solve's dominant kernel: CTAs per LP (the L class's cluster size
+ * 2/4/8/16; 1 for one LP per CTA; 0 for the per-thread S and H classes) and the grid size
+ * in CTAs (of the last chunk's launch).  Either pointer may be NULL.  Errors: LPB_EINVAL. */
+int lpb_last_launch_shape(lpb_ctx* c, int32_t* cluster_ctas, int32_t* grid_ctas);
 
 /* Release every resource of the context.  NULL is accepted. */
 int lpb_destroy(lpb_ctx* c);

@@ -62,7 +62,7 @@ struct lpb_ctx {
   cudaEvent_t kev0 = nullptr, kev1 = nullptr;  // around the dominant (solve) kernel
   bool kev_valid = false;
   bool solved = false, last_nox = false, host_path = false;
-  int last_launches = 0, last_class = 0;
+  int last_launches = 0, last_class = 0, last_cluster = 0, last_grid = 0;
   long long* prof = nullptr;  // diagnostics: per-CTA phase counters (lpb_set_profile_buffer)
   char err[256] = {0};
 };
@@ -92,6 +92,9 @@ extern "C" int lpb_default_options(lpb_options* o) {
   o->n_chunks = 0;
   o->kernel_class = 0;
   o->grid_ctas = 0;
+  o->cluster_ctas = 0;
+  o->pivot_rule = LPB_RULE_LPC;
+  o->rpc_seed = 0;
   return LPB_OK;
 }
 
@@ -112,7 +115,8 @@ extern "C" const char* lpb_last_error(lpb_ctx* c) { return c ? c->err : ""; }
 // Size-class capacity check at the best case (no artificial rows).
 static bool general_fits_any(int m, int n) {
   return thread_fits(m, n) || reg_fits(m, n, 0) || block_fits(1, m, n, 0) ||
-         block_fits(2, m, n, 0) || block_fits(4, m, n, 0);
+         block_fits(2, m, n, 0) || block_fits(4, m, n, 0) || block_fits(8, m, n, 0) ||
+         block_fits(16, m, n, 0);
 }
 
 extern "C" int lpb_create(lpb_ctx** out, int64_t batch, int32_t m, int32_t n, int32_t kind,
@@ -129,6 +133,10 @@ extern "C" int lpb_create(lpb_ctx** out, int64_t batch, int32_t m, int32_t n, in
     opt = *o;
   }
   if (!(opt.eps_enter >= 0) || !(opt.eps_piv >= 0) || !(opt.eps_phase1 >= 0)) return LPB_EINVAL;
+  if (opt.pivot_rule != LPB_RULE_LPC && opt.pivot_rule != LPB_RULE_RPC) return LPB_EINVAL;
+  if (opt.cluster_ctas != 0 && opt.cluster_ctas != 2 && opt.cluster_ctas != 4 &&
+      opt.cluster_ctas != 8 && opt.cluster_ctas != 16)
+    return LPB_EINVAL;
   if (kind == LPB_GENERAL && !general_fits_any(m, n)) return LPB_ETOOBIG;
   if (kind == LPB_HYPERBOX && (size_t)(n | 1) * 256 * 8 > 200 * 1024) return LPB_ETOOBIG;
 
@@ -208,14 +216,20 @@ static int choose_class(const lpb_ctx* c, int kmax, int* cl) {
   if (forced == CLASS_R) return reg_fits(m, n, kmax) ? CLASS_R : -1;
   if (forced == CLASS_T) return row_fits(m, n, kmax) ? CLASS_T : -1;
   if (forced == CLASS_M) return block_fits(1, m, n, kmax) ? CLASS_M : -1;
+  const int fcl = c->opt.cluster_ctas;
+  if (fcl > 0 && (forced == CLASS_L || forced == CLASS_AUTO)) {
+    if (!block_fits(fcl, m, n, kmax)) return -1;
+    *cl = fcl;
+    return CLASS_L;
+  }
   if (forced == CLASS_L) {
-    for (int q : {2, 4})
+    for (int q : {2, 4, 8, 16})
       if (block_fits(q, m, n, kmax)) { *cl = q; return CLASS_L; }
     return -1;
   }
   if (reg_fits(m, n, kmax)) return CLASS_R;
   if (block_fits(1, m, n, kmax)) return CLASS_M;
-  for (int q : {2, 4})
+  for (int q : {2, 4, 8, 16})
     if (block_fits(q, m, n, kmax)) { *cl = q; return CLASS_L; }
   return -1;
 }
@@ -243,6 +257,9 @@ static void fill_args(const lpb_ctx* c, SimplexArgs& a, int64_t lp0, int64_t cnt
   a.bland_K = c->opt.bland_after == 0 ? n + m : c->opt.bland_after;
   a.kmax = kmax;
   a.ticket = ticket;
+  a.rpc = c->opt.pivot_rule == LPB_RULE_RPC ? 1 : 0;
+  a.rpc_seed = c->opt.rpc_seed;
+  a.lp_base = lp0;
   // bulk-copy prefetch needs every LP's A to start 16-byte aligned and be a multiple of 16
   // bytes (m*n even), and to fit SMEM next to the register layouts' small SMEM state
   const int64_t bytes = (int64_t)m * n * 8;
@@ -277,6 +294,8 @@ static int run_general(lpb_ctx* c, cudaStream_t s, int64_t lp0, int64_t cnt, con
     }
     *launches += 1;
     c->last_class = CLASS_S;
+    c->last_cluster = 0;
+    c->last_grid = 0;
     return LPB_OK;
   }
   const bool r_ok_worst = reg_fits(c->m, c->n, c->m);
@@ -311,6 +330,8 @@ static int run_general(lpb_ctx* c, cudaStream_t s, int64_t lp0, int64_t cnt, con
   }
   *launches += 1;
   c->last_class = klass;
+  c->last_cluster = klass == CLASS_L ? cl : 1;
+  c->last_grid = ctas;
   return LPB_OK;
 }
 
@@ -334,6 +355,8 @@ static int run_hyperbox(lpb_ctx* c, cudaStream_t s, int64_t lp0, int64_t cnt, co
   }
   *launches += 1;
   c->last_class = CLASS_H;
+  c->last_cluster = 0;
+  c->last_grid = 0;
   return LPB_OK;
 }
 
@@ -540,5 +563,12 @@ extern "C" int lpb_last_launch_info(lpb_ctx* c, int32_t* launches, int32_t* kern
   if (!c) return LPB_EINVAL;
   if (launches) *launches = c->last_launches;
   if (kernel_class) *kernel_class = c->last_class;
+  return LPB_OK;
+}
+
+extern "C" int lpb_last_launch_shape(lpb_ctx* c, int32_t* cluster_ctas, int32_t* grid_ctas) {
+  if (!c) return LPB_EINVAL;
+  if (cluster_ctas) *cluster_ctas = c->last_cluster;
+  if (grid_ctas) *grid_ctas = c->last_grid;
   return LPB_OK;
 }

@@ -33,6 +33,9 @@ struct SimplexArgs {
   int* ticket;      // persistent-scheduler counter, zeroed before each launch
   int prefetch;     // R class: A (m*n*8 bytes, 16-B aligned per LP) is bulk-prefetched to SMEM
   long long* prof;  // optional per-CTA phase cycle counters (diagnostics), normally null
+  int rpc;           // Step 1 rule: 0 LPC (Dantzig), 1 RPC (include/lpb.h LPB_RULE_RPC)
+  uint64_t rpc_seed;
+  int64_t lp_base;   // index in the lpb_solve_batch call of this launch's LP 0 (RPC key)
 };
 
 struct HyperboxArgs {

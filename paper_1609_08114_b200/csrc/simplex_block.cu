@@ -1,5 +1,5 @@
 // simplex_block.cu — M and L size classes: one LP per thread block (cl = 1) or per
-// thread-block cluster of cl CTAs (cl = 2, 4) with the CONDENSED fp64 simplex tableau
+// thread-block cluster of cl CTAs (cl = 2, 4, 8, 16) with the CONDENSED fp64 simplex tableau
 // resident in shared memory (distributed shared memory across the cluster).
 //
 // The method is the paper's dense-tableau simplex (§3.1 Steps 1-3, lines 91-103;
@@ -31,6 +31,7 @@
 #include "lpb_fp64.cuh"
 #include "lpb_internal.cuh"
 #include "lpb_reduce.cuh"
+#include "lpb_rng.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -157,10 +158,11 @@ __device__ __forceinline__ Cand cluster_reduce(Cand c, const Smem& s, int& par,
     return r;
   } else {
     if (threadIdx.x == 0)
+#pragma unroll 1
       for (int q = 0; q < CL; ++q) *cl.remote(cs + cl.rank, q) = r;
     cl.sync();
     Cand best = cs[0];
-#pragma unroll
+#pragma unroll 4
     for (int q = 1; q < CL; ++q) {
       const Cand o = cs[q];
       if (better<MODE>(o, best)) best = o;
@@ -252,6 +254,7 @@ __device__ __forceinline__ void pivot_local(const Smem& s, const double* colE, i
 
 template <int CL>
 __global__ void __launch_bounds__(NT) simplex_block_kernel(SimplexArgs a) {
+  constexpr bool PULL = CL >= 8;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const Cluster<CL> cl;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
@@ -275,12 +278,13 @@ __global__ void __launch_bounds__(NT) simplex_block_kernel(SimplexArgs a) {
   s.cslots = s.wslots + 2 * NW;
   s.rec = reinterpret_cast<Rec*>(s.cslots + 2 * CL);
   s.colC = reinterpret_cast<double*>(s.rec + 2 * CL);
-  s.ctl = reinterpret_cast<Ctl*>(s.colC + 2 * CL * RC);
+  s.ctl = reinterpret_cast<Ctl*>(s.colC + 2 * (PULL ? 1 : CL) * RC);
 
   int par = 0;
   for (;;) {
     if (cl.rank == 0 && tid == 0) {
       const int t = atomicAdd(a.ticket, 1);
+#pragma unroll 1
       for (int q = 0; q < CL; ++q) cl.remote(s.ctl, q)->lp = t;
     }
     cl.sync();
@@ -322,6 +326,7 @@ __global__ void __launch_bounds__(NT) simplex_block_kernel(SimplexArgs a) {
     __syncthreads();
 
     int st = -1, it1 = 0, it2 = 0;
+    const uint64_t lpkey = a.rpc ? rpc_lp_key(a.rpc_seed, a.lp_base + lp) : 0ull;
     const int cnt = max(0, min(Q, n + k - cl.rank * Q));  // live local positions
     const int Wa = cnt + 1;                               // + RHS at local column cnt
     const int Wp = (Wa + 1) & ~1;                         // whole 128-bit pairs
@@ -373,12 +378,16 @@ __global__ void __launch_bounds__(NT) simplex_block_kernel(SimplexArgs a) {
       // Step 1: this CTA's entering candidate (LPC/Dantzig, lowest variable index on ties;
       // Bland), then Step 2 on that candidate column, speculatively: the global winner is
       // one of the CL proposals, so ONE cluster barrier per pivot publishes them all.
+      // RPC: the candidate's value is its counter-based score u < 2^53 (exact as a double,
+      // lpb_rng.cuh), so the same max-value reductions pick the largest score.
       Cand ce{0.0, 0, -1};
+      const bool rpc = a.rpc && !bland;
+      const uint64_t pkey = rpc ? rpc_pivot_key(lpkey, it1 + it2) : 0ull;
       for (int j = tid; j < cnt; j += NT) {
         const int var = s.nbvar[j];
         const double d = s.T[objrow * S + j];
         if (var != DEAD && d > a.eps_enter) {
-          const Cand cd{d, var, g0 + j};
+          const Cand cd{rpc ? (double)rpc_score(pkey, var) : d, var, g0 + j};
           if (bland ? better<MIN_KEY>(cd, ce) : better<MAX_V>(cd, ce)) ce = cd;
         }
       }
@@ -398,22 +407,32 @@ __global__ void __launch_bounds__(NT) simplex_block_kernel(SimplexArgs a) {
         }
       }
       cr = block_reduce<MIN_V>(cr, s.wslots + NW);
-      double* const myc = s.colC + (size_t)(pp * CL + cl.rank) * RC;
+      // PUSH (CL <= 4): the proposal column goes into every CTA's slot `rank`;
+      // PULL (CL >= 8): it stays in this CTA's own parity slot and the CTAs read the winner's
+      // slot over DSMEM after the barrier (SMEM for CL columns would not fit at m ~ 500).
+      // The PULL slot of parity pp is rewritten two pivots later, after the next cluster
+      // barrier, which every reader has passed only once its pivot_local read is done.
+      double* const myc = PULL ? s.colC + (size_t)pp * RC
+                               : s.colC + (size_t)(pp * CL + cl.rank) * RC;
       if (ce.pos >= 0)
         for (int i = tid; i < nrow; i += NT) {
           const double v = s.T[i * S + jc];
+          if constexpr (PULL) {
+            myc[i] = v;
+          } else {
 #pragma unroll
-          for (int q = 0; q < CL; ++q) cl.remote(myc, q)[i] = v;
+            for (int q = 0; q < CL; ++q) cl.remote(myc, q)[i] = v;
+          }
         }
       if (tid == 0) {
         const Rec r{ce, cr.v, cr.pos, 0};
-#pragma unroll
-        for (int q = 0; q < CL; ++q) *cl.remote(s.rec + pp * CL + cl.rank, q) = r;
+#pragma unroll 1
+        for (int q = 0; q < CL; ++q) *cl.remote(s.rec + pp * CL + cl.rank, q) = r;  // 32 B
       }
       cl.sync();
       int win = 0;
       ce = s.rec[pp * CL].ce;
-#pragma unroll
+#pragma unroll 4
       for (int q = 1; q < CL; ++q) {
         const Cand o = s.rec[pp * CL + q].ce;
         if (bland ? better<MIN_KEY>(o, ce) : better<MAX_V>(o, ce)) {
@@ -443,6 +462,7 @@ __global__ void __launch_bounds__(NT) simplex_block_kernel(SimplexArgs a) {
           if (cl.rank == owner) {
             for (int i = tid; i < m + 2; i += NT) {
               const double v = s.T[i * S + jloc];
+#pragma unroll 1
               for (int q = 0; q < CL; ++q) cl.remote(s.colE, q)[i] = v;
             }
           }
@@ -461,8 +481,9 @@ __global__ void __launch_bounds__(NT) simplex_block_kernel(SimplexArgs a) {
       if (l < 0) { st = (phase == 2) ? ST_UNBOUNDED : ST_NUMERICAL; break; }
       // Step 3: pivot (the winner's column is in this CTA's slot `win`)
       const int jloc = ce.pos - win * Q;
-      pivot_local(s, s.colC + (size_t)(pp * CL + win) * RC, S, Wa, nrow, l, cl.rank == win, jloc,
-                  ce.key);
+      const double* wcol = PULL ? cl.remote(s.colC + (size_t)pp * RC, win)
+                                : s.colC + (size_t)(pp * CL + win) * RC;
+      pivot_local(s, wcol, S, Wa, nrow, l, cl.rank == win, jloc, ce.key);
       pp ^= 1;
       if (phase == 1) ++it1; else ++it2;
       stall = (theta > 0.0) ? 0 : stall + 1;
@@ -503,8 +524,9 @@ size_t block_smem_bytes(int cl, int m, int n, int kmax) {
   size_t bytes = sizeof(double) * ((size_t)(m + 2) * S + 2 * (size_t)(m + 2) + S);
   bytes += sizeof(int) * ((size_t)(Q + 1) + 2 * (size_t)m + NW);
   bytes = (bytes + 15) & ~size_t(15);
+  const size_t ncol = cl >= 8 ? 1 : (size_t)cl;  // proposal columns per parity (PUSH: cl)
   bytes += sizeof(Cand) * (2 * NW + 2 * cl) + sizeof(Rec) * 2 * cl +
-           sizeof(double) * 2 * (size_t)cl * (m + 2) + sizeof(Ctl);
+           sizeof(double) * 2 * ncol * (m + 2) + sizeof(Ctl);
   return bytes;
 }
 
@@ -540,6 +562,11 @@ static cudaError_t launch_cl(const SimplexArgs& a, int grid_override, cudaStream
     cudaError_t e = cudaFuncSetAttribute(simplex_block_kernel<CL>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
+    if constexpr (CL > 8) {  // 16-CTA clusters are a non-portable (opt-in) size on sm_100
+      e = cudaFuncSetAttribute(simplex_block_kernel<CL>,
+                               cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      if (e != cudaSuccess) return e;
+    }
     if constexpr (CL == 1) {
       int per_sm = 0;
       e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, simplex_block_kernel<1>, NT,
@@ -573,6 +600,8 @@ cudaError_t launch_simplex_block(int cl, const SimplexArgs& a, int grid_override
     case 1: return launch_cl<1>(a, grid_override, s, ctas_out);
     case 2: return launch_cl<2>(a, grid_override, s, ctas_out);
     case 4: return launch_cl<4>(a, grid_override, s, ctas_out);
+    case 8: return launch_cl<8>(a, grid_override, s, ctas_out);
+    case 16: return launch_cl<16>(a, grid_override, s, ctas_out);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -28,6 +28,7 @@
 #include "lpb_fp64.cuh"
 #include "lpb_internal.cuh"
 #include "lpb_reduce.cuh"
+#include "lpb_rng.cuh"
 
 namespace lpb {
 namespace {
@@ -94,7 +95,7 @@ struct RegSmem {
 // AS > 0: each thread also owns AS more rows (i = tr + TR*(A+s)) kept in a thread-private
 // SMEM slice (double2 pairs of positions, thread-interleaved: conflict-free 128-bit accesses),
 // so that three LPs fit one SM (registers + SMEM) instead of two (registers only).
-template <int TR, int TC, int A, int AS, int BC, bool TWO, int MINB>
+template <int TR, int TC, int A, int AS, int BC, bool TWO, int MINB, bool RPC>
 __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs a) {
   constexpr int AT = A + AS;  // rows per thread-row
   constexpr int NT = TR * TC, RCAP = TR * AT, CCAP = TC * BC, NWARP = NT / 32;
@@ -282,6 +283,7 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
     // ---- Steps 1-3, two phases ----
     int it1 = 0, it2 = 0, stall = 0, phase = (TWO && k > 0) ? 1 : 2;
     int par = 0, l_prev = -1, dl = 0;
+    const uint64_t lpkey = RPC ? rpc_lp_key(a.rpc_seed, a.lp_base + lp) : 0ull;
     bool pend = false, drive = false;
     while (st < 0) {
       const bool bland = a.bland_K > 0 && stall >= a.bland_K;
@@ -344,7 +346,27 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
         int bb = 0;
         unsigned bvar = 0;
         bool val;
-        if (!bland) {
+        const bool rpc = RPC && !bland;  // a separate instantiation keeps LPC's registers
+        unsigned long long ukey = 0ull;
+        if (rpc) {  // RPC: the candidate with the largest counter-based score (lpb_rng.cuh)
+          val = false;
+          bvar = 0xffffffffu;
+          const uint64_t pkey = rpc_pivot_key(lpkey, it1 + it2);
+#pragma unroll 1
+          for (int b = 0; b < BC; ++b) {
+            const double v = p1 ? d1[TWO ? b : 0] : d2[b];
+            if (v > a.eps_enter) {
+              const unsigned var = (unsigned)sm.nbvar[tc + TC * b];
+              const unsigned long long u = rpc_score(pkey, (int)var);
+              if (!val || u > ukey || (u == ukey && var < bvar)) {
+                val = true;
+                ukey = u;
+                bvar = var;
+                bb = b;
+              }
+            }
+          }
+        } else if (!bland) {
 #pragma unroll
           for (int b = 0; b < BC; ++b) {
             const double v = p1 ? d1[TWO ? b : 0] : d2[b];
@@ -390,7 +412,8 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
             }
           }
         }
-        const int wl = bland ? warp_argmin(val, 0ull, bvar) : warp_argmax(val, okey(bv), bvar);
+        const int wl = bland ? warp_argmin(val, 0ull, bvar)
+                             : warp_argmax(val, rpc ? ukey : okey(bv), bvar);
         if (wl < 0) {
           if (phase == 2) { st = ST_OPTIMAL; break; }
           if (z1 > a.eps_phase1 * fmax(1.0, binf)) { st = ST_INFEASIBLE; break; }
@@ -662,9 +685,9 @@ struct RegCfg {
   X(4, 16, 16, 7, 0, 7, false, 1)       \
   X(5, 16, 16, 7, 0, 7, true, 1)
 
-template <int TR, int TC, int A, int AS, int BC, bool TWO, int MINB>
+template <int TR, int TC, int A, int AS, int BC, bool TWO, int MINB, bool RPC>
 cudaError_t launch_one(const SimplexArgs& a, int grid_override, cudaStream_t s, int* ctas) {
-  auto kern = simplex_reg_kernel<TR, TC, A, AS, BC, TWO, MINB>;
+  auto kern = simplex_reg_kernel<TR, TC, A, AS, BC, TWO, MINB, RPC>;
   const size_t dsm = AS > 0 ? (size_t)AS * ((BC + 1) / 2) * TR * TC * 16
                             : (a.prefetch ? (size_t)a.m * a.n * 8 : 0);
   // attribute + occupancy queries are host round trips: cache them per (device, smem size)
@@ -722,7 +745,9 @@ cudaError_t launch_simplex_reg(const SimplexArgs& a, int grid_override, cudaStre
                                int* ctas_out) {
   switch (pick_cfg(a.m, a.n, a.kmax)) {
 #define X(id, TR, TC, A, AS, BC, TWO, MINB) \
-  case id: return launch_one<TR, TC, A, AS, BC, TWO, MINB>(a, grid_override, s, ctas_out);
+  case id:                                                                        \
+    return a.rpc ? launch_one<TR, TC, A, AS, BC, TWO, MINB, true>(a, grid_override, s, ctas_out) \
+                 : launch_one<TR, TC, A, AS, BC, TWO, MINB, false>(a, grid_override, s, ctas_out);
     LPB_REG_CONFIGS(X)
 #undef X
     default: return cudaErrorInvalidValue;

@@ -12,6 +12,7 @@
 
 #include "lpb_fp64.cuh"
 #include "lpb_internal.cuh"
+#include "lpb_rng.cuh"
 
 namespace lpb {
 namespace {
@@ -79,6 +80,7 @@ __global__ void __launch_bounds__(S_NT) simplex_thread_kernel(SimplexArgs a) {
     }
 
   int st = -1, it1 = 0, it2 = 0, stall = 0, phase = k > 0 ? 1 : 2;
+  const uint64_t lpkey = a.rpc ? rpc_lp_key(a.rpc_seed, a.lp_base + lp) : 0ull;
   auto pivot = [&](int l, int e, int nrow) {
     const double pe = T[l * W + e];
     const double r = recip_of(pe);
@@ -104,13 +106,26 @@ __global__ void __launch_bounds__(S_NT) simplex_thread_kernel(SimplexArgs a) {
     const int orow = phase == 1 ? m + 1 : m;
     const int nrow = phase == 1 ? m + 2 : m + 1;
     const bool bland = a.bland_K > 0 && stall >= a.bland_K;
-    // Step 1 (LPC / Dantzig, lowest variable index on ties; Bland)
+    // Step 1 (LPC / Dantzig, lowest variable index on ties; RPC: largest counter-based
+    // score u_j, include/lpb.h; Bland)
     int e = -1, ev = INT_MAX;
     double best = 0.0;
+    const bool rpc = a.rpc && !bland;
+    const uint64_t pkey = rpc ? rpc_pivot_key(lpkey, it1 + it2) : 0ull;
+    uint64_t ubest = 0;
     for (int p = 0; p < npos; ++p) {
       const int var = nbv(p);
       const double d = T[orow * W + p];
       if (var == DEADV || !(d > a.eps_enter)) continue;
+      if (rpc) {
+        const uint64_t u = rpc_score(pkey, var);
+        if (e < 0 || u > ubest || (u == ubest && var < ev)) {
+          e = p;
+          ev = var;
+          ubest = u;
+        }
+        continue;
+      }
       if (bland ? (var < ev) : (e < 0 || d > best || (d == best && var < ev))) {
         e = p;
         ev = var;

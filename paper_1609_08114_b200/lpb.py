@@ -29,6 +29,8 @@ OK, EINVAL, ENOMEM, ECUDA, ESTATE, ETOOBIG = 0, -1, -2, -3, -4, -5
 DEVICE_PTRS, SHARED_BOX, NO_X, ASYNC, SHARED_AB = 1, 2, 4, 8, 16
 CLASS_NAMES = {0: "auto", 1: "S", 2: "M", 3: "L", 4: "R", 5: "H", 6: "T"}
 CLASS_IDS = {v: k for k, v in CLASS_NAMES.items()}
+RULE_LPC, RULE_RPC = 0, 1  # lpb_options.pivot_rule
+RULE_IDS = {"LPC": RULE_LPC, "RPC": RULE_RPC}
 
 
 class Options(ctypes.Structure):
@@ -44,6 +46,9 @@ class Options(ctypes.Structure):
         ("n_chunks", ctypes.c_int32),
         ("kernel_class", ctypes.c_int32),
         ("grid_ctas", ctypes.c_int32),
+        ("cluster_ctas", ctypes.c_int32),
+        ("pivot_rule", ctypes.c_int32),
+        ("rpc_seed", ctypes.c_uint64),
     ]
 
 
@@ -62,6 +67,8 @@ _lib.lpb_last_kernel_timing.argtypes = [P, ctypes.POINTER(ctypes.c_double)]
 _lib.lpb_last_kernel_timing.restype = ctypes.c_int
 _lib.lpb_last_launch_info.argtypes = [P, ctypes.POINTER(ctypes.c_int32),
                                       ctypes.POINTER(ctypes.c_int32)]
+_lib.lpb_last_launch_shape.argtypes = [P, ctypes.POINTER(ctypes.c_int32),
+                                       ctypes.POINTER(ctypes.c_int32)]
 _lib.lpb_destroy.argtypes = [P]
 _lib.lpb_strerror.argtypes = [ctypes.c_int]
 _lib.lpb_strerror.restype = ctypes.c_char_p
@@ -71,7 +78,7 @@ _lib.lpb_last_error.argtypes = [P]
 _lib.lpb_last_error.restype = ctypes.c_char_p
 for _f in ("lpb_default_options", "lpb_create", "lpb_solve_batch", "lpb_solve_batch_into",
            "lpb_results", "lpb_result_device_ptrs", "lpb_sync", "lpb_last_timing",
-           "lpb_last_launch_info", "lpb_destroy"):
+           "lpb_last_launch_info", "lpb_last_launch_shape", "lpb_destroy"):
     getattr(_lib, _f).restype = ctypes.c_int
 
 
@@ -95,6 +102,8 @@ def default_options(**kw) -> Options:
             continue
         if k == "kernel_class" and isinstance(v, str):
             v = CLASS_IDS[v]
+        if k == "pivot_rule" and isinstance(v, str):
+            v = RULE_IDS[v.upper()]
         setattr(o, k, v)
     return o
 
@@ -227,6 +236,12 @@ class Solver:
         n, k = ctypes.c_int32(), ctypes.c_int32()
         _check(_lib.lpb_last_launch_info(self._ctx, ctypes.byref(n), ctypes.byref(k)))
         return n.value, CLASS_NAMES.get(k.value, str(k.value))
+
+    def launch_shape(self):
+        """(CTAs per LP -- the L class's cluster size --, grid CTAs) of the last launch."""
+        cl, g = ctypes.c_int32(), ctypes.c_int32()
+        _check(_lib.lpb_last_launch_shape(self._ctx, ctypes.byref(cl), ctypes.byref(g)))
+        return cl.value, g.value
 
 
 def _wrap_device(ptr, shape, dtype, device):

@@ -25,7 +25,9 @@ def gpu_solve(A, b, c, *, path="device", want_x=True, **opts):
         s = lpb.Solver(B, m, n, lpb.GENERAL, **opts)
         s.solve_device(At, bt, ct, want_x=want_x, sync=True, shared_ab=shared)
         r = {k: v.cpu().numpy() for k, v in s.device_results(want_x).items()}
-        r["launch"] = s.launch_info()
+        nl, klass = s.launch_info()
+        cl, grid = s.launch_shape()
+        r["launch"] = dict(launches=nl, **{"class": klass}, cluster=cl, grid=grid)
         s.close()
         return r
     r = lpb.solve(A, b, c, want_x=want_x, **opts)

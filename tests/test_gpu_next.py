@@ -1,0 +1,99 @@
+"""GPU parity for the SURVEY §8(f) "next" rows, against the oracle element by element:
+  NEXT-2  larger LPs (the paper's fig:TimeLPplotting dims 300/500 and its limits 511 type-1 /
+          340 type-2) on 4-, 8- and 16-CTA clusters (L class), plus the
+          8/16-CTA PULL column exchange forced on small LPs;
+  NEXT-3  the RPC entering rule (include/lpb.h LPB_RULE_RPC, reading R15) in
+          every size class, on the device and the chunked host path.
+Bit-exact as everywhere else: status, iterations, objective and x identical."""
+import numpy as np
+import pytest
+
+import lpgen
+import oracle
+from gpu_util import compare, gpu_solve
+
+pytestmark = pytest.mark.gpu
+
+CLASSES = ["S", "R", "M", "L", "T"]
+
+
+@pytest.mark.parametrize("gen,m,n,B,cl", [
+    ("G1", 300, 300, 8, 4), ("G2", 340, 340, 4, 8), ("G1", 511, 511, 4, 16),
+    ("G1", 500, 500, 3, 16), ("G2", 300, 300, 3, 8),
+])
+def test_large_sizes(gen, m, n, B, cl):
+    A, b, c = (lpgen.signed_bounded if gen == "G1" else lpgen.twophase_signed)(B, m, n, 11 + m)
+    o = oracle.solve(A, b, c)
+    g = gpu_solve(A, b, c)  # auto size class
+    compare(A, b, c, g, o)
+    assert g["launch"]["class"] == "L" and g["launch"]["cluster"] == cl, g["launch"]
+
+
+@pytest.mark.parametrize("cl", [2, 4, 8, 16])
+@pytest.mark.parametrize("gen,m,n,B", [("G1", 100, 100, 60), ("G2", 50, 50, 80),
+                                       ("mixneg", 20, 20, 400), ("deg", 8, 8, 600)])
+def test_forced_cluster_sizes(cl, gen, m, n, B):
+    if gen == "G1":
+        A, b, c = lpgen.signed_bounded(B, m, n, 21 + cl)
+    elif gen == "G2":
+        A, b, c = lpgen.twophase_signed(B, m, n, 22 + cl)
+    elif gen == "deg":
+        A, b, c = lpgen.degenerate(B, m, n, 23 + cl, negative_b=True)
+    else:
+        A, b, c = lpgen.status_mix(B, m, n, 24 + cl, infeasible_start=True)
+    kw = dict(bland_after=2) if gen == "deg" else {}
+    o = oracle.solve(A, b, c, **kw)
+    g = gpu_solve(A, b, c, kernel_class="L", cluster_ctas=cl, **kw)
+    compare(A, b, c, g, o)
+    assert g["launch"]["cluster"] == cl
+
+
+@pytest.mark.parametrize("klass", CLASSES)
+@pytest.mark.parametrize("gen,m,n,B", [
+    ("G1", 5, 5, 3000), ("G1", 28, 28, 400), ("G1", 100, 100, 100), ("mixneg", 6, 6, 3000),
+    ("G2", 8, 8, 2000), ("G2", 50, 50, 60), ("deg", 8, 8, 2000), ("mix", 7, 60, 300),
+])
+def test_rpc_parity(klass, gen, m, n, B):
+    if gen == "G1":
+        A, b, c = lpgen.signed_bounded(B, m, n, 31 + m)
+    elif gen == "G2":
+        A, b, c = lpgen.twophase_signed(B, m, n, 32 + m)
+    elif gen == "deg":
+        A, b, c = lpgen.degenerate(B, m, n, 33 + m, negative_b=True)
+    else:
+        A, b, c = lpgen.status_mix(B, m, n, 34 + m, infeasible_start=gen.endswith("neg"))
+    k = int((b < 0).sum(axis=1).max())
+    if klass == "S" and (m > 8 or n > 8):
+        pytest.skip("the thread-per-LP class holds m, n <= 8")
+    if klass == "T" and not (m <= 128 and n + k <= 100):
+        pytest.skip("no row-per-thread layout for this size")
+    if klass == "R" and not (m <= 112 and n + k <= 112):
+        pytest.skip("no register layout for this size")
+    seed = 0xC0FFEE + m
+    o = oracle.solve(A, b, c, pivot_rule="RPC", rpc_seed=seed)
+    try:
+        g = gpu_solve(A, b, c, kernel_class=klass, pivot_rule="RPC", rpc_seed=seed)
+    except Exception as ex:  # a class without a layout for (m, n + k) reports ETOOBIG
+        if "size class" in str(ex):
+            pytest.skip(str(ex))
+        raise
+    compare(A, b, c, g, o)
+    if gen == "G1" and m >= 28:  # RPC takes more pivots than LPC on average
+        assert o["iters"][:, 1].mean() > oracle.solve(A, b, c)["iters"][:, 1].mean()
+
+
+def test_rpc_host_path_chunks_keep_batch_indices():
+    """The RPC draw is keyed on the LP's index in the whole call: chunked host pipelines
+    (lp_base per chunk) and the device path give identical pivot paths."""
+    A, b, c = lpgen.status_mix(1999, 9, 9, 41, infeasible_start=True)
+    o = oracle.solve(A, b, c, pivot_rule="RPC", rpc_seed=5)
+    for nch in (1, 7):
+        g = gpu_solve(A, b, c, path="host", n_chunks=nch, pivot_rule="RPC", rpc_seed=5)
+        compare(A, b, c, g, o)
+
+
+def test_rpc_large_cluster():
+    A, b, c = lpgen.twophase_signed(3, 200, 200, 43)
+    o = oracle.solve(A, b, c, pivot_rule="RPC", rpc_seed=9)
+    g = gpu_solve(A, b, c, pivot_rule="RPC", rpc_seed=9)
+    compare(A, b, c, g, o)
