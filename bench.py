@@ -37,10 +37,18 @@ UNIT = "LPs/s"
 PAPER_LPS = {"cfg4": 4001000 / 0.406, "cfg5": 6003000 / 2.388}
 # oracle sample per reference step (bounded CPU work)
 REF_SAMPLE = {"cfg1": 1000, "cfg2": 240, "cfg3": 8, "cfg4": 4001000, "cfg5": 1000000,
-              "cfg2s": 240, "cfg3s": 8}
+              "cfg2s": 240, "cfg3s": 8, "cfg2r": 160, "cfg6": 32, "cfg7": 16, "cfg8": 4}
 CPU_SAMPLE = {"cfg1": 1000, "cfg2": 1200, "cfg3": 24, "cfg4": 4001000, "cfg5": 6003000,
-              "cfg2s": 1200, "cfg3s": 24}
+              "cfg2s": 1200, "cfg3s": 24, "cfg2r": 800, "cfg6": 160, "cfg7": 32, "cfg8": 16}
 L2_BYTES = 126 * 1024 * 1024
+
+
+def rule_opts(name):
+    """Entering-rule options of a config (NEXT-3 RPC runs use the config seed)."""
+    c = lpgen.CONFIGS[name]
+    if c.get("rule", "LPC") == "RPC":
+        return {"pivot_rule": "RPC", "rpc_seed": c["seed"]}
+    return {}
 
 
 def describe(name):
@@ -49,6 +57,8 @@ def describe(name):
         return (f"{name}: type-3 hyperbox, {c['B']} LPs of n={c['n']} (shared box, G3 seed "
                 f"{c['seed']})")
     t = "type-1 (b>=0)" if c["gen"] == "G1" else "type-2 (two-phase)"
+    if c.get("rule", "LPC") != "LPC":
+        t += f", {c['rule']} entering rule (seed {c['seed']})"
     if c.get("shared"):
         return (f"{name}: {t}, {c['B']} objectives over one {c['m']}x{c['n']} polytope "
                 f"({c['gen']} seed {c['seed']}, shared A/b)")
@@ -149,7 +159,7 @@ def cpu_baseline(name, sample_n):
     else:
         A, b, c = general_sample(name, sample_n)
         t = time.perf_counter()
-        r = oracle.solve(A, b, c)
+        r = oracle.solve(A, b, c, **rule_opts(name))
         dt = time.perf_counter() - t
         n_lp = A.shape[0]
     return {"value": n_lp / dt, "unit": UNIT, "cores": int(r["threads"]), "kind": "oracle",
@@ -171,7 +181,7 @@ def run_reference(args):
         n_lp = dirs.shape[0]
     else:
         A, b, c = general_sample(name, n)
-        step = lambda: oracle.solve(A, b, c)  # noqa: E731
+        step = lambda: oracle.solve(A, b, c, **rule_opts(name))  # noqa: E731
         n_lp = A.shape[0]
     for _ in range(args.warmup):
         step()
@@ -245,7 +255,10 @@ def main():
         in_bytes = A.nbytes + b.nbytes + c.nbytes
         host_in = (A, b, c)
         kind = lpb.GENERAL
-    solver = lpb.Solver(B, m, n, kind)
+    ropts = rule_opts(name)
+    if ropts:
+        ropts["lp_index_base"] = lo  # RPC keys on the LP's index in the whole N*B batch
+    solver = lpb.Solver(B, m, n, kind, **ropts)
     flush = None
     if in_bytes <= 2 * L2_BYTES:  # small inputs: flush L2 between timed steps
         flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
@@ -317,7 +330,7 @@ def main():
         out_obj = lpb.pinned_empty((B,))
         out_x = lpb.pinned_empty((B, n))
         out_it = lpb.pinned_empty((B, 2), np.int32) if not hyper else None
-        hs = lpb.Solver(B, m, n, kind)
+        hs = lpb.Solver(B, m, n, kind, **ropts)
         hs.solve_host_into(*pin, out_st, out_obj, out_x, out_it, shared_box=hyper,
                            shared_ab=sab)  # warm
         e_ms = []
@@ -349,7 +362,9 @@ def main():
                        "kind": "hyperbox" if hyper else "general",
                        "l2": "flushed between steps" if flush is not None else "inputs > L2",
                        "parallelism": f"dp{world} (contiguous LP shards, no collective)",
-                       "kernel_class": klass},
+                       "kernel_class": klass,
+                       "ctas_per_lp": solver.launch_shape()[0],
+                       "pivot_rule": lpgen.CONFIGS[name].get("rule", "LPC")},
             "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": e2e,

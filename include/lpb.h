@@ -107,6 +107,10 @@ typedef struct {
                           Positive Coefficient.  Bland's rule still takes over after
                           bland_after degenerate pivots under either rule.                   */
   uint64_t rpc_seed;   /* RPC: seed of the counter-based choice (see LPB_RULE_RPC)            */
+  int64_t lp_index_base;/* index, in the caller's numbering, of this context's LP 0 (RPC keys
+                          k = lp_index_base + position in the call): a rank solving LPs
+                          [lo, hi) of a sharded batch passes lo and follows exactly the pivot
+                          path of an unsharded run; default 0                                */
 } lpb_options;
 
 /* Entering rules (lpb_options.pivot_rule).
@@ -114,7 +118,7 @@ typedef struct {
  * left artificial) without a stored random state: with mix64 the SplitMix64 finaliser
  * (z += 0x9E3779B97F4A7C15; z = (z^(z>>30))*0xBF58476D1CE4E5B9; z = (z^(z>>27))*
  * 0x94D049BB133111EB; z ^= z>>31), candidate variable j (0..n-1 structural, n+i slack of row
- * i) of LP k (its 0-based index in the lpb_solve_batch call) at pivot t (= phase-I + phase-II
+ * i) of LP k (lp_index_base + its 0-based index in the lpb_solve_batch call) at pivot t (= phase-I + phase-II
  * pivots done so far) scores  u = mix64(mix64(mix64(rpc_seed ^ mix64(k)) ^ t) ^ j) >> 11
  * (an integer < 2^53), and the candidate with the largest u enters (ties: lowest j).  Every
  * candidate is equally likely to win, the choice depends only on (seed, k, t, j) -- not on

@@ -230,6 +230,14 @@ CONFIGS = {
     "cfg5": dict(kind="hyperbox", gen="G3", B=6003000, n=28, seed=5),
     "cfg2s": dict(kind="general", gen="G1", B=50000, m=100, n=100, seed=2, shared=True),
     "cfg3s": dict(kind="general", gen="G2", B=10000, m=200, n=200, seed=3, shared=True),
+    # cfg2's workload under the RPC rule (the paper's 6.74x RPC run,
+    # 50k LPs of 100-dim); the rule's seed is the config seed
+    "cfg2r": dict(kind="general", gen="G1", B=50000, m=100, n=100, seed=2, rule="RPC"),
+    # the paper's larger dims (fig:TimeLPplotting 300/500, PAPER.md:
+    # 230-249) and its size limits (511 type-1, 340 type-2)
+    "cfg6": dict(kind="general", gen="G1", B=5000, m=300, n=300, seed=6),
+    "cfg7": dict(kind="general", gen="G1", B=1000, m=500, n=500, seed=7),
+    "cfg8": dict(kind="general", gen="G2", B=1000, m=340, n=340, seed=8),
 }
 
 

@@ -95,6 +95,7 @@ extern "C" int lpb_default_options(lpb_options* o) {
   o->cluster_ctas = 0;
   o->pivot_rule = LPB_RULE_LPC;
   o->rpc_seed = 0;
+  o->lp_index_base = 0;
   return LPB_OK;
 }
 
@@ -259,7 +260,7 @@ static void fill_args(const lpb_ctx* c, SimplexArgs& a, int64_t lp0, int64_t cnt
   a.ticket = ticket;
   a.rpc = c->opt.pivot_rule == LPB_RULE_RPC ? 1 : 0;
   a.rpc_seed = c->opt.rpc_seed;
-  a.lp_base = lp0;
+  a.lp_base = c->opt.lp_index_base + lp0;
   // bulk-copy prefetch needs every LP's A to start 16-byte aligned and be a multiple of 16
   // bytes (m*n even), and to fit SMEM next to the register layouts' small SMEM state
   const int64_t bytes = (int64_t)m * n * 8;

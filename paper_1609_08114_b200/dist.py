@@ -50,6 +50,11 @@ def solve_sharded(A, b, c, B: int, *, gather: bool = True, **opts):
     Returns (results_on_rank0_or_local, max_over_ranks_ms)."""
     from . import lpb
     Bl, m, n = A.shape
+    world = dist.get_world_size() if dist.is_available() and dist.is_initialized() else 1
+    rank = dist.get_rank() if world > 1 else 0
+    # LP indices of the whole batch key the RPC rule: a sharded run follows the same pivot
+    # paths as an unsharded one
+    opts.setdefault("lp_index_base", shard_range(B, rank, world)[0])
     s = lpb.Solver(Bl, m, n, lpb.GENERAL, **opts)
     s.solve_device(A, b, c, sync=True)
     ms = max_over_ranks(s.timing()[0], device=A.device)

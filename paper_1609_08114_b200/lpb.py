@@ -49,6 +49,7 @@ class Options(ctypes.Structure):
         ("cluster_ctas", ctypes.c_int32),
         ("pivot_rule", ctypes.c_int32),
         ("rpc_seed", ctypes.c_uint64),
+        ("lp_index_base", ctypes.c_int64),
     ]
 
 

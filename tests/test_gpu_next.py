@@ -97,3 +97,15 @@ def test_rpc_large_cluster():
     o = oracle.solve(A, b, c, pivot_rule="RPC", rpc_seed=9)
     g = gpu_solve(A, b, c, pivot_rule="RPC", rpc_seed=9)
     compare(A, b, c, g, o)
+
+
+def test_rpc_lp_index_base_reproduces_unsharded_paths():
+    """A rank solving LPs [lo, hi) of a sharded batch passes lp_index_base = lo and follows
+    the pivot paths of the unsharded run (dist.solve_sharded / bench.py do this)."""
+    A, b, c = lpgen.signed_bounded(900, 20, 20, 45)
+    o = oracle.solve(A, b, c, pivot_rule="RPC", rpc_seed=77)
+    for lo, hi in ((0, 300), (300, 900), (451, 452)):
+        g = gpu_solve(A[lo:hi], b[lo:hi], c[lo:hi], pivot_rule="RPC", rpc_seed=77,
+                      lp_index_base=lo)
+        sl = {k: v[lo:hi] for k, v in o.items() if isinstance(v, np.ndarray)}
+        compare(A[lo:hi], b[lo:hi], c[lo:hi], g, sl)
