@@ -72,7 +72,6 @@ struct RegSmem {
   int negrows[RCAP];     // ascending rows with b_i < 0
   int wcount[NWARP];
   Part part[NWARP];      // ratio-test partial per warp
-  double prow_rhs;
   uint64_t mbar;         // completes when the prefetched A of LP `lp` has landed
   int lp;
   int leaving;
@@ -283,6 +282,7 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
     // ---- Steps 1-3, two phases ----
     int it1 = 0, it2 = 0, stall = 0, phase = (TWO && k > 0) ? 1 : 2;
     int par = 0, l_prev = -1, dl = 0;
+    double prr_prev = 0.0;  // RHS of the last pivot row (lazy RHS updates, R13)
     const uint64_t lpkey = RPC ? rpc_lp_key(a.rpc_seed, a.lp_base + lp) : 0ull;
     bool pend = false, drive = false;
     while (st < 0) {
@@ -412,6 +412,9 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
             }
           }
         }
+        // the RPW thread-rows of a warp hold identical replicas: only the first one competes,
+        // so a unique maximum takes warp_argmax's single-REDUX fast path
+        val = val && (RPW == 1 || lane < TC);
         const int wl = bland ? warp_argmin(val, 0ull, bvar)
                              : warp_argmax(val, rpc ? ukey : okey(bv), bvar);
         if (wl < 0) {
@@ -442,8 +445,6 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
         sm.fobj[par][0] = d2[x];                                                      \
         if constexpr (TWO) sm.fobj[par][1] = d1[x];                                   \
       }                                                                               \
-      d2[x] = 0.0;                                                                    \
-      if constexpr (TWO) d1[x] = 0.0;                                                 \
     }                                                                                 \
     break;
         switch (be) { LPB_CASES(LPB_PUB) default: break; }
@@ -453,6 +454,15 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
           double& t = ts(s_, be);
           colE[tr + TR * (A + s_)] = t;
           t = 0.0;
+        }
+      }
+      {  // the objective replicas of position e restart from 0 (branch-free, owner column)
+        const bool mine = tc == etc;
+#pragma unroll
+        for (int b = 0; b < BC; ++b) {
+          const bool z = mine && b == be;
+          d2[b] = z ? 0.0 : d2[b];
+          if constexpr (TWO) d1[b] = z ? 0.0 : d1[b];
         }
       }
       __syncwarp();
@@ -470,8 +480,7 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
           if (i < m) {
             double r = sm.rhs[i];
             if (pend) {
-              const double prr = sm.prow_rhs;
-              r = (i == l_prev) ? prr : __fma_rn(sm.fcol[par ^ 1][i], prr, r);
+              r = (i == l_prev) ? prr_prev : __fma_rn(sm.fcol[par ^ 1][i], prr_prev, r);
               sm.rhs[i] = r;
             }
             if (!drive) {
@@ -484,30 +493,35 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
           }
         }
         if (!drive) {
+          // the winning lane writes the warp's partial itself (no shuffles)
           const int wl = warp_argmin(val, okey(ratio), ikey(tie));
-          Part pw{0.0, INT_MAX, -1};
-          if (wl >= 0) {
-            pw.v = __shfl_sync(FULL, ratio, wl);
-            pw.tie = __shfl_sync(FULL, tie, wl);
-            pw.idx = __shfl_sync(FULL, i, wl);
-          }
-          if (lane == 0) sm.part[w] = pw;
+          if (lane == (wl < 0 ? 0 : wl)) sm.part[w] = wl < 0 ? Part{0.0, INT_MAX, -1}
+                                                             : Part{ratio, tie, i};
         }
       }
       LPB_PROF_MARK(2)
       gsync<NT>();  // barrier 1
       LPB_PROF_MARK(3)
       double theta = 0.0;
-      if (!drive) {  // Step 2c: argmin over the warp partials, in every warp
-        const Part q = (lane < NWARP) ? sm.part[lane] : Part{0.0, INT_MAX, -1};
-        const int ql = warp_argmin(q.idx >= 0, okey(q.v), ikey(q.tie));
-        if (ql < 0) { st = (phase == 2) ? ST_UNBOUNDED : ST_NUMERICAL; break; }
-        l = __shfl_sync(FULL, q.idx, ql);
-        theta = __shfl_sync(FULL, q.v, ql);
+      if (!drive) {  // Step 2c: every thread scans the NWARP warp partials (ascending warp)
+        Part q = sm.part[0];
+#pragma unroll
+        for (int u = 1; u < NWARP; ++u) {
+          const Part o = sm.part[u];
+          // (ratio, tie) order of warp_argmin: IEEE compare (-0 == +0), then the smaller key
+          if (o.idx >= 0 && (q.idx < 0 || o.v < q.v || (o.v == q.v && o.tie < q.tie))) q = o;
+        }
+        if (q.idx < 0) { st = (phase == 2) ? ST_UNBOUNDED : ST_NUMERICAL; break; }
+        l = q.idx;
+        theta = q.v;
       }
 
       LPB_PROF_MARK(4)
-      // Step 3: pivot row / PE by the owners of row l
+      // Step 3 (Listing 1): the owners of row l publish the RAW row (position
+      // e carries 1, the leaving variable's column) and zero their copy; after barrier 2
+      // every thread divides its own positions by PE (one reciprocal, taken before the
+      // barrier), so no single warp holds the others on the divisions and the owner-only
+      // code stays a few stores per case.
       const double pe = colE[l];
       if (tid == 0) {
         const int lv = sm.bkey[l];
@@ -521,20 +535,8 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
 #define LPB_PROW(x)                                                                 \
   case x:                                                                           \
     if constexpr ((x) < A) {                                                        \
-      bool slow_any = false;                                                        \
-      double q[BC];                                                                 \
       _Pragma("unroll") for (int b = 0; b < BC; ++b) {                              \
-        const int p = tc + TC * b;                                                  \
-        bool sl;                                                                    \
-        q[b] = div_fast(p == e ? 1.0 : T[x][b], pe, sl);                            \
-        slow_any |= sl;                                                             \
-      }                                                                             \
-      if (slow_any) {                                                               \
-        _Pragma("unroll") for (int b = 0; b < BC; ++b)                              \
-          q[b] = __ddiv_rn(tc + TC * b == e ? 1.0 : T[x][b], pe);                   \
-      }                                                                             \
-      _Pragma("unroll") for (int b = 0; b < BC; ++b) {                              \
-        sm.prow[tc + TC * b] = q[b];                                                \
+        sm.prow[tc + TC * b] = (tc + TC * b == e) ? 1.0 : T[x][b];                  \
         T[x][b] = 0.0;                                                              \
       }                                                                             \
     }                                                                               \
@@ -543,39 +545,36 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
 #undef LPB_PROW
         if (AS > 0 && al >= A) {  // pivot row in SMEM
           const int s_ = al - A;
-          bool slow_any = false;
-          double q[BC];
 #pragma unroll
           for (int b = 0; b < BC; ++b) {
-            bool sl;
-            q[b] = div_fast(tc + TC * b == e ? 1.0 : ts(s_, b), pe, sl);
-            slow_any |= sl;
-          }
-          if (slow_any) {
-#pragma unroll
-            for (int b = 0; b < BC; ++b) q[b] = __ddiv_rn(tc + TC * b == e ? 1.0 : ts(s_, b), pe);
-          }
-#pragma unroll
-          for (int b = 0; b < BC; ++b) {
-            sm.prow[tc + TC * b] = q[b];
+            sm.prow[tc + TC * b] = (tc + TC * b == e) ? 1.0 : ts(s_, b);
             ts(s_, b) = 0.0;
           }
         }
-        if (tc == 0) {
-          bool sl;
-          const double q = div_fast(sm.rhs[l], pe, sl);
-          sm.prow_rhs = sl ? __ddiv_rn(sm.rhs[l], pe) : q;
-        }
       }
+      const double rpe = recip_of(pe);
+      const double rhs_l = sm.rhs[l];  // current: its lane applied the lazy update in Step 2b
       LPB_PROF_MARK(5)
       gsync<NT>();  // barrier 2
       LPB_PROF_MARK(6)
       {
-        const double prr = sm.prow_rhs;
         const int leaving = sm.leaving;
         double pv[BC];
+        bool slow_any = false;
 #pragma unroll
-        for (int b = 0; b < BC; ++b) pv[b] = sm.prow[tc + TC * b];
+        for (int b = 0; b < BC; ++b) {
+          bool sl;
+          pv[b] = div_with(sm.prow[tc + TC * b], pe, rpe, sl);
+          slow_any |= sl;
+        }
+        bool slr;
+        double prr = div_with(rhs_l, pe, rpe, slr);
+        if (slow_any || slr) {  // rare: outside div_with's fast range -> IEEE __ddiv_rn
+#pragma unroll
+          for (int b = 0; b < BC; ++b) pv[b] = __ddiv_rn(sm.prow[tc + TC * b], pe);
+          prr = __ddiv_rn(rhs_l, pe);
+        }
+        prr_prev = prr;
         const double f2 = -sm.fobj[par][0];
         const bool upd1 = TWO && phase == 1;
         const double f1 = TWO ? -sm.fobj[par][1] : 0.0;
@@ -638,9 +637,9 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
     // ---- extract (R10) ----
     gsync<NT>();
     if (st == ST_OPTIMAL && pend) {  // apply the last pending RHS update
-      const double prr = sm.prow_rhs;
       for (int i = tid; i < m; i += NT)
-        sm.rhs[i] = (i == l_prev) ? prr : __fma_rn(sm.fcol[par ^ 1][i], prr, sm.rhs[i]);
+        sm.rhs[i] = (i == l_prev) ? prr_prev
+                                  : __fma_rn(sm.fcol[par ^ 1][i], prr_prev, sm.rhs[i]);
     }
     if (tid == 0) {
       a.status[lp] = st;
