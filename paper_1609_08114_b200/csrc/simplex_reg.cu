@@ -285,6 +285,8 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
     double prr_prev = 0.0;  // RHS of the last pivot row (lazy RHS updates, R13)
     const uint64_t lpkey = RPC ? rpc_lp_key(a.rpc_seed, a.lp_base + lp) : 0ull;
     bool pend = false, drive = false;
+    bool pre = false;  // Step 1 of this pivot was computed at the end of the last update
+    int pre_wl = -1, pre_e = 0, pre_evar = 0;
     while (st < 0) {
       const bool bland = a.bland_K > 0 && stall >= a.bland_K;
       const bool p1 = TWO && phase == 1;
@@ -339,6 +341,18 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
         if (ql < 0) continue;  // redundant row: the artificial stays basic at 0
         e = __shfl_sync(FULL, q.idx, ql);
         evar = __shfl_sync(FULL, q.tie, ql);
+      } else if (pre) {  // Step 1 done at the end of the last update (same rule and order)
+        pre = false;
+        if (pre_wl < 0) {
+          if (phase == 2) { st = ST_OPTIMAL; break; }
+          if (z1 > a.eps_phase1 * fmax(1.0, binf)) { st = ST_INFEASIBLE; break; }
+          drive = true;  // phase-I optimum with w* ~ 0
+          dl = 0;
+          continue;
+        }
+        if (it1 + it2 >= a.max_iter) { st = ST_ITER_LIMIT; break; }
+        e = pre_e;
+        evar = pre_evar;
       } else {
         LPB_PROF_MARK(7)
         // Step 1: entering position from the replicated objective row (warp-local)
@@ -487,7 +501,7 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
               val = v > a.eps_piv;
               bool slow;
               ratio = div_fast(r, val ? v : 1.0, slow);
-              if (slow) ratio = __ddiv_rn(r, val ? v : 1.0);  // rare: outside the fast range
+              if (slow) ratio = ddiv_slow(r, val ? v : 1.0);  // rare: outside the fast range
               tie = bland ? sm.bkey[i] : i;
             }
           }
@@ -571,8 +585,8 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
         double prr = div_with(rhs_l, pe, rpe, slr);
         if (slow_any || slr) {  // rare: outside div_with's fast range -> IEEE __ddiv_rn
 #pragma unroll
-          for (int b = 0; b < BC; ++b) pv[b] = __ddiv_rn(sm.prow[tc + TC * b], pe);
-          prr = __ddiv_rn(rhs_l, pe);
+          for (int b = 0; b < BC; ++b) pv[b] = ddiv_slow(sm.prow[tc + TC * b], pe);
+          prr = ddiv_slow(rhs_l, pe);
         }
         prr_prev = prr;
         const double f2 = -sm.fobj[par][0];
@@ -609,16 +623,46 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
             Ts2[(s_ * BH + h) * NT] = v;
           }
         }
-        if (leaving < 0 && tc == etc) {  // an artificial left: position e is dead (rare)
-#define LPB_DEAD(x)                            \
-  case x:                                      \
-    if constexpr ((x) < BC) {                  \
-      d2[x] = neg_inf();                       \
-      if constexpr (TWO) d1[x] = neg_inf();    \
-    }                                          \
-    break;
-          switch (be) { LPB_CASES(LPB_DEAD) default: break; }
-#undef LPB_DEAD
+        if constexpr (TWO) {  // an artificial left: position e is dead (-inf), branch-free
+          const bool dead = leaving < 0 && tc == etc;
+#pragma unroll
+          for (int b = 0; b < BC; ++b) {
+            const bool z = dead && b == be;
+            d2[b] = z ? neg_inf() : d2[b];
+            d1[b] = z ? neg_inf() : d1[b];
+          }
+        }
+        // Step 1 of the NEXT pivot (Dantzig, no Bland), straight-line in the same block as the
+        // update's DFMAs so the compiler fills its latency chain with them; the loop head uses
+        // the result when the next pivot is an LPC pivot (pre).
+        if constexpr (!RPC) {
+          const bool p1n = TWO && phase == 1;
+          double bv = neg_inf();
+          int bb = 0;
+          unsigned bvar = 0xffffffffu;
+#pragma unroll
+          for (int b = 0; b < BC; ++b) {
+            const double v = p1n ? d1[TWO ? b : 0] : d2[b];
+            const unsigned var = (unsigned)sm.nbvar[tc + TC * b];
+            const bool take = v > bv || (v == bv && var < bvar);
+            bv = take ? v : bv;
+            bb = take ? b : bb;
+            bvar = take ? var : bvar;
+          }
+          const bool val = bv > a.eps_enter && (RPW == 1 || lane < TC);
+          const unsigned long long key = okey(bv);
+          // branch-free (value, variable) warp argmax: three REDUX steps
+          const unsigned hi = val ? (unsigned)(key >> 32) : 0u;
+          const unsigned mhi = __reduce_max_sync(FULL, hi);
+          const bool c1 = val && hi == mhi;
+          const unsigned lo = c1 ? (unsigned)key : 0u;
+          const unsigned mlo = __reduce_max_sync(FULL, lo);
+          const bool c2 = c1 && (unsigned)key == mlo;
+          const unsigned mt = __reduce_min_sync(FULL, c2 ? bvar : 0xffffffffu);
+          const unsigned win = __ballot_sync(FULL, c2 && bvar == mt);
+          pre_wl = win ? __ffs(win) - 1 : -1;
+          pre_e = __shfl_sync(FULL, tc + TC * bb, pre_wl & 31);
+          pre_evar = (int)__shfl_sync(FULL, bvar, pre_wl & 31);
         }
       }
       LPB_PROF_MARK(8)
@@ -627,10 +671,12 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
       par ^= 1;
       if (drive) {
         ++it1;
+        pre = false;
         gsync<NT>();  // the next drive-out scan reads bkey
       } else {
         if (phase == 1) ++it1; else ++it2;
         stall = (theta > 0.0) ? 0 : stall + 1;
+        pre = !RPC && !(a.bland_K > 0 && stall >= a.bland_K);
       }
     }
 
