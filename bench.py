@@ -76,6 +76,18 @@ def general_sample(name, n_lp):
     return A, b, c
 
 
+def traffic_per_launch(name, B):
+    """roofline.traffic: DRAM bytes (read + write) of the dominant kernel per launch, from the
+    committed ncu --set full capture of this config (profiles/traffic.json, per LP x B), or
+    None when the config has no capture."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            t = json.load(f)
+        return float(t[name]["dram_bytes_per_lp"]) * B
+    except Exception:
+        return None
+
+
 def peaks():
     p = {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0, "src": "fallback (B200_PROFILING.md)"}
     try:
@@ -301,7 +313,7 @@ def main():
         traffic_alg = B * (8 * n + 8 * n + 8 + 4)  # read l, write x, obj, status
         achieved = traffic_alg / (kmean / 1e3) / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": p["hbm_gbs"], "unit": "GB/s",
-                "frac": achieved / p["hbm_gbs"], "traffic": None,
+                "frac": achieved / p["hbm_gbs"], "traffic": traffic_per_launch(name, B),
                 "kernel": "hyperbox_kernel", "peak_src": p["src"],
                 "algorithmic_bytes_per_launch": traffic_alg}
         iters_mean = None
@@ -311,7 +323,8 @@ def main():
         flops = algorithmic_flops(iters, k, m, n)
         achieved = flops / (kmean / 1e3) / 1e12
         roof = {"bound": "alu", "achieved": achieved, "peak": p["fp64_tflops"],
-                "unit": "TFLOP/s", "frac": achieved / p["fp64_tflops"], "traffic": None,
+                "unit": "TFLOP/s", "frac": achieved / p["fp64_tflops"],
+                "traffic": traffic_per_launch(name, B),
                 "kernel": f"simplex ({klass} class)",
                 "peak_src": "FP64 unit count x clock: 148 SM x 64 DFMA/clk x 2 x "
                             f"{p['sm_max_mhz']:.0f} MHz (DESIGN.md)",

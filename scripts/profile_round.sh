@@ -1,16 +1,21 @@
 #!/bin/bash
-# Runs on the GPU box: bench lines for every config + ncu evidence (launch lists, full captures).
-# Usage: bash scripts/profile_round.sh <tag>
+# Runs on the GPU box: gpu tests, smoke, bench lines for every config + ncu evidence (launch
+# lists, full captures of the dominant kernels).  Usage: bash scripts/profile_round.sh <tag>
 TAG=${1:-r01}
 OUT=gpurun_out/$TAG
 mkdir -p $OUT
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $OUT/gpu.txt
-for cf in cfg2 cfg1 cfg4 cfg5; do
+timeout 1500 python -m pytest tests -m gpu -q > $OUT/pytest_gpu.txt 2>&1
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.txt 2>&1
+for cf in cfg2 cfg1 cfg4 cfg5 cfg2s cfg2r; do
   timeout 900 python bench.py --config $cf > $OUT/bench_$cf.json 2> $OUT/bench_$cf.err
 done
-timeout 900 python bench.py --config cfg3 --steps 2 --warmup 1 --e2e-steps 1 > $OUT/bench_cfg3.json 2> $OUT/bench_cfg3.err
-timeout 900 python bench.py --config cfg2s > $OUT/bench_cfg2s.json 2> $OUT/bench_cfg2s.err
-timeout 900 python bench.py --config cfg3s --steps 2 --warmup 1 --e2e-steps 1 > $OUT/bench_cfg3s.json 2> $OUT/bench_cfg3s.err
+for cf in cfg3 cfg3s; do
+  timeout 900 python bench.py --config $cf --steps 3 --warmup 3 --e2e-steps 1 > $OUT/bench_$cf.json 2> $OUT/bench_$cf.err
+done
+for cf in cfg6 cfg8 cfg7; do
+  timeout 900 python bench.py --config $cf --steps 3 --warmup 3 --e2e-steps 1 > $OUT/bench_$cf.json 2> $OUT/bench_$cf.err
+done
 timeout 300 python bench.py --impl reference --config cfg2 --steps 3 --warmup 1 > $OUT/ref_cfg2.json 2>&1
 # launch lists (cold-cache, serialised: compare shares, not absolutes)
 for cf in cfg2 cfg5 cfg1; do
