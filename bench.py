@@ -321,6 +321,14 @@ def main():
         iters = res["iters"].cpu().numpy()
         k = (np.broadcast_to(host_in[1], (B, m)) < 0).sum(axis=1)
         flops = algorithmic_flops(iters, k, m, n)
+        if sab and k[0] > 0 and klass in ("M", "L"):
+            # phase-I warm start (NEXT-1): phase I ran once for the polytope; every LP only
+            # replays its carried objective row through the recorded pivots (2 flop per
+            # element per pivot) -- count that, not B phase-I solves
+            W = n + float(k[0]) + 1
+            it1 = float(iters[0, 0])
+            flops -= float(np.sum(2.0 * W * iters[:, 0] * (m + 2)))
+            flops += 2.0 * W * it1 * (m + 2) + B * 2.0 * W * it1
         achieved = flops / (kmean / 1e3) / 1e12
         roof = {"bound": "alu", "achieved": achieved, "peak": p["fp64_tflops"],
                 "unit": "TFLOP/s", "frac": achieved / p["fp64_tflops"],

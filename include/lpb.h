@@ -111,6 +111,12 @@ typedef struct {
                           k = lp_index_base + position in the call): a rank solving LPs
                           [lo, hi) of a sharded batch passes lo and follows exactly the pivot
                           path of an unsharded run; default 0                                */
+  int32_t warm_start;  /* LPB_SHARED_AB batches with an infeasible slack basis (b has negative
+                          entries): phase I depends on A and b only, so by default (0) it is
+                          solved ONCE and every LP starts phase II from the recorded tableau,
+                          its carried objective row rebuilt by replaying the recorded pivots
+                          (bit-identical to solving each LP from scratch; M/L classes, LPC).
+                          -1: solve every LP from scratch                                     */
 } lpb_options;
 
 /* Entering rules (lpb_options.pivot_rule).

@@ -64,6 +64,11 @@ struct lpb_ctx {
   bool solved = false, last_nox = false, host_path = false;
   int last_launches = 0, last_class = 0, last_cluster = 0, last_grid = 0;
   long long* prof = nullptr;  // diagnostics: per-CTA phase counters (lpb_set_profile_buffer)
+  // phase-I record of a shared-constraint two-phase batch (warm start, NEXT-1)
+  double* rec_rows = nullptr;
+  double* rec_T = nullptr;
+  int* rec_ints = nullptr;  // rec_e[cap] | nbvar[n+kmax] | bkey[m] | info[4]
+  int rec_cap = 0, rec_W = 0;
   char err[256] = {0};
 };
 
@@ -96,6 +101,7 @@ extern "C" int lpb_default_options(lpb_options* o) {
   o->pivot_rule = LPB_RULE_LPC;
   o->rpc_seed = 0;
   o->lp_index_base = 0;
+  o->warm_start = 0;
   return LPB_OK;
 }
 
@@ -199,6 +205,9 @@ extern "C" int lpb_destroy(lpb_ctx* c) {
   cudaFree(c->d_c);
   cudaFree(c->d_ticket);
   cudaFree(c->d_kmax);
+  cudaFree(c->rec_rows);
+  cudaFree(c->rec_T);
+  cudaFree(c->rec_ints);
   if (c->h_kmax) cudaFreeHost(c->h_kmax);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
@@ -258,6 +267,10 @@ static void fill_args(const lpb_ctx* c, SimplexArgs& a, int64_t lp0, int64_t cnt
   a.bland_K = c->opt.bland_after == 0 ? n + m : c->opt.bland_after;
   a.kmax = kmax;
   a.ticket = ticket;
+  a.mode = 0;
+  a.rec_cap = 0;
+  a.rec_rows = a.rec_T = nullptr;
+  a.rec_e = a.rec_nbvar = a.rec_bkey = a.rec_info = nullptr;
   a.rpc = c->opt.pivot_rule == LPB_RULE_RPC ? 1 : 0;
   a.rpc_seed = c->opt.rpc_seed;
   a.lp_base = c->opt.lp_index_base + lp0;
@@ -323,6 +336,44 @@ static int run_general(lpb_ctx* c, cudaStream_t s, int64_t lp0, int64_t cnt, con
   } else if (klass == CLASS_T) {
     LPB_CUDA(c, launch_simplex_row(a, c->opt.grid_ctas, s, &ctas));
   } else {
+    // Shared constraints with an infeasible slack basis (LPB_SHARED_AB, k > 0): phase I
+    // depends on A and b only, so it is solved once (mode 1, LP 0) and every LP starts at
+    // phase II from that record (mode 2).  Under RPC the phase-I path
+    // depends on the LP index, so RPC batches take the cold path.
+    const bool warm = sab && kmax > 0 && c->opt.warm_start >= 0 &&
+                      c->opt.pivot_rule == LPB_RULE_LPC;
+    if (warm) {
+      const int W = c->n + kmax + 1;
+      const int cap = a.max_iter + c->m;
+      if (c->rec_cap < cap || c->rec_W < W) {
+        cudaFree(c->rec_rows);
+        cudaFree(c->rec_T);
+        cudaFree(c->rec_ints);
+        c->rec_rows = nullptr;
+        c->rec_T = nullptr;
+        c->rec_ints = nullptr;
+        c->rec_cap = c->rec_W = 0;
+        LPB_CUDA(c, cudaMalloc(&c->rec_rows, sizeof(double) * (size_t)cap * W));
+        LPB_CUDA(c, cudaMalloc(&c->rec_T, sizeof(double) * (size_t)c->m * W));
+        LPB_CUDA(c, cudaMalloc(&c->rec_ints, sizeof(int) * ((size_t)cap + W + c->m + 4)));
+        c->rec_cap = cap;
+        c->rec_W = W;
+      }
+      a.rec_cap = c->rec_cap;
+      a.rec_rows = c->rec_rows;
+      a.rec_T = c->rec_T;
+      a.rec_e = c->rec_ints;
+      a.rec_nbvar = c->rec_ints + c->rec_cap;
+      a.rec_bkey = a.rec_nbvar + W;
+      a.rec_info = a.rec_bkey + c->m;
+      SimplexArgs r = a;
+      r.mode = 1;
+      r.batch = 1;
+      LPB_CUDA(c, launch_simplex_block(cl, r, 0, s, &ctas));
+      LPB_CUDA(c, cudaMemsetAsync(ticket, 0, sizeof(int), s));
+      a.mode = 2;
+      *launches += 1;
+    }
     LPB_CUDA(c, launch_simplex_block(cl, a, c->opt.grid_ctas, s, &ctas));
   }
   if (timed) {

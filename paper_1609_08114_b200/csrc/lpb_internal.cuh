@@ -36,6 +36,18 @@ struct SimplexArgs {
   int rpc;           // Step 1 rule: 0 LPC (Dantzig), 1 RPC (include/lpb.h LPB_RULE_RPC)
   uint64_t rpc_seed;
   int64_t lp_base;   // index in the lpb_solve_batch call of this launch's LP 0 (RPC key)
+  // Phase-I warm start for shared-constraint two-phase batches (M/L classes; SURVEY §8(f)
+  // NEXT-1): phase I depends on A and b only, so it runs once (mode 1, LP 0) and records its
+  // pivot rows; mode 2 starts every LP at phase II from the recorded tableau, its carried
+  // phase-II row rebuilt by replaying the recorded pivots (the same fma sequence, bit-exact).
+  int mode;            // 0 normal, 1 record phase I of LP 0, 2 warm start from the record
+  int rec_cap;         // pivot rows the record can hold
+  double* rec_rows;    // [rec_cap][W] pivot rows / PE (W = n + kmax + 1: positions, RHS)
+  int* rec_e;          // [rec_cap] entering (global) position of each recorded pivot
+  double* rec_T;       // [m][W] constraint rows after phase I (positions, then RHS)
+  int* rec_nbvar;      // [n + kmax] position -> nonbasic variable (DEAD: left artificial)
+  int* rec_bkey;       // [m] row -> basic-variable key
+  int* rec_info;       // {status after phase I (-1: phase II follows), it1, pivots, k}
 };
 
 struct HyperboxArgs {

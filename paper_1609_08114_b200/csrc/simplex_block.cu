@@ -113,6 +113,7 @@ struct Smem {
   Rec* rec;       // 2 x CL proposals (parity-buffered), written by every CTA of the cluster
   double* colC;   // 2 x CL x RC proposal columns (parity-buffered)
   Ctl* ctl;
+  double* rbuf;   // 2 x (n + kmax + 1): phase-II row replay (warm start, mode 2)
 };
 
 template <int CL>
@@ -180,8 +181,17 @@ __device__ __forceinline__ Cand cluster_reduce(Cand c, const Smem& s, int& par,
 // the pivot row (fma(1, prow, 0)), the swapped column (fma(-f_i, rl, 0)) and every other
 // element -- no per-element branch.  Warps walk rows, lanes walk columns (conflict-free
 // SMEM rows, odd stride), the lane's prow values stay in registers.
+// rec (mode 1): the new pivot row is also written to the record, local column j at global
+// position g0 + j and the RHS (local column Wa - 1) at npos by rank 0.
+struct RecRow {
+  double* row;  // null: no recording
+  int g0, npos;
+  bool rank0;
+};
+
 __device__ __forceinline__ void pivot_local(const Smem& s, const double* colE, int S, int Wa,
-                                            int nrow, int l, bool own, int jloc, int ent_var) {
+                                            int nrow, int l, bool own, int jloc, int ent_var,
+                                            const RecRow& rec = RecRow{nullptr, 0, 0, false}) {
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const double pe = colE[l];
   const double rpe = recip_of(pe);
@@ -191,9 +201,13 @@ __device__ __forceinline__ void pivot_local(const Smem& s, const double* colE, i
     const double num = sw ? 1.0 : *tl;
     bool slow;
     double q = div_with(num, pe, rpe, slow);
-    if (slow) q = __ddiv_rn(num, pe);
+    if (slow) q = ddiv_slow(num, pe);
     s.prow[j] = q;
     *tl = 0.0;
+    if (rec.row) {
+      if (j < Wa - 1) rec.row[rec.g0 + j] = q;
+      else if (rec.rank0) rec.row[rec.npos] = q;
+    }
   }
   for (int i = tid; i < nrow; i += NT) {
     s.fcol[i] = (i == l) ? 1.0 : -colE[i];
@@ -279,6 +293,7 @@ __global__ void __launch_bounds__(NT) simplex_block_kernel(SimplexArgs a) {
   s.rec = reinterpret_cast<Rec*>(s.cslots + 2 * CL);
   s.colC = reinterpret_cast<double*>(s.rec + 2 * CL);
   s.ctl = reinterpret_cast<Ctl*>(s.colC + 2 * (PULL ? 1 : CL) * RC);
+  s.rbuf = reinterpret_cast<double*>(s.ctl + 1);
 
   int par = 0;
   for (;;) {
@@ -296,9 +311,10 @@ __global__ void __launch_bounds__(NT) simplex_block_kernel(SimplexArgs a) {
     const double* __restrict__ ck = a.c + lp * (int64_t)n;
 
     // ---- build (reading R7): negated rows, basis keys, |b|_inf ----
-    int k = 0;
+    const bool warm = a.mode == 2;
+    int k = warm ? a.rec_info[3] : 0;
     double binf = 0.0;
-    for (int base = 0; base < m; base += NT) {
+    for (int base = 0; base < (warm ? 0 : m); base += NT) {
       const int i = base + tid;
       const double bi = (i < m) ? __ldg(bk + i) : 0.0;
       const bool neg = (i < m) && (bi < 0.0);
@@ -332,8 +348,46 @@ __global__ void __launch_bounds__(NT) simplex_block_kernel(SimplexArgs a) {
     const int Wp = (Wa + 1) & ~1;                         // whole 128-bit pairs
     const int g0 = cl.rank * Q;
     if (k > a.kmax) st = ST_NUMERICAL;  // cannot happen: kmax comes from the prepass
+    const int npos = n + k, Wr = npos + 1;              // record row: positions, then RHS
+    int phase = (k > 0) ? 1 : 2;
 
-    if (st < 0) {
+    if (warm && st < 0) {
+      // Warm start (mode 2): phase I of this polytope was solved once (mode 1).  Terminal
+      // phase-I outcomes apply to every LP; otherwise load the recorded tableau and rebuild
+      // this LP's carried phase-II row by replaying the recorded pivots on c -- the same
+      // fma(-f, prow_j, T_mj) sequence phase I applies to it (R7, R13): bit-identical.
+      const int rst = a.rec_info[0];
+      it1 = a.rec_info[1];
+      if (rst >= 0) {
+        st = rst;
+      } else {
+        const int npiv = a.rec_info[2];
+        phase = 2;
+        for (int i = w; i < m; i += NW)
+          for (int j = lane; j < Wp; j += 32)
+            s.T[i * S + j] = (j < cnt) ? a.rec_T[(size_t)i * Wr + g0 + j]
+                                       : (j == cnt ? a.rec_T[(size_t)i * Wr + npos] : 0.0);
+        for (int j = tid; j < cnt; j += NT) s.nbvar[j] = a.rec_nbvar[g0 + j];
+        for (int i = tid; i < m; i += NT) s.bkey[i] = a.rec_bkey[i];
+        double* cur = s.rbuf;
+        double* nxt = s.rbuf + Wr;
+        for (int p = tid; p < Wr; p += NT) cur[p] = (p < n) ? __ldg(ck + p) : 0.0;
+        __syncthreads();
+        for (int t = 0; t < npiv; ++t) {
+          const int e = __ldg(a.rec_e + t);
+          const double f = cur[e];
+          const double* __restrict__ pr = a.rec_rows + (size_t)t * Wr;
+          for (int p = tid; p < Wr; p += NT) nxt[p] = __fma_rn(-f, __ldg(pr + p), p == e ? 0.0 : cur[p]);
+          double* tmp = cur;
+          cur = nxt;
+          nxt = tmp;
+          __syncthreads();
+        }
+        for (int j = tid; j < Wp; j += NT)
+          s.T[m * S + j] = (j < cnt) ? cur[g0 + j] : (j == cnt ? cur[npos] : 0.0);
+        __syncthreads();
+      }
+    } else if (st < 0) {
       for (int i = w; i < m; i += NW) {
         const bool neg = s.bkey[i] < 0;
         for (int j = lane; j < Wp; j += 32) {
@@ -370,7 +424,9 @@ __global__ void __launch_bounds__(NT) simplex_block_kernel(SimplexArgs a) {
     }
 
     // ---- Steps 1-3 loop, two phases ----
-    int phase = (k > 0) ? 1 : 2, stall = 0, pp = 0;
+    int stall = 0, pp = 0;
+    const bool record = a.mode == 1;  // record phase I (LP 0 only), then stop
+    bool recorded = false;
     while (st < 0) {
       const int objrow = (phase == 1) ? m + 1 : m;
       const int nrow = (phase == 1) ? m + 2 : m + 1;
@@ -400,7 +456,7 @@ __global__ void __launch_bounds__(NT) simplex_block_kernel(SimplexArgs a) {
           if (ai > a.eps_piv) {
             bool slow;
             double r = div_fast(s.T[i * S + cnt], ai, slow);
-            if (slow) r = __ddiv_rn(s.T[i * S + cnt], ai);
+            if (slow) r = ddiv_slow(s.T[i * S + cnt], ai);
             const Cand cc{r, bland ? s.bkey[i] : i, i};
             if (better<MIN_V>(cc, cr)) cr = cc;
           }
@@ -467,12 +523,36 @@ __global__ void __launch_bounds__(NT) simplex_block_kernel(SimplexArgs a) {
             }
           }
           cl.sync();
-          pivot_local(s, s.colE, S, Wa, m + 2, l, cl.rank == owner, jloc, cd.key);
+          RecRow rr{nullptr, g0, npos, cl.rank == 0};
+          if (record && it1 < a.rec_cap) {
+            rr.row = a.rec_rows + (size_t)it1 * Wr;
+            if (cl.rank == 0 && tid == 0) a.rec_e[it1] = cd.pos;
+          }
+          pivot_local(s, s.colE, S, Wa, m + 2, l, cl.rank == owner, jloc, cd.key, rr);
           ++it1;
         }
         phase = 2;
         stall = 0;
         pp ^= 1;  // the proposal slots of this round may still be read by a peer CTA
+        if (record) {  // phase I recorded: dump the tableau it leaves, then stop (mode 1)
+          for (int i = w; i < m; i += NW)
+            for (int j = lane; j < Wa; j += 32) {
+              if (j < cnt) a.rec_T[(size_t)i * Wr + g0 + j] = s.T[i * S + j];
+              else if (cl.rank == 0) a.rec_T[(size_t)i * Wr + npos] = s.T[i * S + cnt];
+            }
+          for (int j = tid; j < cnt; j += NT) a.rec_nbvar[g0 + j] = s.nbvar[j];
+          if (cl.rank == 0) {
+            for (int i = tid; i < m; i += NT) a.rec_bkey[i] = s.bkey[i];
+            if (tid == 0) {
+              a.rec_info[0] = it1 <= a.rec_cap ? -1 : ST_NUMERICAL;
+              a.rec_info[1] = it1;
+              a.rec_info[2] = it1;
+              a.rec_info[3] = k;
+            }
+          }
+          recorded = true;
+          break;
+        }
         continue;
       }
       if (it1 + it2 >= a.max_iter) { st = ST_ITER_LIMIT; break; }
@@ -483,12 +563,28 @@ __global__ void __launch_bounds__(NT) simplex_block_kernel(SimplexArgs a) {
       const int jloc = ce.pos - win * Q;
       const double* wcol = PULL ? cl.remote(s.colC + (size_t)pp * RC, win)
                                 : s.colC + (size_t)(pp * CL + win) * RC;
-      pivot_local(s, wcol, S, Wa, nrow, l, cl.rank == win, jloc, ce.key);
+      RecRow rr{nullptr, g0, npos, cl.rank == 0};
+      if (record && phase == 1 && it1 < a.rec_cap) {
+        rr.row = a.rec_rows + (size_t)it1 * Wr;
+        if (cl.rank == 0 && tid == 0) a.rec_e[it1] = ce.pos;
+      }
+      pivot_local(s, wcol, S, Wa, nrow, l, cl.rank == win, jloc, ce.key, rr);
       pp ^= 1;
       if (phase == 1) ++it1; else ++it2;
       stall = (theta > 0.0) ? 0 : stall + 1;
     }
 
+    if (record) {  // mode 1: no result for LP 0 here (the warm pass solves it); a phase-I
+                   // outcome that ends every LP (INFEASIBLE, NUMERICAL, ITER_LIMIT) is recorded
+      if (!recorded && cl.rank == 0 && tid == 0) {
+        a.rec_info[0] = st;
+        a.rec_info[1] = it1;
+        a.rec_info[2] = 0;
+        a.rec_info[3] = k;
+      }
+      cl.sync();
+      continue;
+    }
     // ---- extract (R10) ----
     if (cl.rank == 0) {
       if (tid == 0) {
@@ -527,6 +623,7 @@ size_t block_smem_bytes(int cl, int m, int n, int kmax) {
   const size_t ncol = cl >= 8 ? 1 : (size_t)cl;  // proposal columns per parity (PUSH: cl)
   bytes += sizeof(Cand) * (2 * NW + 2 * cl) + sizeof(Rec) * 2 * cl +
            sizeof(double) * 2 * ncol * (m + 2) + sizeof(Ctl);
+  bytes += sizeof(double) * 2 * ((size_t)n + kmax + 1);  // warm-start replay buffer
   return bytes;
 }
 

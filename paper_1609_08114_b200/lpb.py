@@ -50,6 +50,7 @@ class Options(ctypes.Structure):
         ("pivot_rule", ctypes.c_int32),
         ("rpc_seed", ctypes.c_uint64),
         ("lp_index_base", ctypes.c_int64),
+        ("warm_start", ctypes.c_int32),
     ]
 
 

@@ -109,3 +109,62 @@ def test_rpc_lp_index_base_reproduces_unsharded_paths():
                       lp_index_base=lo)
         sl = {k: v[lo:hi] for k, v in o.items() if isinstance(v, np.ndarray)}
         compare(A[lo:hi], b[lo:hi], c[lo:hi], g, sl)
+
+
+# ---------------- NEXT-1: phase-I warm start of shared-constraint two-phase batches ----------
+
+def _shared(kind, B, m, n, seed):
+    g = lpgen.rng(seed)
+    if kind == "G2":
+        A, b, _ = lpgen.twophase_signed(1, m, n, seed)
+    elif kind == "deg":  # degenerate pivots, Bland mode, artificial drive-outs
+        A, b, _ = lpgen.degenerate(1, m, n, seed, negative_b=True)
+    elif kind == "infeasible":  # x1 <= -1 style rows: phase I ends with w* > 0
+        A, b, _ = lpgen.status_mix(1, m, n, seed, infeasible_start=True)
+        A[0, 0, :] = np.abs(A[0, 0, :])
+        b[0, 0] = -5.0
+    else:
+        A, b, _ = lpgen.status_mix(1, m, n, seed, infeasible_start=True)
+    c = g.uniform(-10.0, 10.0, size=(B, n))
+    return A[0], b[0], c
+
+
+@pytest.mark.parametrize("klass,cl", [("M", 0), ("L", 0), ("L", 8)])
+@pytest.mark.parametrize("kind,m,n,B", [("G2", 60, 60, 300), ("deg", 12, 12, 800),
+                                        ("mix", 20, 20, 500), ("infeasible", 10, 10, 200),
+                                        ("G2", 200, 200, 20)])
+def test_warm_start_shared_two_phase(klass, cl, kind, m, n, B):
+    A, b, c = _shared(kind, B, m, n, 7 + m)
+    if not np.any(b < 0):
+        pytest.skip("no infeasible row drawn")
+    if klass == "M" and m >= 200:
+        pytest.skip("200x200 two-phase needs the cluster class")
+    Ab = np.ascontiguousarray(np.broadcast_to(A, (B, m, n)))
+    bb = np.ascontiguousarray(np.broadcast_to(b, (B, m)))
+    kw = dict(bland_after=2) if kind == "deg" else {}
+    o = oracle.solve(Ab, bb, c, **kw)
+    opts = dict(kernel_class=klass, **kw)
+    if cl:
+        opts["cluster_ctas"] = cl
+    warm = gpu_solve(A, b, c, **opts)
+    assert warm["launch"]["launches"] >= 2  # the phase-I record pass ran
+    compare(Ab, bb, c, warm, o)
+    cold = gpu_solve(A, b, c, warm_start=-1, **opts)
+    for key in ("status", "iters"):
+        assert np.array_equal(warm[key], cold[key])
+    assert np.array_equal(warm["obj"], cold["obj"], equal_nan=True)
+    assert np.array_equal(warm["x"], cold["x"], equal_nan=True)
+    gh = gpu_solve(A, b, c, path="host", n_chunks=3, **opts)  # record once, chunks reuse it
+    compare(Ab, bb, c, gh, o)
+    if kind == "infeasible":
+        assert np.all(o["status"] == oracle.INFEASIBLE)
+
+
+def test_warm_start_iteration_limit_in_phase_one():
+    A, b, c = _shared("G2", 300, 40, 40, 3)
+    Ab = np.ascontiguousarray(np.broadcast_to(A, (300, 40, 40)))
+    bb = np.ascontiguousarray(np.broadcast_to(b, (300, 40)))
+    o = oracle.solve(Ab, bb, c, max_iter=5)
+    g = gpu_solve(A, b, c, kernel_class="M", max_iter=5)
+    compare(Ab, bb, c, g, o)
+    assert np.all(g["status"] == oracle.ITER_LIMIT)
