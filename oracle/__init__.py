@@ -33,6 +33,7 @@ class OracleOpts(ctypes.Structure):
         ("bland_after", ctypes.c_int),
         ("pivot_rule", ctypes.c_int),
         ("rpc_seed", ctypes.c_uint64),
+        ("lp_base", ctypes.c_int64),
     ]
 
 
@@ -79,9 +80,10 @@ RULES = {"LPC": 0, "RPC": 1}  # Step 1 entering rules
 
 
 def solve(A, b, c, *, eps_enter=1e-9, eps_piv=1e-9, eps_phase1=1e-9, max_iter=0,
-          bland_after=0, pivot_rule="LPC", rpc_seed=0, threads=None, certs=False):
-    """Solve a batch: A [B,m,n], b [B,m], c [B,n] (fp64); LP k of the batch is LP index k
-    of the RPC stream (pivot_rule="RPC", reading R15).  Returns a dict with
+          bland_after=0, pivot_rule="LPC", rpc_seed=0, lp_index_base=0, threads=None,
+          certs=False):
+    """Solve a batch: A [B,m,n], b [B,m], c [B,n] (fp64); LP k of the batch is LP index
+    lp_index_base + k of the RPC stream (pivot_rule="RPC", reading R15).  Returns a dict with
     status int32[B], obj f64[B], x f64[B,n], iters int32[B,2] and, with ``certs``,
     y f64[B,m], ray f64[B,n] and the terminal basic point xb f64[B,n],
     plus ``threads`` actually used."""
@@ -95,7 +97,7 @@ def solve(A, b, c, *, eps_enter=1e-9, eps_piv=1e-9, eps_phase1=1e-9, max_iter=0,
     assert b.shape == (B, m) and c.shape == (B, n)
     rule = RULES[pivot_rule.upper()] if isinstance(pivot_rule, str) else int(pivot_rule)
     o = OracleOpts(eps_enter, eps_piv, eps_phase1, int(max_iter), int(bland_after), rule,
-                   int(rpc_seed) & 0xFFFFFFFFFFFFFFFF)
+                   int(rpc_seed) & 0xFFFFFFFFFFFFFFFF, int(lp_index_base))
     status = np.empty(B, np.int32)
     obj = np.empty(B, np.float64)
     x = np.empty((B, n), np.float64)

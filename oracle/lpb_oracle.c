@@ -41,6 +41,7 @@ typedef struct {
   int bland_after;    /* 0 -> n+m ; < 0 -> never (pure Dantzig) (R6)                       */
   int pivot_rule;     /* 0 LPC, 1 RPC (reading R15)             */
   uint64_t rpc_seed;  /* RPC: seed of the counter-based choice (R15)                          */
+  int64_t lp_base;    /* RPC: the batch's LP k is LP lp_base + k of the caller's numbering     */
 } oracle_opts;
 
 /* One LP's full tableau.  Rows 0..m-1 constraints, row m the phase-II (original objective)
@@ -335,7 +336,7 @@ static void* batch_worker(void* arg) {
     if (k >= j->batch) break;
     const size_t mn = (size_t)j->m * (size_t)j->n;
     oracle_solve_lp(j->m, j->n, j->A + (size_t)k * mn, j->b + (size_t)k * j->m,
-                    j->c + (size_t)k * j->n, j->o, k, j->status + k, j->obj + k,
+                    j->c + (size_t)k * j->n, j->o, j->o->lp_base + k, j->status + k, j->obj + k,
                     j->x + (size_t)k * j->n, j->iters + 2 * k,
                     j->y ? j->y + (size_t)k * j->m : NULL,
                     j->ray ? j->ray + (size_t)k * j->n : NULL,

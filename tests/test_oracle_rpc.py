@@ -132,3 +132,14 @@ def test_lpc_fewer_iterations_than_rpc_on_average():
     lpc = oracle.solve(A, b, c)["iters"][:, 1].mean()
     rpc = oracle.solve(A, b, c, pivot_rule="RPC", rpc_seed=1)["iters"][:, 1].mean()
     assert rpc > 1.2 * lpc, (lpc, rpc)
+
+
+def test_rpc_lp_index_base_selects_the_stream():
+    """lp_index_base = k makes a one-LP batch follow LP k's draws in a larger batch."""
+    A, b, c = lpgen.signed_bounded(40, 12, 12, 51)
+    full = oracle.solve(A, b, c, pivot_rule="RPC", rpc_seed=8)
+    for k in (0, 7, 39):
+        one = oracle.solve(A[k:k + 1], b[k:k + 1], c[k:k + 1], pivot_rule="RPC", rpc_seed=8,
+                           lp_index_base=k)
+        assert np.array_equal(one["iters"][0], full["iters"][k])
+        assert one["obj"][0] == full["obj"][k] and np.array_equal(one["x"][0], full["x"][k])
