@@ -275,8 +275,10 @@ def main():
     if in_bytes <= 2 * L2_BYTES:  # small inputs: flush L2 between timed steps
         flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
 
-    def step():
-        solver.solve_device(d_A, d_b, d_c, shared_box=hyper, shared_ab=sab)
+    def step(timing=False):
+        # timed steps record no library events (each is GPU work between back-to-back
+        # solves); the kernel-time pass below turns them on
+        solver.solve_device(d_A, d_b, d_c, shared_box=hyper, shared_ab=sab, timing=timing)
 
     for _ in range(args.warmup):
         step()
@@ -294,12 +296,19 @@ def main():
             ev[i][0].record()
             step()
             ev[i][1].record()
-            nl, klass = solver.launch_info()
+            nl, klass = solver.launch_info()  # host-side fields: no synchronisation
             launches += nl
-            kern_ms.append(solver.kernel_ms())
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
+    # the dominant kernel's own duration (device events around it inside the library), read
+    # after each of a few extra, untimed steps: reading it synchronises, so it stays out of
+    # the timed loop (whose steps are issued back to back, as a user's would be)
+    for i in range(min(args.steps, 5)):
+        if flush is not None:
+            flush.fill_(float(i))
+        step(timing=True)
+        kern_ms.append(solver.kernel_ms())
     step_ms = [a.elapsed_time(b_) for a, b_ in ev]
     my_ms = float(sum(step_ms))
     tot_ms = lpdist.max_over_ranks(my_ms, device=torch.device("cuda", local))

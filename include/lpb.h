@@ -75,10 +75,13 @@ enum { /* lpb_solve_batch flags */
   LPB_SHARED_BOX = 2u,  /* hyperbox: one box (2n entries of b) for the whole batch             */
   LPB_NO_X = 4u,        /* do not produce x (saves 8n bytes per LP of HBM / D2H traffic)       */
   LPB_ASYNC = 8u,       /* enqueue only; do not synchronize before returning                   */
-  LPB_SHARED_AB = 16u   /* general LPs: one constraint system (A: m x n, b: m) for the whole
+  LPB_SHARED_AB = 16u,  /* general LPs: one constraint system (A: m x n, b: m) for the whole
                            batch, only c varies per LP -- many objectives over one polytope,
                            the support-function sampling of PAPER.md:313,330 (SURVEY §8(f)
                            NEXT-1); A and b are read with stride 0                            */
+  LPB_NO_TIMING = 32u   /* device-pointer solves: record no timing events (lpb_last_timing /
+                           lpb_last_kernel_timing then return LPB_ESTATE).  For back-to-back
+                           solves timed by the caller: each event record is GPU work        */
 };
 
 typedef struct {

@@ -61,6 +61,7 @@ struct lpb_ctx {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   cudaEvent_t kev0 = nullptr, kev1 = nullptr;  // around the dominant (solve) kernel
   bool kev_valid = false;
+  bool no_timing = false, timing_valid = false;  // LPB_NO_TIMING on the last solve
   bool solved = false, last_nox = false, host_path = false;
   int last_launches = 0, last_class = 0, last_cluster = 0, last_grid = 0;
   long long* prof = nullptr;  // diagnostics: per-CTA phase counters (lpb_set_profile_buffer)
@@ -299,7 +300,7 @@ static int run_general(lpb_ctx* c, cudaStream_t s, int64_t lp0, int64_t cnt, con
     if (!thread_fits(c->m, c->n)) return LPB_ETOOBIG;
     SimplexArgs a;  // worst-case width reserved: no prepass
     fill_args(c, a, lp0, cnt, A, b, cv, nox, c->m, ticket, sab);
-    const bool timed = (s == c->stream);
+    const bool timed = (s == c->stream) && !c->no_timing;
     if (timed) LPB_CUDA(c, cudaEventRecord(c->kev0, s));
     LPB_CUDA(c, launch_simplex_thread(a, s));
     if (timed) {
@@ -327,9 +328,8 @@ static int run_general(lpb_ctx* c, cudaStream_t s, int64_t lp0, int64_t cnt, con
   if (klass < 0) return LPB_ETOOBIG;
   SimplexArgs a;
   fill_args(c, a, lp0, cnt, A, b, cv, nox, kmax, ticket, sab);
-  LPB_CUDA(c, cudaMemsetAsync(ticket, 0, sizeof(int), s));
   int ctas = 0;
-  const bool timed = (s == c->stream);
+  const bool timed = (s == c->stream) && !c->no_timing;
   if (timed) LPB_CUDA(c, cudaEventRecord(c->kev0, s));
   if (klass == CLASS_R) {
     LPB_CUDA(c, launch_simplex_reg(a, c->opt.grid_ctas, s, &ctas));
@@ -370,7 +370,6 @@ static int run_general(lpb_ctx* c, cudaStream_t s, int64_t lp0, int64_t cnt, con
       r.mode = 1;
       r.batch = 1;
       LPB_CUDA(c, launch_simplex_block(cl, r, 0, s, &ctas));
-      LPB_CUDA(c, cudaMemsetAsync(ticket, 0, sizeof(int), s));
       a.mode = 2;
       *launches += 1;
     }
@@ -398,7 +397,7 @@ static int run_hyperbox(lpb_ctx* c, cudaStream_t s, int64_t lp0, int64_t cnt, co
   h.status = c->d_status + lp0;
   h.obj = c->d_obj + lp0;
   h.x = nox ? nullptr : c->d_x + lp0 * c->n;
-  const bool timed = (s == c->stream);
+  const bool timed = (s == c->stream) && !c->no_timing;
   if (timed) LPB_CUDA(c, cudaEventRecord(c->kev0, s));
   LPB_CUDA(c, launch_hyperbox(h, s));
   if (timed) {
@@ -447,6 +446,8 @@ static int solve_impl(lpb_ctx* c, const double* A, const double* b, const double
   LPB_CUDA(c, cudaSetDevice(c->device));
   c->solved = false;
   c->kev_valid = false;
+  c->no_timing = (flags & LPB_NO_TIMING) && (flags & LPB_DEVICE_PTRS);
+  c->timing_valid = true;
   c->last_launches = 0;
   c->last_nox = nox;
   const int64_t B = c->batch;
@@ -454,12 +455,13 @@ static int solve_impl(lpb_ctx* c, const double* A, const double* b, const double
 
   if (flags & LPB_DEVICE_PTRS) {
     c->host_path = false;
-    LPB_CUDA(c, cudaEventRecord(c->ev0, c->stream));
+    if (!c->no_timing) LPB_CUDA(c, cudaEventRecord(c->ev0, c->stream));
     int rc = general ? run_general(c, c->stream, 0, B, A, b, cv, nox, sab, -1, c->d_ticket,
                                    &c->last_launches)
                      : run_hyperbox(c, c->stream, 0, B, cv, b, shared, nox, &c->last_launches);
     if (rc != LPB_OK) return rc;
-    LPB_CUDA(c, cudaEventRecord(c->ev1, c->stream));
+    if (!c->no_timing) LPB_CUDA(c, cudaEventRecord(c->ev1, c->stream));
+    c->timing_valid = !c->no_timing;
     if (o_status) LPB_CUDA(c, cudaMemcpyAsync(o_status, c->d_status, 4 * B, cudaMemcpyDefault, c->stream));
     if (o_obj) LPB_CUDA(c, cudaMemcpyAsync(o_obj, c->d_obj, 8 * B, cudaMemcpyDefault, c->stream));
     if (o_x) LPB_CUDA(c, cudaMemcpyAsync(o_x, c->d_x, 8 * B * (int64_t)n, cudaMemcpyDefault, c->stream));
@@ -584,7 +586,7 @@ extern "C" int lpb_sync(lpb_ctx* c) {
 
 extern "C" int lpb_last_timing(lpb_ctx* c, double* solve_ms, double* e2e_ms) {
   if (!c) return LPB_EINVAL;
-  if (!c->solved) return LPB_ESTATE;
+  if (!c->solved || !c->timing_valid) return LPB_ESTATE;
   LPB_CUDA(c, cudaSetDevice(c->device));
   LPB_CUDA(c, cudaEventSynchronize(c->ev1));
   float ms = 0.f;

@@ -688,6 +688,8 @@ static cudaError_t launch_cl(const SimplexArgs& a, int grid_override, cudaStream
   if (grid < CL) grid = CL;
   cfg.gridDim = dim3(grid);
   if (ctas_out) *ctas_out = grid;
+  const cudaError_t e = cudaMemsetAsync(a.ticket, 0, sizeof(int), s);  // persistent LP ticket
+  if (e != cudaSuccess) return e;
   return cudaLaunchKernelEx(&cfg, simplex_block_kernel<CL>, a);
 }
 

@@ -26,7 +26,7 @@ _lib = ctypes.CDLL(LIB_PATH)
 GENERAL, HYPERBOX = 0, 1
 OPTIMAL, UNBOUNDED, INFEASIBLE, ITER_LIMIT, NUMERICAL = range(5)
 OK, EINVAL, ENOMEM, ECUDA, ESTATE, ETOOBIG = 0, -1, -2, -3, -4, -5
-DEVICE_PTRS, SHARED_BOX, NO_X, ASYNC, SHARED_AB = 1, 2, 4, 8, 16
+DEVICE_PTRS, SHARED_BOX, NO_X, ASYNC, SHARED_AB, NO_TIMING = 1, 2, 4, 8, 16, 32
 CLASS_NAMES = {0: "auto", 1: "S", 2: "M", 3: "L", 4: "R", 5: "H", 6: "T"}
 CLASS_IDS = {v: k for k, v in CLASS_NAMES.items()}
 RULE_LPC, RULE_RPC = 0, 1  # lpb_options.pivot_rule
@@ -184,7 +184,7 @@ class Solver:
 
     # -- solves --
     def solve_device(self, A, b, c, *, shared_box=False, shared_ab=False, want_x=True,
-                     sync=False):
+                     sync=False, timing=True):
         """Device tensors in; results stay in the context's device buffers (see
         ``device_results``).  Asynchronous on the context's stream unless ``sync``.
         ``shared_ab``: A (m x n) and b (m) are one constraint system for the whole batch."""
@@ -192,6 +192,8 @@ class Solver:
                  (SHARED_AB if shared_ab else 0))
         if not sync:
             flags |= ASYNC
+        if not timing:
+            flags |= NO_TIMING
         _check(_lib.lpb_solve_batch(self._ctx, _dptr(A), _dptr(b), _dptr(c), flags), self._ctx)
 
     def solve_host_into(self, A, b, c, status, obj, x=None, iters=None, *, shared_box=False,

@@ -76,6 +76,7 @@ def test_binding_enums_match_header():
         name = k[4:]
         if hasattr(lpb, name):
             assert getattr(lpb, name) == v, k
-    for k in ("DEVICE_PTRS", "SHARED_BOX", "NO_X", "ASYNC", "SHARED_AB", "GENERAL", "HYPERBOX",
+    for k in ("DEVICE_PTRS", "SHARED_BOX", "NO_X", "ASYNC", "SHARED_AB", "NO_TIMING", "GENERAL",
+              "HYPERBOX", "RULE_LPC", "RULE_RPC",
               "OPTIMAL", "UNBOUNDED", "INFEASIBLE", "ITER_LIMIT", "NUMERICAL"):
         assert getattr(lpb, k) == consts["LPB_" + k], k
