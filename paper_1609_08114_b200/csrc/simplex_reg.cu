@@ -459,6 +459,8 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
         sm.fobj[par][0] = d2[x];                                                      \
         if constexpr (TWO) sm.fobj[par][1] = d1[x];                                   \
       }                                                                               \
+      d2[x] = 0.0;                                                                    \
+      if constexpr (TWO) d1[x] = 0.0;                                                 \
     }                                                                                 \
     break;
         switch (be) { LPB_CASES(LPB_PUB) default: break; }
@@ -468,15 +470,6 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
           double& t = ts(s_, be);
           colE[tr + TR * (A + s_)] = t;
           t = 0.0;
-        }
-      }
-      {  // the objective replicas of position e restart from 0 (branch-free, owner column)
-        const bool mine = tc == etc;
-#pragma unroll
-        for (int b = 0; b < BC; ++b) {
-          const bool z = mine && b == be;
-          d2[b] = z ? 0.0 : d2[b];
-          if constexpr (TWO) d1[b] = z ? 0.0 : d1[b];
         }
       }
       __syncwarp();
