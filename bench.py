@@ -136,6 +136,11 @@ class ClockSampler:
         if self.ok:
             self.t = threading.Thread(target=self._run, daemon=True)
             self.t.start()
+            # the first NVML queries are slow and hold driver locks: let them finish before
+            # the timed region starts (short timed regions would otherwise absorb them)
+            deadline = time.time() + 1.0
+            while not self.samples and time.time() < deadline:
+                time.sleep(0.001)
         return self
 
     def __exit__(self, *a):
