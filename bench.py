@@ -323,6 +323,7 @@ def main():
     # roofline of the dominant kernel (per launch, averaged over the timed launches)
     res = solver.device_results(want_x=True)
     p = peaks()
+    roof_smem = None
     if hyper:
         traffic_alg = B * (8 * n + 8 * n + 8 + 4)  # read l, write x, obj, status
         achieved = traffic_alg / (kmean / 1e3) / 1e9
@@ -351,6 +352,15 @@ def main():
                 "peak_src": "FP64 unit count x clock: 148 SM x 64 DFMA/clk x 2 x "
                             f"{p['sm_max_mhz']:.0f} MHz (DESIGN.md)",
                 "algorithmic_flops_per_launch": flops}
+        if klass in ("M", "L"):
+            # SMEM-resident tableau (SURVEY §8(d) "%SMEM"): every updated element is one 8-byte
+            # SMEM read + one write; peak = 148 SMs x 128 B/clk (one shared wavefront per
+            # clock, ncu's l1tex__data_pipe_lsu_wavefronts_mem_shared model) x max SM clock
+            smem_peak = 148 * 128 * p["sm_max_mhz"] * 1e6 / 1e9
+            smem_ach = 16.0 * (flops / 2.0) / (kmean / 1e3) / 1e9
+            roof_smem = {"bound": "smem", "achieved": smem_ach, "peak": smem_peak,
+                         "unit": "GB/s", "frac": smem_ach / smem_peak,
+                         "algorithmic_bytes_per_launch": 16.0 * flops / 2.0}
         iters_mean = iters.mean(axis=0).tolist()
         st = res["status"].cpu().numpy()
 
@@ -401,6 +411,7 @@ def main():
                        "ctas_per_lp": solver.launch_shape()[0],
                        "pivot_rule": lpgen.CONFIGS[name].get("rule", "LPC")},
             "roofline": roof,
+            **({"roofline_smem": roof_smem} if roof_smem else {}),
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,

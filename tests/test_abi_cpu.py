@@ -80,3 +80,16 @@ def test_binding_enums_match_header():
               "HYPERBOX", "RULE_LPC", "RULE_RPC",
               "OPTIMAL", "UNBOUNDED", "INFEASIBLE", "ITER_LIMIT", "NUMERICAL"):
         assert getattr(lpb, k) == consts["LPB_" + k], k
+
+
+def test_option_validation_without_gpu(lib):
+    """Undefined entering rules and cluster sizes are LPB_EINVAL at create (include/lpb.h)."""
+    from paper_1609_08114_b200 import lpb
+    ctx = ctypes.c_void_p()
+    for kw in (dict(pivot_rule=2), dict(pivot_rule=-1), dict(cluster_ctas=3),
+               dict(cluster_ctas=32), dict(eps_enter=-1.0)):
+        o = lpb.default_options(**kw)
+        assert lib.lpb_create(ctypes.byref(ctx), 10, 5, 5, 0, ctypes.byref(o)) == -1, kw
+    o = lpb.default_options()
+    o.struct_size = 8  # an older / foreign layout
+    assert lib.lpb_create(ctypes.byref(ctx), 10, 5, 5, 0, ctypes.byref(o)) == -1
