@@ -366,7 +366,7 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
           val = false;
           bvar = 0xffffffffu;
           const uint64_t pkey = rpc_pivot_key(lpkey, it1 + it2);
-#pragma unroll 1
+#pragma unroll
           for (int b = 0; b < BC; ++b) {
             const double v = p1 ? d1[TWO ? b : 0] : d2[b];
             if (v > a.eps_enter) {
@@ -625,26 +625,39 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
             d1[b] = z ? neg_inf() : d1[b];
           }
         }
-        // Step 1 of the NEXT pivot (Dantzig, no Bland), straight-line in the same block as the
-        // update's DFMAs so the compiler fills its latency chain with them; the loop head uses
-        // the result when the next pivot is an LPC pivot (pre).
-        if constexpr (!RPC) {
+        // Step 1 of the NEXT pivot (LPC or RPC, no Bland), straight-line in the same block as
+        // the update's DFMAs so the compiler fills its latency chain with them; the loop head
+        // uses the result when the next pivot is not a Bland pivot (pre).
+        {
           const bool p1n = TWO && phase == 1;
+          // RPC: the next pivot's draw is keyed on the pivot count after this pivot
+          const uint64_t pkey = RPC ? rpc_pivot_key(lpkey, it1 + it2 + 1) : 0ull;
           double bv = neg_inf();
+          unsigned long long bu = 0ull;
+          bool bval = false;
           int bb = 0;
           unsigned bvar = 0xffffffffu;
 #pragma unroll
           for (int b = 0; b < BC; ++b) {
             const double v = p1n ? d1[TWO ? b : 0] : d2[b];
             const unsigned var = (unsigned)sm.nbvar[tc + TC * b];
-            const bool take = v > bv || (v == bv && var < bvar);
-            bv = take ? v : bv;
+            bool take;
+            if constexpr (RPC) {
+              const bool cand = v > a.eps_enter;
+              const unsigned long long u = rpc_score(pkey, (int)var);
+              take = cand && (!bval || u > bu || (u == bu && var < bvar));
+              bu = take ? u : bu;
+              bval = bval || cand;
+            } else {
+              take = v > bv || (v == bv && var < bvar);
+              bv = take ? v : bv;
+            }
             bb = take ? b : bb;
             bvar = take ? var : bvar;
           }
-          const bool val = bv > a.eps_enter && (RPW == 1 || lane < TC);
-          const unsigned long long key = okey(bv);
-          // branch-free (value, variable) warp argmax: three REDUX steps
+          const bool val = (RPC ? bval : bv > a.eps_enter) && (RPW == 1 || lane < TC);
+          const unsigned long long key = RPC ? bu : okey(bv);
+          // branch-free (key, variable) warp argmax: three REDUX steps
           const unsigned hi = val ? (unsigned)(key >> 32) : 0u;
           const unsigned mhi = __reduce_max_sync(FULL, hi);
           const bool c1 = val && hi == mhi;
@@ -669,7 +682,7 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
       } else {
         if (phase == 1) ++it1; else ++it2;
         stall = (theta > 0.0) ? 0 : stall + 1;
-        pre = !RPC && !(a.bland_K > 0 && stall >= a.bland_K);
+        pre = !(a.bland_K > 0 && stall >= a.bland_K);
       }
     }
 
