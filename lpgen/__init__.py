@@ -129,25 +129,49 @@ def oct_directions(n: int) -> np.ndarray:
     return np.concatenate(out, axis=0)
 
 
-def hyperbox(B: int, n: int, seed: int):
-    """G3 (type-3 workload; SURVEY §8(d)).  One shared box (PAPER.md:313, 672) and B
-    directions.  n=5: the five-dimensional benchmark's initial set, a box centred at
-    (1,0,0,0,0) with side 0.02 (reading C16).  Other n: lo ~ U[-1,0),
-    hi = lo + U[0.01,1).  Directions: the oct template first, then row-normalised
-    standard normals.  Returns (lo, hi, dirs)."""
-    g = rng(seed)
+# directions beyond the template come in blocks of HB_BLOCK rows, block q drawn from its own
+# stream PCG64([seed, 2, q]): any contiguous shard of a batch is generated without drawing the
+# rest (multi-GPU ranks each draw only their slice of a 6M x 28 batch)
+HB_BLOCK = 1 << 16
+
+
+def hyperbox_box(n: int, seed: int):
+    """The shared box of G3: n=5 is the five-dimensional benchmark's initial set, a box
+    centred at (1,0,0,0,0) with side 0.02 (reading R14); other n:
+    lo ~ U[-1,0), hi = lo + U[0.01,1) from PCG64(seed)."""
     if n == 5:
         lo = np.array([0.99, -0.01, -0.01, -0.01, -0.01])
-        hi = lo + 0.02
-    else:
-        lo = g.uniform(-1.0, 0.0, size=n)
-        hi = lo + g.uniform(0.01, 1.0, size=n)
+        return lo, lo + 0.02
+    g = rng(seed)
+    lo = g.uniform(-1.0, 0.0, size=n)
+    return lo, lo + g.uniform(0.01, 1.0, size=n)
+
+
+def hyperbox_dirs(n: int, seed: int, lo: int, hi: int):
+    """Rows [lo, hi) of G3's direction list: the oct template (2n^2 rows, SPEC.md:365-367,
+    exercising l_i = 0) first, then row-normalised standard normals, HB_BLOCK rows per
+    independently seeded block."""
     tmpl = oct_directions(n)
-    if B <= tmpl.shape[0]:
-        return lo, hi, np.ascontiguousarray(tmpl[:B])
-    z = g.standard_normal(size=(B - tmpl.shape[0], n))
-    z /= np.linalg.norm(z, axis=1, keepdims=True)
-    return lo, hi, np.ascontiguousarray(np.concatenate([tmpl, z], axis=0))
+    t = tmpl.shape[0]
+    out = np.empty((hi - lo, n))
+    if lo < t:
+        out[: min(hi, t) - lo] = tmpl[lo:min(hi, t)]
+    a, b = max(lo, t), hi
+    if a < b:
+        for q in range((a - t) // HB_BLOCK, (b - 1 - t) // HB_BLOCK + 1):
+            z = np.random.Generator(np.random.PCG64([seed, 2, q])).standard_normal((HB_BLOCK, n))
+            z /= np.linalg.norm(z, axis=1, keepdims=True)
+            g0 = t + q * HB_BLOCK  # global row of the block's first row
+            s0, s1 = max(a, g0), min(b, g0 + HB_BLOCK)
+            out[s0 - lo:s1 - lo] = z[s0 - g0:s1 - g0]
+    return np.ascontiguousarray(out)
+
+
+def hyperbox(B: int, n: int, seed: int):
+    """G3 (type-3 workload; SURVEY §8(d)).  One shared box (PAPER.md:313, 672) and B
+    directions (hyperbox_box, hyperbox_dirs).  Returns (lo, hi, dirs)."""
+    lo, hi = hyperbox_box(n, seed)
+    return lo, hi, hyperbox_dirs(n, seed, 0, B)
 
 
 def status_mix(B: int, m: int, n: int, seed: int, infeasible_start: bool = False):
@@ -305,11 +329,11 @@ def twophase_signed_shard(B: int, m: int, n: int, seed: int, lo: int, hi: int):
 
 def make_config_shard(name: str, B: int, lo: int, hi: int):
     """LPs [lo, hi) of config `name` drawn for a batch of B (general configs are drawn
-    shard-locally; hyperbox directions use normals, so the batch is drawn and sliced)."""
+    shard-locally, hyperbox directions block by block)."""
     cfg = CONFIGS[name]
     if cfg["kind"] == "hyperbox":
-        lo_b, hi_b, dirs = hyperbox(B, cfg["n"], cfg["seed"])
-        return lo_b, hi_b, np.ascontiguousarray(dirs[lo:hi])
+        lo_b, hi_b = hyperbox_box(cfg["n"], cfg["seed"])
+        return lo_b, hi_b, hyperbox_dirs(cfg["n"], cfg["seed"], lo, hi)
     if cfg.get("shared"):
         A, b, _ = shared_polytope(1, cfg["m"], cfg["n"], cfg["seed"], cfg["gen"])
         bg = np.random.PCG64([cfg["seed"], 1])

@@ -79,3 +79,17 @@ def test_shared_polytope_layout_and_shards():
     assert np.array_equal(A2, Af) and np.array_equal(b2, bf) and np.array_equal(c2, cf[40:90])
     _, b3, _ = lpgen.shared_polytope(3, 40, 40, 3, "G2")
     assert (b3 < 0).sum() == 10  # ceil(m/4) covering rows
+
+
+def test_hyperbox_shards_cross_blocks():
+    """G3 shards are generated block by block and equal slices of the full batch, across
+    template / block boundaries (multi-GPU ranks draw only their slice)."""
+    n, B = 3, 3 * lpgen.HB_BLOCK + 77
+    full = lpgen.hyperbox(B, n, 9)[2]
+    t = 2 * n * n
+    for lo, hi in ((0, 5), (t - 2, t + 3), (t + lpgen.HB_BLOCK - 4, t + lpgen.HB_BLOCK + 9),
+                   (1000, B), (B - 1, B)):
+        _, _, d = lpgen.make_config_shard("cfg4", B, lo, hi) if n == 5 else (None, None,
+                                                                               lpgen.hyperbox_dirs(n, 9, lo, hi))
+        assert np.array_equal(d, full[lo:hi])
+    assert np.array_equal(lpgen.hyperbox(B, n, 9)[2], full)  # deterministic
