@@ -6,17 +6,19 @@
 //   * thread (tr, tc) of a TR x TC grid owns constraint rows i = tr + TR*a (a < A) and
 //     nonbasic positions p = tc + TC*b (b < BC): double T[A][BC] in registers;
 //   * the objective row(s) are REPLICATED in every thread for its positions (d2, d1), so
-//     Step 1 (Dantzig argmax) is a register scan + a REDUX-based warp argmax
-//     in every warp (no barrier);
+//     Step 1 (Dantzig argmax; or RPC) is a register scan + a
+//     REDUX-based warp argmax in every warp (no barrier), computed straight-line at the end
+//     of the previous pivot's update so its latency interleaves with the update's DFMAs;
 //   * Step 2 (ratio test): the owners of column e publish it to SMEM; each
 //     lane of a warp then takes one of the warp's rows (one IEEE division per lane), applies
 //     the previous pivot's RHS update to it (the RHS column lives in SMEM and is updated
-//     lazily, each row by exactly one lane), and the warp argmin goes to a per-warp partial
-//     -> barrier 1 -> every warp reduces the partials;
-//   * Step 3: the owners of row l publish prow = row / PE -> barrier 2 ->
-//     every thread applies T_ip = fma(f_i, prow_p, T_ip) to its registers (A*BC DFMAs with
-//     no per-element branch).  Row l and position e were zeroed when they were read, so the
-//     same fma produces the pivot row (f_l = 1) and the leaving variable's column.
+//     lazily, each row by exactly one lane), and the winning lane writes the warp's partial
+//     -> barrier 1 -> every thread scans the partials;
+//   * Step 3: the owners of row l publish the RAW row -> barrier 2 ->
+//     every thread divides its own positions by PE and applies T_ip = fma(f_i, prow_p, T_ip)
+//     to its registers (A*BC DFMAs with no per-element branch).  Row l and position e were
+//     zeroed when they were read, so the same fma produces the pivot row (f_l = 1) and the
+//     leaving variable's column.
 // Reductions use order-preserving integer keys and the sm_100 REDUX (__reduce_*_sync)
 // instructions: (value, tie key) argmax/argmin in three warp-wide REDUX steps.
 // All arithmetic matches oracle/lpb_oracle.c bit for bit (IEEE __ddiv_rn, explicit
