@@ -260,3 +260,21 @@ def test_hyperbox_no_x_empty_shared_box_and_misaligned_chunks(n, B):
     assert np.array_equal(ge["x"].cpu().numpy(), oe["x"], equal_nan=True)
     gh = lpb.hyperbox(lo, hi, dirs, n_chunks=7)  # odd chunk boundaries
     assert np.array_equal(gh["obj"], o["obj"]) and np.array_equal(gh["x"], o["x"])
+
+
+@pytest.mark.parametrize("klass", CLASSES)
+@pytest.mark.parametrize("scale_a,scale_b", [(1e-300, 1.0), (1.0, 1e-310), (1e300, 1e-300),
+                                             (2.0 ** -1060, 2.0 ** 1000)])
+def test_extreme_magnitudes(klass, scale_a, scale_b):
+    """Quotients outside the branch-free division's fast range (subnormal / huge ratios and
+    pivot elements) take the IEEE fallback (ddiv_slow) in the ratio test and the pivot row;
+    the result must still be the oracle's bit for bit.  Magnitudes also move the eps tests,
+    so statuses differ from the unscaled LPs -- only parity is asserted."""
+    A, b, c = lpgen.status_mix(400, 6, 6, 77, infeasible_start=True)
+    A = A * scale_a
+    b = b * scale_b
+    o = oracle.solve(A, b, c)
+    g = gpu_solve(A, b, c, kernel_class=klass)
+    compare(A, b, c, g, o, check_x=False)
+    ok = o["status"] == oracle.OPTIMAL
+    assert np.array_equal(g["x"][ok], o["x"][ok])
