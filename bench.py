@@ -388,7 +388,8 @@ def main():
         d2h = out_st.nbytes + out_obj.nbytes + out_x.nbytes + (out_it.nbytes if out_it is not None else 0)
         e2e = {"value": B * world * args.e2e_steps / (e_tot / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": int(in_bytes), "d2h_bytes_per_step": int(d2h),
-               "ms_per_step": e_tot / args.e2e_steps, "n_chunks": 10 if B > 100 else 1,
+               "ms_per_step": e_tot / args.e2e_steps,
+               "n_chunks": 10 if (B > 100 and in_bytes >= (1 << 20)) else 1,
                "gpu_launches_per_step": launches_e2e}
         hs.close()
 

@@ -95,8 +95,9 @@ typedef struct {
   int32_t device;      /* CUDA device ordinal; -1 -> the current device                       */
   void* stream;        /* cudaStream_t to run on (cudaStreamLegacy = 0x1 for the legacy default
                           stream); NULL -> a non-blocking stream owned by the context          */
-  int32_t n_chunks;    /* host-pointer pipeline depth; 0 -> 10 if batch > 100 else 1
-                          (the paper's stream count)                            */
+  int32_t n_chunks;    /* host-pointer pipeline depth; 0 -> 10 if batch > 100 and the inputs
+                          are >= 1 MiB, else 1 (the paper's stream count; tiny
+                          inputs cannot pay for per-chunk copy latency)                       */
   int32_t kernel_class;/* 0 auto; 1 S (thread/LP, m,n <= 8), 2 M (block/LP, SMEM tableau),
                           3 L (2/4-CTA cluster/LP, DSMEM), 4 R (block or warp/LP, register-
                           resident tableau tiles), 6 T (block/LP, one register-resident row

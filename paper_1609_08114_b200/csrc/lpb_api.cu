@@ -473,7 +473,14 @@ static int solve_impl(lpb_ctx* c, const double* A, const double* b, const double
 
   // ---- host pointers: chunked H2D -> kernel -> D2H pipeline on n_chunks streams ----
   c->host_path = true;
-  int nch = c->opt.n_chunks > 0 ? c->opt.n_chunks : (B > 100 ? 10 : 1);
+  // default pipeline depth: the paper's 10 streams for batches > 100 when the
+  // inputs are big enough to overlap; a chunk's copies and launch cost ~10 us of fixed
+  // latency, so inputs under 1 MiB go as one chunk (reading R16)
+  const int64_t in_bytes = 8 * (general ? (sab ? (int64_t)m * n + m + B * (int64_t)n
+                                               : B * ((int64_t)m * n + m + n))
+                                        : (shared ? 2 * (int64_t)n : 2 * B * (int64_t)n) + B * (int64_t)n);
+  int nch = c->opt.n_chunks > 0 ? c->opt.n_chunks
+                                : ((B > 100 && in_bytes >= (1 << 20)) ? 10 : 1);
   if (nch > 64) nch = 64;
   if (nch > B) nch = (int)B;
   int rc = ensure_host_path(c, nch);
