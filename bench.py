@@ -37,9 +37,11 @@ UNIT = "LPs/s"
 PAPER_LPS = {"cfg4": 4001000 / 0.406, "cfg5": 6003000 / 2.388}
 # oracle sample per reference step (bounded CPU work)
 REF_SAMPLE = {"cfg1": 1000, "cfg2": 240, "cfg3": 8, "cfg4": 4001000, "cfg5": 1000000,
-              "cfg2s": 240, "cfg3s": 8, "cfg2r": 160, "cfg6": 32, "cfg7": 16, "cfg8": 4}
+              "cfg2s": 240, "cfg3s": 8, "cfg2r": 160, "cfg6": 32, "cfg7": 16, "cfg8": 4,
+              "cfg9": 20000, "cfg10": 4000}
 CPU_SAMPLE = {"cfg1": 1000, "cfg2": 1200, "cfg3": 24, "cfg4": 4001000, "cfg5": 6003000,
-              "cfg2s": 1200, "cfg3s": 24, "cfg2r": 800, "cfg6": 160, "cfg7": 32, "cfg8": 16}
+              "cfg2s": 1200, "cfg3s": 24, "cfg2r": 800, "cfg6": 160, "cfg7": 32, "cfg8": 16,
+              "cfg9": 50000, "cfg10": 20000}
 L2_BYTES = 126 * 1024 * 1024
 
 

@@ -262,6 +262,10 @@ CONFIGS = {
     "cfg6": dict(kind="general", gen="G1", B=5000, m=300, n=300, seed=6),
     "cfg7": dict(kind="general", gen="G1", B=1000, m=500, n=500, seed=7),
     "cfg8": dict(kind="general", gen="G2", B=1000, m=340, n=340, seed=8),
+    # the rest of the paper's type-1 dimension sweep (fig:TimeLPplotting: 5, 28, 50, 100,
+    # 300, 500) at its largest batch
+    "cfg9": dict(kind="general", gen="G1", B=50000, m=28, n=28, seed=9),
+    "cfg10": dict(kind="general", gen="G1", B=50000, m=50, n=50, seed=10),
 }
 
 

@@ -313,7 +313,12 @@ static int run_general(lpb_ctx* c, cudaStream_t s, int64_t lp0, int64_t cnt, con
     c->last_grid = 0;
     return LPB_OK;
   }
-  const bool r_ok_worst = reg_fits(c->m, c->n, c->m);
+  // Worst-case capacity (k = m) saves the kmax prepass (a tiny kernel + a 4-byte D2H round
+  // trip) -- worth it only when the worst-case register layout is already the one the
+  // smallest k would get (tiny LPs); otherwise the exact kmax buys a denser layout (e.g. a
+  // warp per LP at 28x28 instead of a 128-thread CTA).
+  const int worst_layout = reg_layout(c->m, c->n, c->m);
+  const bool r_ok_worst = worst_layout >= 0 && worst_layout == reg_layout(c->m, c->n, 0);
   if (kmax < 0 && r_ok_worst && (forced == CLASS_AUTO || forced == CLASS_R))
     kmax = c->m;  // worst-case capacity, no prepass
   if (kmax < 0) {  // device prepass: kmax over the chunk (one tiny kernel + 4-byte D2H)

@@ -78,6 +78,7 @@ cudaError_t launch_simplex_row(const SimplexArgs& a, int grid_override, cudaStre
 
 // ---- R class: one LP per CTA (one warp for small LPs), tableau resident in registers ----
 bool reg_fits(int m, int n, int kmax);
+int reg_layout(int m, int n, int kmax);  // the layout id the R class would use (-1: none)
 cudaError_t launch_simplex_reg(const SimplexArgs& a, int grid_override, cudaStream_t s,
                                int* ctas_out);
 

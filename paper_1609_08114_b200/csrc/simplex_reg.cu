@@ -733,6 +733,8 @@ struct RegCfg {
   X(0, 8, 4, 1, 0, 3, true, 16)         \
   X(1, 8, 4, 2, 0, 6, true, 12)         \
   X(2, 8, 4, 4, 0, 8, true, 6)          \
+  X(8, 8, 8, 7, 0, 7, false, 4)         \
+  X(9, 8, 8, 7, 0, 7, true, 4)          \
   X(3, 16, 8, 4, 0, 8, true, 2)         \
   X(6, 8, 16, 13, 0, 7, false, 2)       \
   X(4, 16, 16, 7, 0, 7, false, 1)       \
@@ -797,6 +799,8 @@ static int pick_cfg(int m, int n, int kmax) {
 }
 
 bool reg_fits(int m, int n, int kmax) { return pick_cfg(m, n, kmax) >= 0; }
+
+int reg_layout(int m, int n, int kmax) { return pick_cfg(m, n, kmax); }
 
 cudaError_t launch_simplex_reg(const SimplexArgs& a, int grid_override, cudaStream_t s,
                                int* ctas_out) {
