@@ -735,7 +735,8 @@ struct RegCfg {
   X(2, 8, 4, 4, 0, 8, true, 6)          \
   X(8, 8, 8, 7, 0, 7, false, 4)         \
   X(9, 8, 8, 7, 0, 7, true, 4)          \
-  X(3, 16, 8, 4, 0, 8, true, 2)         \
+  X(10, 8, 8, 8, 0, 8, false, 4)        \
+  X(11, 8, 8, 8, 0, 8, true, 4)         \
   X(6, 8, 16, 13, 0, 7, false, 2)       \
   X(4, 16, 16, 7, 0, 7, false, 1)       \
   X(5, 16, 16, 7, 0, 7, true, 1)

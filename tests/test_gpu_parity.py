@@ -35,7 +35,8 @@ def _skip_class(klass, m, n, k):
 
 def _reg_fits(m, n, k):
     # mirrors the instantiated register layouts in csrc/simplex_reg.cu (capacity m x (n+k))
-    caps = [(8, 12, 1), (16, 24, 1), (32, 32, 1), (56, 56, 0), (56, 56, 1), (64, 64, 1),
+    caps = [(8, 12, 1), (16, 24, 1), (32, 32, 1), (56, 56, 0), (56, 56, 1), (64, 64, 0),
+            (64, 64, 1),
             (104, 112, 0), (112, 112, 0), (112, 112, 1)]
     return any(m <= r and n + k <= c and (k == 0 or two) for r, c, two in caps)
 
@@ -76,6 +77,7 @@ CASES = [
     ("mix", 100, 100, 60), ("G2", 8, 8, 2000), ("G2", 50, 50, 100), ("G2light", 60, 60, 60),
     ("deg", 8, 8, 3000), ("degneg", 8, 8, 3000), ("degneg", 20, 20, 1000),
     ("G1", 50, 50, 300), ("G2", 40, 40, 150), ("mixneg", 48, 40, 300),
+    ("G1", 64, 60, 200), ("G2", 56, 48, 100),
 ]
 
 
