@@ -168,3 +168,16 @@ def test_warm_start_iteration_limit_in_phase_one():
     g = gpu_solve(A, b, c, kernel_class="M", max_iter=5)
     compare(Ab, bb, c, g, o)
     assert np.all(g["status"] == oracle.ITER_LIMIT)
+
+
+@pytest.mark.parametrize("klass", ["M", "L", "R"])
+def test_rpc_shared_two_phase_cold_path(klass):
+    """Under RPC the phase-I path depends on the LP index, so shared-constraint two-phase
+    batches are solved from scratch (no warm start) -- still the oracle's, bit for bit."""
+    A, b, c = _shared("G2", 300, 40, 40, 19)
+    Ab = np.ascontiguousarray(np.broadcast_to(A, (300, 40, 40)))
+    bb = np.ascontiguousarray(np.broadcast_to(b, (300, 40)))
+    o = oracle.solve(Ab, bb, c, pivot_rule="RPC", rpc_seed=4)
+    g = gpu_solve(A, b, c, kernel_class=klass, pivot_rule="RPC", rpc_seed=4)
+    compare(Ab, bb, c, g, o)
+    assert len(np.unique(o["iters"][:, 0])) > 1  # phase I differs across the batch under RPC
