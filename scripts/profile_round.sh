@@ -7,7 +7,7 @@ mkdir -p $OUT
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $OUT/gpu.txt
 timeout 1500 python -m pytest tests -m gpu -q > $OUT/pytest_gpu.txt 2>&1
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.txt 2>&1
-for cf in cfg2 cfg1 cfg4 cfg5 cfg2s cfg2r; do
+for cf in cfg2 cfg1 cfg4 cfg5 cfg2s cfg2r cfg9 cfg10; do
   timeout 900 python bench.py --config $cf > $OUT/bench_$cf.json 2> $OUT/bench_$cf.err
 done
 for cf in cfg3 cfg3s; do
