@@ -4,7 +4,8 @@
  * Solves a batch of independent linear programs in standard form
  *     maximize c.x  subject to  A x <= b,  x >= 0                (Eq. 1-3)
  * with the dense-tableau simplex method (Dantzig's "Largest Positive Coefficient" entering
- * rule; ratio test PAPER.md:97,126; pivot PAPER.md:163-172), the two-phase
+ * rule, or the "Random Positive Coefficient" rule, see
+ * lpb_options.pivot_rule; ratio test PAPER.md:97,126; pivot PAPER.md:163-172), the two-phase
  * method when the slack basis is infeasible, and the closed-form hyperbox LP
  * (Eq. 6).  One LP per CUDA thread block (or thread-block cluster, or
  * thread), as in PAPER.md:114 ("We assign a CUDA block of threads to solve an LP").
