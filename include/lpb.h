@@ -102,7 +102,8 @@ typedef struct {
   int32_t kernel_class;/* 0 auto; 1 S (thread/LP, m,n <= 8), 2 M (block/LP, SMEM tableau),
                           3 L (2/4-CTA cluster/LP, DSMEM), 4 R (block or warp/LP, register-
                           resident tableau tiles), 6 T (block/LP, one register-resident row
-                          per thread); for tests / benches                                 */
+                          per thread), 7 W (warp/LP, m <= 32 and n + k <= 32, tableau in
+                          registers, shuffle exchanges); for tests / benches               */
   int32_t grid_ctas;   /* 0 auto; persistent grid size override (scheduling-invariance tests) */
   int32_t cluster_ctas;/* L class cluster size: 0 auto (the smallest of 2/4/8/16 CTAs whose
                           distributed SMEM holds the tableau); 2/4/8/16 forces that size when
@@ -188,7 +189,7 @@ int lpb_last_timing(lpb_ctx* c, double* solve_ms, double* e2e_ms);
 int lpb_last_kernel_timing(lpb_ctx* c, double* kernel_ms);
 
 /* Number of kernel launches the last solve issued (for the bench's gpu_launches count),
- * and the size class it dispatched to (1 S, 2 M, 3 L, 4 R, 5 H, 6 T). */
+ * and the size class it dispatched to (1 S, 2 M, 3 L, 4 R, 5 H, 6 T, 7 W). */
 int lpb_last_launch_info(lpb_ctx* c, int32_t* launches, int32_t* kernel_class);
 
 /* Launch shape of the last solve's dominant kernel: CTAs per LP (the L class's cluster size

@@ -122,7 +122,7 @@ extern "C" const char* lpb_last_error(lpb_ctx* c) { return c ? c->err : ""; }
 
 // Size-class capacity check at the best case (no artificial rows).
 static bool general_fits_any(int m, int n) {
-  return thread_fits(m, n) || reg_fits(m, n, 0) || block_fits(1, m, n, 0) ||
+  return thread_fits(m, n) || warp_fits(m, n, 0) || reg_fits(m, n, 0) || block_fits(1, m, n, 0) ||
          block_fits(2, m, n, 0) || block_fits(4, m, n, 0) || block_fits(8, m, n, 0) ||
          block_fits(16, m, n, 0);
 }
@@ -224,6 +224,7 @@ static int choose_class(const lpb_ctx* c, int kmax, int* cl) {
   const int m = c->m, n = c->n;
   const int forced = c->opt.kernel_class;
   *cl = 1;
+  if (forced == CLASS_W) return warp_fits(m, n, kmax) ? CLASS_W : -1;
   if (forced == CLASS_R) return reg_fits(m, n, kmax) ? CLASS_R : -1;
   if (forced == CLASS_T) return row_fits(m, n, kmax) ? CLASS_T : -1;
   if (forced == CLASS_M) return block_fits(1, m, n, kmax) ? CLASS_M : -1;
@@ -238,6 +239,7 @@ static int choose_class(const lpb_ctx* c, int kmax, int* cl) {
       if (block_fits(q, m, n, kmax)) { *cl = q; return CLASS_L; }
     return -1;
   }
+  if (warp_fits(m, n, kmax)) return CLASS_W;
   if (reg_fits(m, n, kmax)) return CLASS_R;
   if (block_fits(1, m, n, kmax)) return CLASS_M;
   for (int q : {2, 4, 8, 16})
@@ -319,8 +321,12 @@ static int run_general(lpb_ctx* c, cudaStream_t s, int64_t lp0, int64_t cnt, con
   // warp per LP at 28x28 instead of a 128-thread CTA).
   const int worst_layout = reg_layout(c->m, c->n, c->m);
   const bool r_ok_worst = worst_layout >= 0 && worst_layout == reg_layout(c->m, c->n, 0);
-  if (kmax < 0 && r_ok_worst && (forced == CLASS_AUTO || forced == CLASS_R))
+  const int w_worst = warp_layout(c->m, c->n, c->m);
+  const bool w_ok_worst = w_worst >= 0 && w_worst == warp_layout(c->m, c->n, 0);
+  if (kmax < 0 && w_ok_worst && (forced == CLASS_AUTO || forced == CLASS_W))
     kmax = c->m;  // worst-case capacity, no prepass
+  if (kmax < 0 && r_ok_worst && (forced == CLASS_AUTO || forced == CLASS_R))
+    kmax = c->m;
   if (kmax < 0) {  // device prepass: kmax over the chunk (one tiny kernel + 4-byte D2H)
     LPB_CUDA(c, launch_count_art(b, sab ? 1 : cnt, c->m, c->d_kmax, s));
     LPB_CUDA(c, cudaMemcpyAsync(c->h_kmax, c->d_kmax, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -336,7 +342,9 @@ static int run_general(lpb_ctx* c, cudaStream_t s, int64_t lp0, int64_t cnt, con
   int ctas = 0;
   const bool timed = (s == c->stream) && !c->no_timing;
   if (timed) LPB_CUDA(c, cudaEventRecord(c->kev0, s));
-  if (klass == CLASS_R) {
+  if (klass == CLASS_W) {
+    LPB_CUDA(c, launch_simplex_warp(a, c->opt.grid_ctas, s, &ctas));
+  } else if (klass == CLASS_R) {
     LPB_CUDA(c, launch_simplex_reg(a, c->opt.grid_ctas, s, &ctas));
   } else if (klass == CLASS_T) {
     LPB_CUDA(c, launch_simplex_row(a, c->opt.grid_ctas, s, &ctas));

@@ -13,7 +13,7 @@ enum : int32_t { ST_OPTIMAL = 0, ST_UNBOUNDED = 1, ST_INFEASIBLE = 2, ST_ITER_LI
 
 // Size classes (lpb_options.kernel_class / lpb_last_launch_info).
 enum : int32_t { CLASS_AUTO = 0, CLASS_S = 1, CLASS_M = 2, CLASS_L = 3, CLASS_R = 4,
-                 CLASS_H = 5, CLASS_T = 6 };
+                 CLASS_H = 5, CLASS_T = 6, CLASS_W = 7 };
 
 struct SimplexArgs {
   int64_t batch;
@@ -81,6 +81,12 @@ bool reg_fits(int m, int n, int kmax);
 int reg_layout(int m, int n, int kmax);  // the layout id the R class would use (-1: none)
 cudaError_t launch_simplex_reg(const SimplexArgs& a, int grid_override, cudaStream_t s,
                                int* ctas_out);
+
+// ---- W class: one LP per warp (m <= 32, n + kmax <= 32), tableau in registers, shuffles ----
+bool warp_fits(int m, int n, int kmax);
+int warp_layout(int m, int n, int kmax);  // the layout id the W class would use (-1: none)
+cudaError_t launch_simplex_warp(const SimplexArgs& a, int grid_override, cudaStream_t s,
+                                int* ctas_out);
 
 // ---- prepass: kmax = max over LPs of #{i : b_i < 0} ----
 cudaError_t launch_count_art(const double* b, int64_t batch, int m, int* kmax_dev,

@@ -1,0 +1,466 @@
+// simplex_warp.cu — W class: one LP per WARP for small LPs (up to 32 x 32 condensed), the
+// tableau in registers and every exchange a warp shuffle (no shared memory, no barrier).
+//
+// Same method and arithmetic as the oracle (§3.1 Steps 1-3, Listing 1; two-phase
+// PAPER.md:76; readings R1-R15 in DESIGN.md), laid out for latency: a small LP's pivot is a
+// chain of dependent steps, so each step is the shortest exchange that does it.
+//   * lane = (tr, tc) with tr = lane / 4 (8 thread-rows), tc = lane % 4 (4 thread-cols);
+//     lane owns rows i = tr + 8a (a < A) and positions p = tc + 4b (b < BC) of the condensed
+//     tableau; the objective row(s) are replicated per thread-row (d2, d1); lane L owns row L
+//     for the ratio test (its RHS and basic-variable key live in its registers);
+//   * Step 1: a register scan on the 4 lanes of thread-row 0 + a REDUX warp argmax;
+//   * column e: its owner lanes pick T[.][e] with a uniform switch and the ratio lanes and
+//     update multipliers fetch it with A shuffles; the ratio test is one IEEE division per
+//     lane + a REDUX warp argmin;
+//   * pivot row l: picked with a uniform switch, BC shuffles bring each lane its positions;
+//     every lane divides its own positions by PE and applies fma(f_i, prow_p, T_ip).
+// Warps are independent LPs (4 per CTA); a CTA never synchronises.
+#include <climits>
+
+#include "lpb_fp64.cuh"
+#include "lpb_internal.cuh"
+#include "lpb_reduce.cuh"
+#include "lpb_rng.cuh"
+
+namespace lpb {
+namespace {
+
+constexpr unsigned WFULL = 0xffffffffu;
+constexpr int W_WARPS = 4;  // LPs (warps) per CTA
+constexpr int DEADW = INT_MAX;
+
+__device__ __forceinline__ double w_neg_inf() {
+  return __longlong_as_double(0xfff0000000000000ll);
+}
+
+// warp argmax of (64-bit key desc, tie asc) over valid lanes, branch-free; -1 if none
+__device__ __forceinline__ int w_argmax(bool valid, unsigned long long key, unsigned tie) {
+  const unsigned hi = valid ? (unsigned)(key >> 32) : 0u;
+  const unsigned mhi = __reduce_max_sync(WFULL, hi);
+  const bool c1 = valid && hi == mhi;
+  const unsigned b1 = __ballot_sync(WFULL, c1);
+  if (b1 == 0u) return -1;
+  if ((b1 & (b1 - 1u)) == 0u) return __ffs(b1) - 1;
+  const unsigned lo = c1 ? (unsigned)key : 0u;
+  const unsigned mlo = __reduce_max_sync(WFULL, lo);
+  const bool c2 = c1 && (unsigned)key == mlo;
+  const unsigned mt = __reduce_min_sync(WFULL, c2 ? tie : 0xffffffffu);
+  return __ffs(__ballot_sync(WFULL, c2 && tie == mt)) - 1;
+}
+
+template <int A, int BC, bool TWO, bool RPC>
+__global__ void __launch_bounds__(32 * W_WARPS) simplex_warp_kernel(SimplexArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int tr = lane >> 2, tc = lane & 3;
+  const int m = a.m, n = a.n;
+  const int64_t gw = (int64_t)blockIdx.x * W_WARPS + (threadIdx.x >> 5);
+  const int64_t nw = (int64_t)gridDim.x * W_WARPS;
+  const bool direct = a.ticket == nullptr;
+
+  int64_t lp = direct ? gw : 0;
+  if (!direct) {
+    int t = 0;
+    if (lane == 0) t = atomicAdd(a.ticket, 1);
+    lp = __shfl_sync(WFULL, t, 0);
+  }
+  while (lp < a.batch) {
+    const double* __restrict__ Ak = a.A + lp * a.sA;
+    const double* __restrict__ bk = a.b + lp * a.sb;
+    const double* __restrict__ ck = a.c + lp * (int64_t)n;
+
+    // ---- build (R7) ----
+    const bool rowL = lane < m;
+    const double bL = rowL ? __ldg(bk + lane) : 0.0;
+    const bool negL = rowL && bL < 0.0;
+    const unsigned negmask = __ballot_sync(WFULL, negL);
+    const int k = __popc(negmask);
+    const int npos = n + k;
+    double binf = fabs(bL);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) binf = fmax(binf, __shfl_xor_sync(WFULL, binf, off));
+    int st = (m > 8 * A || npos > 4 * BC || (!TWO && k > 0)) ? ST_NUMERICAL : -1;
+    double rhs = negL ? -bL : bL;                 // RHS of row `lane`
+    int bkey = negL ? (lane - m) : (n + lane);    // key of row `lane`'s basic variable
+    double T[A][BC];
+    int nbv[BC];  // position -> variable (replicated across thread-rows)
+#pragma unroll
+    for (int b = 0; b < BC; ++b) {
+      const int p = tc + 4 * b;
+      int var = DEADW;
+      if (p < n) {
+        var = p;
+      } else if (p < npos) {  // slack of the (p-n)-th negated row (ascending)
+        unsigned mk = negmask;
+        for (int t = 0; t < p - n; ++t) mk &= mk - 1u;
+        var = n + (__ffs(mk) - 1);
+      }
+      nbv[b] = var;
+    }
+#pragma unroll
+    for (int ai = 0; ai < A; ++ai) {
+      const int i = tr + 8 * ai;
+      const bool neg = (negmask >> (i & 31)) & 1u;
+#pragma unroll
+      for (int b = 0; b < BC; ++b) {
+        const int p = tc + 4 * b;
+        double v = 0.0;
+        if (st < 0 && i < m && p < npos) {
+          if (p < n) {
+            v = __ldg(Ak + (int64_t)i * n + p);
+            v = neg ? -v : v;
+          } else {
+            v = (nbv[b] == n + i) ? -1.0 : (neg ? -0.0 : 0.0);
+          }
+        }
+        T[ai][b] = v;
+      }
+    }
+    double d2[BC], d1[TWO ? BC : 1];
+#pragma unroll
+    for (int b = 0; b < BC; ++b) {
+      const int p = tc + 4 * b;
+      d2[b] = (p < n) ? __ldg(ck + p) : (p < npos ? 0.0 : w_neg_inf());
+    }
+    double z2 = 0.0, z1 = 0.0;
+    if constexpr (TWO) {
+      // phase-I row: ascending-row sums of the negated rows (R7), each lane for its positions
+#pragma unroll
+      for (int b = 0; b < BC; ++b) d1[b] = (tc + 4 * b < npos) ? 0.0 : w_neg_inf();
+      if (k == 0) {
+#pragma unroll
+        for (int b = 0; b < BC; ++b) d1[b] = w_neg_inf();
+      }
+      unsigned mk = negmask;
+      while (mk) {
+        const int r = __ffs(mk) - 1;
+        mk &= mk - 1u;
+        const int ar = r >> 3, src = ((r & 7) << 2) | tc;
+        double rv[BC];
+#pragma unroll
+        for (int b = 0; b < BC; ++b) {
+          double v = T[0][b];
+#pragma unroll
+          for (int ai = 1; ai < A; ++ai) v = (ai == ar) ? T[ai][b] : v;
+          rv[b] = __shfl_sync(WFULL, v, src);
+        }
+#pragma unroll
+        for (int b = 0; b < BC; ++b)
+          if (tc + 4 * b < npos) d1[b] = __dadd_rn(d1[b], rv[b]);
+        z1 = __dadd_rn(z1, __shfl_sync(WFULL, rhs, r));
+      }
+    }
+
+    // ---- Steps 1-3, two phases ----
+    int it1 = 0, it2 = 0, stall = 0, phase = (TWO && k > 0) ? 1 : 2, dl = 0;
+    bool drive = false;
+    const uint64_t lpkey = RPC ? rpc_lp_key(a.rpc_seed, a.lp_base + lp) : 0ull;
+    while (st < 0) {
+      const bool bland = a.bland_K > 0 && stall >= a.bland_K;
+      const bool p1 = TWO && phase == 1;
+      int e, evar, l;
+      double dE2 = 0.0, dE1 = 0.0;  // the objective rows' entries at position e
+      if (drive) {
+        // R9: drive the next basic artificial out on max |T[l][p]| over live positions
+        const unsigned art = __ballot_sync(WFULL, lane < m && bkey < 0);
+        const unsigned rest = art & ~((dl >= 32) ? 0xffffffffu : ((1u << dl) - 1u));
+        if (rest == 0u) {
+          drive = false;
+          phase = 2;
+          stall = 0;
+          continue;
+        }
+        l = __ffs(rest) - 1;
+        dl = l + 1;
+        const int al = l >> 3;
+        bool val = false;
+        double bv = 0.0;
+        unsigned bvar = 0xffffffffu;
+        int bb = 0;
+        if (tr == (l & 7)) {
+#pragma unroll
+          for (int b = 0; b < BC; ++b) {
+            double v = T[0][b];
+#pragma unroll
+            for (int ai = 1; ai < A; ++ai) v = (ai == al) ? T[ai][b] : v;
+            v = fabs(v);
+            const unsigned var = (unsigned)nbv[b];
+            if (d2[b] != w_neg_inf() && v > a.eps_piv &&
+                (!val || v > bv || (v == bv && var < bvar))) {
+              val = true;
+              bv = v;
+              bvar = var;
+              bb = b;
+            }
+          }
+        }
+        const int wl = w_argmax(val, okey(bv), bvar);
+        if (wl < 0) continue;  // redundant row: the artificial stays basic at 0
+        e = __shfl_sync(WFULL, tc + 4 * bb, wl);
+        evar = (int)__shfl_sync(WFULL, bvar, wl);
+        dE2 = __shfl_sync(WFULL, d2[bb], wl);
+        if constexpr (TWO) dE1 = __shfl_sync(WFULL, d1[bb], wl);
+      } else {
+        // Step 1 on thread-row 0 (the replicas are identical across thread-rows)
+        bool val = false;
+        double bv = w_neg_inf();
+        unsigned long long bu = 0ull;
+        unsigned bvar = 0xffffffffu;
+        int bb = 0;
+        const bool rpc = RPC && !bland;
+        const uint64_t pkey = RPC ? rpc_pivot_key(lpkey, it1 + it2) : 0ull;
+#pragma unroll
+        for (int b = 0; b < BC; ++b) {
+          const double v = p1 ? d1[TWO ? b : 0] : d2[b];
+          const unsigned var = (unsigned)nbv[b];
+          const bool cand = v > a.eps_enter;
+          bool take;
+          if (bland) {
+            take = cand && var < bvar;
+          } else if (rpc) {
+            const unsigned long long u = rpc_score(pkey, (int)var);
+            take = cand && (!val || u > bu || (u == bu && var < bvar));
+            bu = take ? u : bu;
+          } else {
+            take = cand && (!val || v > bv || (v == bv && var < bvar));
+          }
+          val = val || take;
+          bv = take ? v : bv;
+          bvar = take ? var : bvar;
+          bb = take ? b : bb;
+        }
+        val = val && tr == 0;
+        const int wl = bland ? warp_argmin(val, 0ull, bvar)
+                             : w_argmax(val, rpc ? bu : okey(bv), bvar);
+        if (wl < 0) {
+          if (phase == 2) { st = ST_OPTIMAL; break; }
+          if (z1 > a.eps_phase1 * fmax(1.0, binf)) { st = ST_INFEASIBLE; break; }
+          drive = true;  // phase-I optimum with w* ~ 0
+          dl = 0;
+          continue;
+        }
+        if (it1 + it2 >= a.max_iter) { st = ST_ITER_LIMIT; break; }
+        e = __shfl_sync(WFULL, tc + 4 * bb, wl);
+        evar = (int)__shfl_sync(WFULL, bvar, wl);
+        dE2 = __shfl_sync(WFULL, d2[bb], wl);
+        if constexpr (TWO) dE1 = __shfl_sync(WFULL, d1[bb], wl);
+        l = -1;
+      }
+
+      // ---- column e: owners (tc == e%4) pick it; shuffles bring it to the ratio lanes and
+      //      to every lane's update multipliers ----
+      const int be = e >> 2, etc = e & 3;
+      double col[A];
+#pragma unroll
+      for (int ai = 0; ai < A; ++ai) {
+        double v = T[ai][0];
+#pragma unroll
+        for (int b = 1; b < BC; ++b) v = (b == be) ? T[ai][b] : v;
+        col[ai] = v;
+      }
+      double f[A];  // -T[i][e] for the lane's rows
+#pragma unroll
+      for (int ai = 0; ai < A; ++ai) f[ai] = -__shfl_sync(WFULL, col[ai], (tr << 2) | etc);
+      // ratio lane L = row L: T[L][e] comes from lane ((L & 7) << 2 | etc), register L >> 3
+      double vL = 0.0;
+      {
+        const int src = ((lane & 7) << 2) | etc, aL = lane >> 3;
+#pragma unroll
+        for (int ai = 0; ai < A; ++ai) {
+          const double v = __shfl_sync(WFULL, col[ai], src);
+          vL = (ai == aL) ? v : vL;
+        }
+      }
+      double theta = 0.0;
+      if (!drive) {  // Step 2: ratio test, one row per lane (R1, R2, R5)
+        const bool cand = lane < m && vL > a.eps_piv;
+        bool slow;
+        double r = div_fast(rhs, cand ? vL : 1.0, slow);
+        if (slow) r = ddiv_slow(rhs, cand ? vL : 1.0);
+        const int tie = bland ? bkey : lane;
+        const int wr = warp_argmin(cand, okey(r), ikey(tie));
+        if (wr < 0) { st = (phase == 2) ? ST_UNBOUNDED : ST_NUMERICAL; break; }
+        l = wr;
+        theta = __shfl_sync(WFULL, r, wr);
+      }
+
+      // ---- Step 3: pivot row l / PE, rank-1 update ----
+      const double pe = __shfl_sync(WFULL, vL, l);
+      const double rhs_l = __shfl_sync(WFULL, rhs, l);
+      const int leaving = __shfl_sync(WFULL, bkey, l);
+      const int al = l >> 3, ltr = l & 7;
+      double prow[BC];
+      {
+        double rv[BC];
+#pragma unroll
+        for (int b = 0; b < BC; ++b) {
+          double v = T[0][b];
+#pragma unroll
+          for (int ai = 1; ai < A; ++ai) v = (ai == al) ? T[ai][b] : v;
+          rv[b] = __shfl_sync(WFULL, v, (ltr << 2) | tc);
+        }
+        const double rpe = recip_of(pe);
+        bool slow_any = false;
+#pragma unroll
+        for (int b = 0; b < BC; ++b) {
+          const double num = (tc + 4 * b == e) ? 1.0 : rv[b];
+          bool sl;
+          prow[b] = div_with(num, pe, rpe, sl);
+          slow_any |= sl;
+        }
+        bool slr;
+        double prr = div_with(rhs_l, pe, rpe, slr);
+        if (slow_any || slr) {
+#pragma unroll
+          for (int b = 0; b < BC; ++b) prow[b] = ddiv_slow((tc + 4 * b == e) ? 1.0 : rv[b], pe);
+          prr = ddiv_slow(rhs_l, pe);
+        }
+        // the lane's row L: RHS and basic variable
+        rhs = (lane == l) ? prr : __fma_rn(-vL, prr, rhs);
+        bkey = (lane == l) ? evar : bkey;
+        // objective rows: position e restarts from 0, fma(-d_e, prow_p, d_p)
+        const bool mine = tc == etc;
+#pragma unroll
+        for (int b = 0; b < BC; ++b) {
+          const bool z = mine && b == be;
+          d2[b] = __fma_rn(-dE2, prow[b], z ? 0.0 : d2[b]);
+          if constexpr (TWO) {
+            if (p1) d1[b] = __fma_rn(-dE1, prow[b], z ? 0.0 : d1[b]);
+          }
+        }
+        z2 = __fma_rn(-dE2, prr, z2);
+        if constexpr (TWO) {
+          if (p1) z1 = __fma_rn(-dE1, prr, z1);
+        }
+        // tableau: row l and column e zeroed, multiplier of row l = 1
+#pragma unroll
+        for (int ai = 0; ai < A; ++ai) {
+          const bool isl = tr == ltr && ai == al;
+          const double fi = isl ? 1.0 : f[ai];
+#pragma unroll
+          for (int b = 0; b < BC; ++b) {
+            const bool z = isl || (mine && b == be);
+            T[ai][b] = __fma_rn(fi, prow[b], z ? 0.0 : T[ai][b]);
+          }
+        }
+        // position e now holds the leaving variable (dead if artificial, R7)
+#pragma unroll
+        for (int b = 0; b < BC; ++b) {
+          if (mine && b == be) {
+            nbv[b] = leaving >= 0 ? leaving : DEADW;
+            if (leaving < 0) {
+              d2[b] = w_neg_inf();
+              if constexpr (TWO) d1[b] = w_neg_inf();
+            }
+          }
+        }
+      }
+      if (drive) {
+        ++it1;
+      } else {
+        if (phase == 1) ++it1; else ++it2;
+        stall = (theta > 0.0) ? 0 : stall + 1;
+      }
+    }
+
+    // ---- extract (R10) ----
+    if (lane == 0) {
+      a.status[lp] = st;
+      a.iters[2 * lp] = it1;
+      a.iters[2 * lp + 1] = it2;
+      a.obj[lp] = (st == ST_OPTIMAL) ? -z2
+                : (st == ST_UNBOUNDED) ? __longlong_as_double(0x7ff0000000000000ll)
+                : (st == ST_INFEASIBLE) ? w_neg_inf()
+                                        : __longlong_as_double(0x7ff8000000000000ll);
+    }
+    if (a.x) {
+      double* xk = a.x + lp * (int64_t)n;
+      const double fill = (st == ST_OPTIMAL) ? 0.0 : __longlong_as_double(0x7ff8000000000000ll);
+      for (int j = lane; j < n; j += 32) xk[j] = fill;
+      __syncwarp();
+      if (st == ST_OPTIMAL && lane < m && bkey >= 0 && bkey < n) xk[bkey] = rhs;
+    }
+    if (direct) {
+      lp += nw;  // grid-stride (one pass when the grid covers the batch)
+    } else {
+      int t = 0;
+      if (lane == 0) t = atomicAdd(a.ticket, 1);
+      lp = __shfl_sync(WFULL, t, 0);
+    }
+  }
+}
+
+struct WarpCfg {
+  int rcap, ccap, two, id;
+};
+
+// {id, A (row slots per thread-row), BC (positions per thread-col), TWO}
+#define LPB_WARP_CONFIGS(X) \
+  X(0, 1, 3, true)          \
+  X(1, 2, 6, true)          \
+  X(2, 4, 8, false)         \
+  X(3, 4, 8, true)
+
+template <int A, int BC, bool TWO, bool RPC>
+cudaError_t launch_w(const SimplexArgs& a, int grid_override, cudaStream_t s, int* ctas) {
+  auto kern = simplex_warp_kernel<A, BC, TWO, RPC>;
+  static int cached_dev = -1, per_sm = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev != cached_dev) {
+    const cudaError_t e =
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * W_WARPS, 0);
+    if (e != cudaSuccess) return e;
+    cached_dev = dev;
+  }
+  const int64_t resident = (int64_t)(per_sm < 1 ? 1 : per_sm) * device_sm_count();
+  const int64_t need = (a.batch + W_WARPS - 1) / W_WARPS;
+  SimplexArgs d = a;
+  int64_t grid;
+  if (need <= resident && grid_override <= 0) {
+    d.ticket = nullptr;  // one resident wave: warp w solves LP w
+    grid = need;
+  } else {
+    grid = grid_override > 0 ? grid_override : resident;
+    if (grid > need) grid = need;
+    const cudaError_t e = cudaMemsetAsync(d.ticket, 0, sizeof(int), s);
+    if (e != cudaSuccess) return e;
+  }
+  if (ctas) *ctas = (int)grid;
+  kern<<<(unsigned)grid, 32 * W_WARPS, 0, s>>>(d);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+static const WarpCfg kWarpCfgs[] = {
+#define X(id, A, BC, TWO) {8 * A, 4 * BC, TWO ? 1 : 0, id},
+    LPB_WARP_CONFIGS(X)
+#undef X
+};
+
+static int pick_warp(int m, int n, int kmax) {
+  for (const WarpCfg& c : kWarpCfgs) {
+    if (m > c.rcap || m > 32 || n + kmax > c.ccap) continue;
+    if (kmax > 0 && !c.two) continue;
+    return c.id;
+  }
+  return -1;
+}
+
+bool warp_fits(int m, int n, int kmax) { return pick_warp(m, n, kmax) >= 0; }
+int warp_layout(int m, int n, int kmax) { return pick_warp(m, n, kmax); }
+
+cudaError_t launch_simplex_warp(const SimplexArgs& a, int grid_override, cudaStream_t s,
+                                int* ctas_out) {
+  switch (pick_warp(a.m, a.n, a.kmax)) {
+#define X(id, A, BC, TWO)                                                         \
+  case id:                                                                        \
+    return a.rpc ? launch_w<A, BC, TWO, true>(a, grid_override, s, ctas_out)      \
+                 : launch_w<A, BC, TWO, false>(a, grid_override, s, ctas_out);
+    LPB_WARP_CONFIGS(X)
+#undef X
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace lpb

@@ -27,7 +27,7 @@ GENERAL, HYPERBOX = 0, 1
 OPTIMAL, UNBOUNDED, INFEASIBLE, ITER_LIMIT, NUMERICAL = range(5)
 OK, EINVAL, ENOMEM, ECUDA, ESTATE, ETOOBIG = 0, -1, -2, -3, -4, -5
 DEVICE_PTRS, SHARED_BOX, NO_X, ASYNC, SHARED_AB, NO_TIMING = 1, 2, 4, 8, 16, 32
-CLASS_NAMES = {0: "auto", 1: "S", 2: "M", 3: "L", 4: "R", 5: "H", 6: "T"}
+CLASS_NAMES = {0: "auto", 1: "S", 2: "M", 3: "L", 4: "R", 5: "H", 6: "T", 7: "W"}
 CLASS_IDS = {v: k for k, v in CLASS_NAMES.items()}
 RULE_LPC, RULE_RPC = 0, 1  # lpb_options.pivot_rule
 RULE_IDS = {"LPC": RULE_LPC, "RPC": RULE_RPC}

@@ -14,7 +14,7 @@ from gpu_util import compare, gpu_solve
 
 pytestmark = pytest.mark.gpu
 
-CLASSES = ["S", "R", "M", "L", "T"]
+CLASSES = ["S", "W", "R", "M", "L", "T"]
 
 
 @pytest.mark.parametrize("gen,m,n,B,cl", [
@@ -65,6 +65,8 @@ def test_rpc_parity(klass, gen, m, n, B):
     k = int((b < 0).sum(axis=1).max())
     if klass == "S" and (m > 8 or n > 8):
         pytest.skip("the thread-per-LP class holds m, n <= 8")
+    if klass == "W" and (m > 32 or n + k > 32):
+        pytest.skip("the warp-per-LP class holds m <= 32, n + k <= 32")
     if klass == "T" and not (m <= 128 and n + k <= 100):
         pytest.skip("no row-per-thread layout for this size")
     if klass == "R" and not (m <= 112 and n + k <= 112):

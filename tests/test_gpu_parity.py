@@ -16,7 +16,7 @@ from gpu_util import compare, gpu_solve
 pytestmark = pytest.mark.gpu
 
 GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "lp_fixtures.json")))
-CLASSES = ["S", "R", "M", "L", "T"]
+CLASSES = ["S", "W", "R", "M", "L", "T"]
 
 
 def _row_fits(m, n, k):
@@ -31,6 +31,8 @@ def _skip_class(klass, m, n, k):
         pytest.skip("no row-per-thread layout for this size")
     if klass == "S" and (m > 8 or n > 8):
         pytest.skip("the thread-per-LP class holds m, n <= 8")
+    if klass == "W" and (m > 32 or n + k > 32):
+        pytest.skip("the warp-per-LP class holds m <= 32, n + k <= 32")
 
 
 def _reg_fits(m, n, k):
