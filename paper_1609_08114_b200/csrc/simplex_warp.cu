@@ -48,26 +48,58 @@ __device__ __forceinline__ int w_argmax(bool valid, unsigned long long key, unsi
   return __ffs(__ballot_sync(WFULL, c2 && tie == mt)) - 1;
 }
 
+// Optional phase profiler (-DLPB_PROFILE, scripts/wphase_prof.py): warp 0 of the grid adds
+// clock64() deltas per phase into prof[phase]; prof[15] counts pivots.
+#ifdef LPB_PROFILE
+#define W_MARK(ph)                                   \
+  if (prof_on) {                                     \
+    const long long t_ = clock64();                  \
+    pacc[ph] += t_ - pt;                             \
+    pt = t_;                                         \
+  }
+#else
+#define W_MARK(ph)
+#endif
+
 template <int A, int BC, bool TWO, bool RPC>
 __global__ void __launch_bounds__(32 * W_WARPS) simplex_warp_kernel(SimplexArgs a) {
   const int lane = threadIdx.x & 31;
+#ifdef LPB_PROFILE
+  const bool prof_on = a.prof != nullptr && blockIdx.x == 0 && threadIdx.x < 32;
+  long long pacc[16] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  long long pt = clock64();
+#endif
   const int tr = lane >> 2, tc = lane & 3;
   const int m = a.m, n = a.n;
   const int64_t gw = (int64_t)blockIdx.x * W_WARPS + (threadIdx.x >> 5);
   const int64_t nw = (int64_t)gridDim.x * W_WARPS;
   const bool direct = a.ticket == nullptr;
 
-  int64_t lp = direct ? gw : 0;
-  if (!direct) {
+  // persistent warps take their next LP's ticket one LP ahead and prefetch its A, b, c into
+  // L2 while the current LP is solved (the build's loads then miss HBM only once)
+  auto take_ticket = [&]() -> int64_t {
     int t = 0;
     if (lane == 0) t = atomicAdd(a.ticket, 1);
-    lp = __shfl_sync(WFULL, t, 0);
-  }
+    return __shfl_sync(WFULL, t, 0);
+  };
+  auto prefetch_lp = [&](int64_t q) {
+    if (q >= a.batch) return;
+    const char* pa = reinterpret_cast<const char*>(a.A + q * a.sA);
+    const int64_t abytes = a.sA ? (int64_t)m * n * 8 : 0;
+    for (int64_t off = (int64_t)lane * 128; off < abytes; off += 32 * 128)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(pa + off));
+    if (lane == 0 && a.sb) asm volatile("prefetch.global.L2 [%0];" ::"l"(a.b + q * a.sb));
+    if (lane == 1) asm volatile("prefetch.global.L2 [%0];" ::"l"(a.c + q * (int64_t)n));
+  };
+  int64_t lp = direct ? gw : take_ticket();
+  int64_t lp_next = direct ? lp + nw : take_ticket();
+  if (!direct) prefetch_lp(lp_next);
   while (lp < a.batch) {
     const double* __restrict__ Ak = a.A + lp * a.sA;
     const double* __restrict__ bk = a.b + lp * a.sb;
     const double* __restrict__ ck = a.c + lp * (int64_t)n;
 
+    W_MARK(0)  // ticket / loop
     // ---- build (R7) ----
     const bool rowL = lane < m;
     const double bL = rowL ? __ldg(bk + lane) : 0.0;
@@ -150,6 +182,7 @@ __global__ void __launch_bounds__(32 * W_WARPS) simplex_warp_kernel(SimplexArgs 
       }
     }
 
+    W_MARK(1)  // loads + build
     // ---- Steps 1-3, two phases ----
     int it1 = 0, it2 = 0, stall = 0, phase = (TWO && k > 0) ? 1 : 2, dl = 0;
     bool drive = false;
@@ -176,6 +209,7 @@ __global__ void __launch_bounds__(32 * W_WARPS) simplex_warp_kernel(SimplexArgs 
         double bv = 0.0;
         unsigned bvar = 0xffffffffu;
         int bb = 0;
+        double bd2 = 0.0, bd1 = 0.0;
         if (tr == (l & 7)) {
 #pragma unroll
           for (int b = 0; b < BC; ++b) {
@@ -190,6 +224,8 @@ __global__ void __launch_bounds__(32 * W_WARPS) simplex_warp_kernel(SimplexArgs 
               bv = v;
               bvar = var;
               bb = b;
+              bd2 = d2[b];
+              if constexpr (TWO) bd1 = d1[b];
             }
           }
         }
@@ -197,8 +233,8 @@ __global__ void __launch_bounds__(32 * W_WARPS) simplex_warp_kernel(SimplexArgs 
         if (wl < 0) continue;  // redundant row: the artificial stays basic at 0
         e = __shfl_sync(WFULL, tc + 4 * bb, wl);
         evar = (int)__shfl_sync(WFULL, bvar, wl);
-        dE2 = __shfl_sync(WFULL, d2[bb], wl);
-        if constexpr (TWO) dE1 = __shfl_sync(WFULL, d1[bb], wl);
+        dE2 = __shfl_sync(WFULL, bd2, wl);
+        if constexpr (TWO) dE1 = __shfl_sync(WFULL, bd1, wl);
       } else {
         // Step 1 on thread-row 0 (the replicas are identical across thread-rows)
         bool val = false;
@@ -206,6 +242,7 @@ __global__ void __launch_bounds__(32 * W_WARPS) simplex_warp_kernel(SimplexArgs 
         unsigned long long bu = 0ull;
         unsigned bvar = 0xffffffffu;
         int bb = 0;
+        double bd2 = 0.0, bd1 = 0.0;  // d2 / d1 at the chosen position (static indices only)
         const bool rpc = RPC && !bland;
         const uint64_t pkey = RPC ? rpc_pivot_key(lpkey, it1 + it2) : 0ull;
 #pragma unroll
@@ -227,6 +264,8 @@ __global__ void __launch_bounds__(32 * W_WARPS) simplex_warp_kernel(SimplexArgs 
           bv = take ? v : bv;
           bvar = take ? var : bvar;
           bb = take ? b : bb;
+          bd2 = take ? d2[b] : bd2;
+          if constexpr (TWO) bd1 = take ? d1[b] : bd1;
         }
         val = val && tr == 0;
         const int wl = bland ? warp_argmin(val, 0ull, bvar)
@@ -241,11 +280,12 @@ __global__ void __launch_bounds__(32 * W_WARPS) simplex_warp_kernel(SimplexArgs 
         if (it1 + it2 >= a.max_iter) { st = ST_ITER_LIMIT; break; }
         e = __shfl_sync(WFULL, tc + 4 * bb, wl);
         evar = (int)__shfl_sync(WFULL, bvar, wl);
-        dE2 = __shfl_sync(WFULL, d2[bb], wl);
-        if constexpr (TWO) dE1 = __shfl_sync(WFULL, d1[bb], wl);
+        dE2 = __shfl_sync(WFULL, bd2, wl);
+        if constexpr (TWO) dE1 = __shfl_sync(WFULL, bd1, wl);
         l = -1;
       }
 
+      W_MARK(2)  // Step 1
       // ---- column e: owners (tc == e%4) pick it; shuffles bring it to the ratio lanes and
       //      to every lane's update multipliers ----
       const int be = e >> 2, etc = e & 3;
@@ -270,6 +310,7 @@ __global__ void __launch_bounds__(32 * W_WARPS) simplex_warp_kernel(SimplexArgs 
           vL = (ai == aL) ? v : vL;
         }
       }
+      W_MARK(3)  // column e shuffles
       double theta = 0.0;
       if (!drive) {  // Step 2: ratio test, one row per lane (R1, R2, R5)
         const bool cand = lane < m && vL > a.eps_piv;
@@ -283,6 +324,7 @@ __global__ void __launch_bounds__(32 * W_WARPS) simplex_warp_kernel(SimplexArgs 
         theta = __shfl_sync(WFULL, r, wr);
       }
 
+      W_MARK(4)  // ratio test + argmin
       // ---- Step 3: pivot row l / PE, rank-1 update ----
       const double pe = __shfl_sync(WFULL, vL, l);
       const double rhs_l = __shfl_sync(WFULL, rhs, l);
@@ -298,6 +340,7 @@ __global__ void __launch_bounds__(32 * W_WARPS) simplex_warp_kernel(SimplexArgs 
           for (int ai = 1; ai < A; ++ai) v = (ai == al) ? T[ai][b] : v;
           rv[b] = __shfl_sync(WFULL, v, (ltr << 2) | tc);
         }
+        W_MARK(5)  // pe / row shuffles
         const double rpe = recip_of(pe);
         bool slow_any = false;
 #pragma unroll
@@ -314,6 +357,7 @@ __global__ void __launch_bounds__(32 * W_WARPS) simplex_warp_kernel(SimplexArgs 
           for (int b = 0; b < BC; ++b) prow[b] = ddiv_slow((tc + 4 * b == e) ? 1.0 : rv[b], pe);
           prr = ddiv_slow(rhs_l, pe);
         }
+        W_MARK(6)  // divisions
         // the lane's row L: RHS and basic variable
         rhs = (lane == l) ? prr : __fma_rn(-vL, prr, rhs);
         bkey = (lane == l) ? evar : bkey;
@@ -360,7 +404,12 @@ __global__ void __launch_bounds__(32 * W_WARPS) simplex_warp_kernel(SimplexArgs 
         if (phase == 1) ++it1; else ++it2;
         stall = (theta > 0.0) ? 0 : stall + 1;
       }
+      W_MARK(7)  // update
+#ifdef LPB_PROFILE
+      if (prof_on) pacc[15] += 1;
+#endif
     }
+    W_MARK(8)  // loop exit
 
     // ---- extract (R10) ----
     if (lane == 0) {
@@ -379,14 +428,19 @@ __global__ void __launch_bounds__(32 * W_WARPS) simplex_warp_kernel(SimplexArgs 
       __syncwarp();
       if (st == ST_OPTIMAL && lane < m && bkey >= 0 && bkey < n) xk[bkey] = rhs;
     }
-    if (direct) {
-      lp += nw;  // grid-stride (one pass when the grid covers the batch)
+    W_MARK(9)  // extract
+    lp = lp_next;  // direct: grid-stride (one pass when the grid covers the batch)
+    if (!direct && lp < a.batch) {
+      lp_next = take_ticket();
+      prefetch_lp(lp_next);
     } else {
-      int t = 0;
-      if (lane == 0) t = atomicAdd(a.ticket, 1);
-      lp = __shfl_sync(WFULL, t, 0);
+      lp_next = lp + nw;
     }
   }
+#ifdef LPB_PROFILE
+  if (prof_on && lane == 0)
+    for (int q = 0; q < 16; ++q) atomicAdd((unsigned long long*)&a.prof[q], (unsigned long long)pacc[q]);
+#endif
 }
 
 struct WarpCfg {
