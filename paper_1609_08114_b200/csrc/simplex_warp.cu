@@ -245,28 +245,39 @@ __global__ void __launch_bounds__(32 * W_WARPS) simplex_warp_kernel(SimplexArgs 
         double bd2 = 0.0, bd1 = 0.0;  // d2 / d1 at the chosen position (static indices only)
         const bool rpc = RPC && !bland;
         const uint64_t pkey = RPC ? rpc_pivot_key(lpkey, it1 + it2) : 0ull;
+#define W_SCAN(RULE)                                                \
+  _Pragma("unroll") for (int b = 0; b < BC; ++b) {                 \
+    const double v = p1 ? d1[TWO ? b : 0] : d2[b];                  \
+    const unsigned var = (unsigned)nbv[b];                          \
+    const bool take = v > a.eps_enter && (RULE);                    \
+    val = val || take;                                              \
+    bv = take ? v : bv;                                             \
+    bvar = take ? var : bvar;                                       \
+    bb = take ? b : bb;                                             \
+    bd2 = take ? d2[b] : bd2;                                       \
+    if constexpr (TWO) bd1 = take ? d1[b] : bd1;                    \
+  }
+        if (bland) {  // the lowest variable index (R6)
+          W_SCAN(var < bvar)
+        } else if (rpc) {  // the largest counter-based score (R15)
 #pragma unroll
-        for (int b = 0; b < BC; ++b) {
-          const double v = p1 ? d1[TWO ? b : 0] : d2[b];
-          const unsigned var = (unsigned)nbv[b];
-          const bool cand = v > a.eps_enter;
-          bool take;
-          if (bland) {
-            take = cand && var < bvar;
-          } else if (rpc) {
+          for (int b = 0; b < BC; ++b) {
+            const double v = p1 ? d1[TWO ? b : 0] : d2[b];
+            const unsigned var = (unsigned)nbv[b];
             const unsigned long long u = rpc_score(pkey, (int)var);
-            take = cand && (!val || u > bu || (u == bu && var < bvar));
+            const bool take = v > a.eps_enter && (!val || u > bu || (u == bu && var < bvar));
+            val = val || take;
             bu = take ? u : bu;
-          } else {
-            take = cand && (!val || v > bv || (v == bv && var < bvar));
+            bv = take ? v : bv;
+            bvar = take ? var : bvar;
+            bb = take ? b : bb;
+            bd2 = take ? d2[b] : bd2;
+            if constexpr (TWO) bd1 = take ? d1[b] : bd1;
           }
-          val = val || take;
-          bv = take ? v : bv;
-          bvar = take ? var : bvar;
-          bb = take ? b : bb;
-          bd2 = take ? d2[b] : bd2;
-          if constexpr (TWO) bd1 = take ? d1[b] : bd1;
+        } else {  // LPC: the largest reduced cost, ties to the lowest variable index (R5)
+          W_SCAN(!val || v > bv || (v == bv && var < bvar))
         }
+#undef W_SCAN
         val = val && tr == 0;
         const int wl = bland ? warp_argmin(val, 0ull, bvar)
                              : w_argmax(val, rpc ? bu : okey(bv), bvar);
@@ -289,14 +300,23 @@ __global__ void __launch_bounds__(32 * W_WARPS) simplex_warp_kernel(SimplexArgs 
       // ---- column e: owners (tc == e%4) pick it; shuffles bring it to the ratio lanes and
       //      to every lane's update multipliers ----
       const int be = e >> 2, etc = e & 3;
+      const bool mine = tc == etc;  // this lane holds position e
       double col[A];
-#pragma unroll
-      for (int ai = 0; ai < A; ++ai) {
-        double v = T[ai][0];
-#pragma unroll
-        for (int b = 1; b < BC; ++b) v = (b == be) ? T[ai][b] : v;
-        col[ai] = v;
+      // uniform switch on the position slot: read column e, then the owners zero it (the
+      // update's fma then yields the leaving variable's column, R13)
+#define W_COL(x)                                                    \
+  case x:                                                           \
+    if constexpr ((x) < BC) {                                       \
+      _Pragma("unroll") for (int ai = 0; ai < A; ++ai) {           \
+        col[ai] = T[ai][x];                                         \
+      }                                                             \
+    }                                                               \
+    break;
+      switch (be) {
+        W_COL(0) W_COL(1) W_COL(2) W_COL(3) W_COL(4) W_COL(5) W_COL(6) W_COL(7)
+        default: break;
       }
+#undef W_COL
       double f[A];  // -T[i][e] for the lane's rows
 #pragma unroll
       for (int ai = 0; ai < A; ++ai) f[ai] = -__shfl_sync(WFULL, col[ai], (tr << 2) | etc);
@@ -333,13 +353,22 @@ __global__ void __launch_bounds__(32 * W_WARPS) simplex_warp_kernel(SimplexArgs 
       double prow[BC];
       {
         double rv[BC];
-#pragma unroll
-        for (int b = 0; b < BC; ++b) {
-          double v = T[0][b];
-#pragma unroll
-          for (int ai = 1; ai < A; ++ai) v = (ai == al) ? T[ai][b] : v;
-          rv[b] = __shfl_sync(WFULL, v, (ltr << 2) | tc);
+        const bool lrow = tr == ltr;  // this lane holds row l
+#define W_ROW(x)                                                    \
+  case x:                                                           \
+    if constexpr ((x) < A) {                                        \
+      _Pragma("unroll") for (int b = 0; b < BC; ++b) {             \
+        rv[b] = T[x][b];                                            \
+      }                                                             \
+    }                                                               \
+    break;
+        switch (al) {
+          W_ROW(0) W_ROW(1) W_ROW(2) W_ROW(3)
+          default: break;
         }
+#undef W_ROW
+#pragma unroll
+        for (int b = 0; b < BC; ++b) rv[b] = __shfl_sync(WFULL, rv[b], (ltr << 2) | tc);
         W_MARK(5)  // pe / row shuffles
         const double rpe = recip_of(pe);
         bool slow_any = false;
@@ -362,7 +391,6 @@ __global__ void __launch_bounds__(32 * W_WARPS) simplex_warp_kernel(SimplexArgs 
         rhs = (lane == l) ? prr : __fma_rn(-vL, prr, rhs);
         bkey = (lane == l) ? evar : bkey;
         // objective rows: position e restarts from 0, fma(-d_e, prow_p, d_p)
-        const bool mine = tc == etc;
 #pragma unroll
         for (int b = 0; b < BC; ++b) {
           const bool z = mine && b == be;
@@ -375,10 +403,10 @@ __global__ void __launch_bounds__(32 * W_WARPS) simplex_warp_kernel(SimplexArgs 
         if constexpr (TWO) {
           if (p1) z1 = __fma_rn(-dE1, prr, z1);
         }
-        // tableau: row l and column e zeroed, multiplier of row l = 1
+        // tableau: row l and column e restart from 0, multiplier of row l = 1
 #pragma unroll
         for (int ai = 0; ai < A; ++ai) {
-          const bool isl = tr == ltr && ai == al;
+          const bool isl = lrow && ai == al;
           const double fi = isl ? 1.0 : f[ai];
 #pragma unroll
           for (int b = 0; b < BC; ++b) {
@@ -387,15 +415,23 @@ __global__ void __launch_bounds__(32 * W_WARPS) simplex_warp_kernel(SimplexArgs 
           }
         }
         // position e now holds the leaving variable (dead if artificial, R7)
-#pragma unroll
-        for (int b = 0; b < BC; ++b) {
-          if (mine && b == be) {
-            nbv[b] = leaving >= 0 ? leaving : DEADW;
-            if (leaving < 0) {
-              d2[b] = w_neg_inf();
-              if constexpr (TWO) d1[b] = w_neg_inf();
-            }
+        if (mine) {
+          const int nv = leaving >= 0 ? leaving : DEADW;
+#define W_NBV(x)                                                    \
+  case x:                                                           \
+    if constexpr ((x) < BC) {                                       \
+      nbv[x] = nv;                                                  \
+      if (leaving < 0) {                                            \
+        d2[x] = w_neg_inf();                                        \
+        if constexpr (TWO) d1[x] = w_neg_inf();                     \
+      }                                                             \
+    }                                                               \
+    break;
+          switch (be) {
+            W_NBV(0) W_NBV(1) W_NBV(2) W_NBV(3) W_NBV(4) W_NBV(5) W_NBV(6) W_NBV(7)
+            default: break;
           }
+#undef W_NBV
         }
       }
       if (drive) {
