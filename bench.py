@@ -246,10 +246,15 @@ def main():
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    # one process per GPU; more ranks than GPUs only in the gloo test mode (ranks share GPUs)
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("LPB_DIST_BACKEND", "nccl")  # gloo: 2 ranks on 1 GPU (tests)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     name = args.config
     cfg = lpgen.CONFIGS[name]
     B = args.batch or cfg["B"]
@@ -324,6 +329,22 @@ def main():
 
     # roofline of the dominant kernel (per launch, averaged over the timed launches)
     res = solver.device_results(want_x=True)
+    # the only multi-GPU communication is a final gather of the results to rank
+    # 0 (padded all_gather over NCCL), outside the timed solve; its time is reported apart
+    gather_ms = None
+    if world > 1:
+        try:
+            g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            dist.barrier()
+            g0.record()
+            for key in ("status", "obj", "x"):
+                lpdist.gather_rows(res[key], B * world)
+            g1.record()
+            torch.cuda.synchronize()
+            gather_ms = lpdist.max_over_ranks(g0.elapsed_time(g1),
+                                              device=torch.device("cuda", local))
+        except Exception as ex:  # the gather is reported, never required for the metric
+            print(f"bench: result gather failed: {ex}", file=sys.stderr)
     p = peaks()
     roof_smem = None
     if hyper:
@@ -418,6 +439,7 @@ def main():
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,
+            "gather_ms": gather_ms,
             "clocks": clk.summary(),
             "kernel_ms_per_step": kmean,
         }

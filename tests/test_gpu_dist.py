@@ -1,0 +1,40 @@
+"""The multi-rank bench path on one GPU: two torchrun ranks share the device with the gloo
+backend (LPB_DIST_BACKEND=gloo; on a multi-GPU box each rank owns a GPU and uses NCCL).
+Checks the contract pieces that only exist for N > 1: contiguous per-rank shards (weak
+scaling), the MAX-over-ranks device time, the post-solve results gather, one JSON line."""
+import json
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.mark.parametrize("config,extra", [("cfg1", []), ("cfg4", ["--batch", "200000"]),
+                                          ("cfg2r", ["--batch", "1000"])])
+def test_two_rank_bench_line(config, extra):
+    env = dict(os.environ, LPB_DIST_BACKEND="gloo")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_port()), "bench.py", "--gpus",
+           "2", "--config", config, "--steps", "3", "--warmup", "3", "--e2e-steps", "1", *extra]
+    r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout  # rank 0 alone prints
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["scaling"] == "weak" and d["value"] > 0
+    assert d["config"]["parallelism"].startswith("dp2")
+    assert d["gather_ms"] is not None and d["gather_ms"] > 0
+    assert d["e2e"]["value"] > 0 and d["cpu_baseline"] is None  # baseline at N = 1 only
