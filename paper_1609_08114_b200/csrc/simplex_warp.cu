@@ -192,6 +192,7 @@ __global__ void __launch_bounds__(32 * W_WARPS) simplex_warp_kernel(SimplexArgs 
       const bool p1 = TWO && phase == 1;
       int e, evar, l;
       double dE2 = 0.0, dE1 = 0.0;  // the objective rows' entries at position e
+      W_MARK(10)  // loop head
       if (drive) {
         // R9: drive the next basic artificial out on max |T[l][p]| over live positions
         const unsigned art = __ballot_sync(WFULL, lane < m && bkey < 0);
@@ -274,13 +275,50 @@ __global__ void __launch_bounds__(32 * W_WARPS) simplex_warp_kernel(SimplexArgs 
             bd2 = take ? d2[b] : bd2;
             if constexpr (TWO) bd1 = take ? d1[b] : bd1;
           }
-        } else {  // LPC: the largest reduced cost, ties to the lowest variable index (R5)
-          W_SCAN(!val || v > bv || (v == bv && var < bvar))
+        } else {  // LPC: the largest reduced cost, ties to the lowest variable index (R5):
+                  // a pairwise tree (depth log2 BC) -- each level is a chain of dependent fp64
+                  // compares, so the depth, not the count, sets the latency
+          bool tv[BC];
+          double tx[BC], t2[BC], t1[TWO ? BC : 1];
+          unsigned tvr[BC];
+          int tb[BC];
+#pragma unroll
+          for (int b = 0; b < BC; ++b) {
+            tx[b] = p1 ? d1[TWO ? b : 0] : d2[b];
+            tv[b] = tx[b] > a.eps_enter;
+            tvr[b] = (unsigned)nbv[b];
+            tb[b] = b;
+            t2[b] = d2[b];
+            if constexpr (TWO) t1[b] = d1[b];
+          }
+#pragma unroll
+          for (int st_ = 1; st_ < BC; st_ *= 2) {
+#pragma unroll
+            for (int b = 0; b + st_ < BC; b += 2 * st_) {
+              const int o = b + st_;
+              const bool take = tv[o] && (!tv[b] || tx[o] > tx[b] ||
+                                          (tx[o] == tx[b] && tvr[o] < tvr[b]));
+              tv[b] = tv[b] || tv[o];
+              tx[b] = take ? tx[o] : tx[b];
+              tvr[b] = take ? tvr[o] : tvr[b];
+              tb[b] = take ? tb[o] : tb[b];
+              t2[b] = take ? t2[o] : t2[b];
+              if constexpr (TWO) t1[b] = take ? t1[o] : t1[b];
+            }
+          }
+          val = tv[0];
+          bv = tx[0];
+          bvar = tvr[0];
+          bb = tb[0];
+          bd2 = t2[0];
+          if constexpr (TWO) bd1 = t1[0];
         }
 #undef W_SCAN
+        W_MARK(11)  // scan
         val = val && tr == 0;
         const int wl = bland ? warp_argmin(val, 0ull, bvar)
                              : w_argmax(val, rpc ? bu : okey(bv), bvar);
+        W_MARK(12)  // argmax
         if (wl < 0) {
           if (phase == 2) { st = ST_OPTIMAL; break; }
           if (z1 > a.eps_phase1 * fmax(1.0, binf)) { st = ST_INFEASIBLE; break; }
