@@ -39,6 +39,11 @@ int lpb_selftest_prow(long long* out3);
 /* lpb_selftest_fp64_peak: measured FP64 FMA throughput (TFLOP/s, 2 flop per DFMA) and
  * MUFU.RCP64H throughput (G ops/s) on the current device.  Returns LPB_OK / LPB_ECUDA. */
 int lpb_selftest_fp64_peak(double* dfma_tflops, double* rcp_gops);
+
+/* lpb_selftest_cmp: cycles per step of three dependent chains on one warp: a running fp64
+ * max (DSETP + FSEL), the same on 64-bit integer keys, and a DFMA chain (reference).
+ * Returns LPB_OK / LPB_ECUDA. */
+int lpb_selftest_cmp(long long* out3);
 #ifdef __cplusplus
 }
 #endif

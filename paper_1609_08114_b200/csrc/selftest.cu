@@ -295,3 +295,55 @@ extern "C" int lpb_selftest_fp64_peak(double* dfma_tflops, double* rcp_gops) {
   cudaFree(d);
   return err == cudaSuccess ? LPB_OK : LPB_ECUDA;
 }
+
+// ---- compare-chain latency: fp64 DSETP/FSEL vs 64-bit integer keys (diagnostics) ----
+namespace {
+__global__ void cmp_chain(const double* in, long long* out, int iters) {
+  double v[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = in[(threadIdx.x + i) & 63];
+  long long t0 = clock64();
+  double bv = -1e300;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) bv = (v[i] + it > bv) ? v[i] + it : bv;  // fp64 chain
+  }
+  long long t1 = clock64();
+  unsigned long long bk = 0;
+  unsigned long long kv[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) kv[i] = (unsigned long long)__double_as_longlong(v[i]);
+  long long t2 = clock64();
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) bk = (kv[i] + it > bk) ? kv[i] + it : bk;  // u64 chain
+  }
+  long long t3 = clock64();
+  double dv = 1.0;
+  long long t4 = clock64();
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) dv = __fma_rn(dv, 0.999, v[i]);  // dfma chain (reference)
+  }
+  long long t5 = clock64();
+  if (threadIdx.x == 0) {
+    out[0] = (t1 - t0) / (16LL * iters);
+    out[1] = (t3 - t2) / (16LL * iters);
+    out[2] = (t5 - t4) / (16LL * iters);
+    out[3] = (long long)bv + (long long)bk + (long long)dv;
+  }
+}
+}  // namespace
+
+extern "C" int lpb_selftest_cmp(long long* out3) {
+  double* d_in = nullptr;
+  long long* d_out = nullptr;
+  if (cudaMalloc(&d_in, 64 * sizeof(double)) != cudaSuccess) return LPB_ECUDA;
+  cudaMalloc(&d_out, 8 * sizeof(long long));
+  cudaMemset(d_in, 0, 64 * sizeof(double));
+  cmp_chain<<<1, 32>>>(d_in, d_out, 200);
+  const cudaError_t e = cudaMemcpy(out3, d_out, 3 * sizeof(long long), cudaMemcpyDeviceToHost);
+  cudaFree(d_in);
+  cudaFree(d_out);
+  return e == cudaSuccess ? LPB_OK : LPB_ECUDA;
+}
