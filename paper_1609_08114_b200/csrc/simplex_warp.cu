@@ -14,7 +14,7 @@
 //     lane + a REDUX warp argmin;
 //   * pivot row l: picked with a uniform switch, BC shuffles bring each lane its positions;
 //     every lane divides its own positions by PE and applies fma(f_i, prow_p, T_ip).
-// Warps are independent LPs (4 per CTA); a CTA never synchronises.
+// One warp (LP) per CTA: 32-thread CTAs let the register file hold the most LPs per SM.
 #include <climits>
 
 #include "lpb_fp64.cuh"
@@ -26,7 +26,7 @@ namespace lpb {
 namespace {
 
 constexpr unsigned WFULL = 0xffffffffu;
-constexpr int W_WARPS = 4;  // LPs (warps) per CTA
+constexpr int W_WARPS = 1;  // LPs (warps) per CTA: a 32-thread CTA packs the SM to its register limit
 constexpr int DEADW = INT_MAX;
 
 __device__ __forceinline__ double w_neg_inf() {
