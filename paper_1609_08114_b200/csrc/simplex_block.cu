@@ -295,6 +295,10 @@ __global__ void __launch_bounds__(NT) simplex_block_kernel(SimplexArgs a) {
   s.ctl = reinterpret_cast<Ctl*>(s.colC + 2 * (PULL ? 1 : CL) * RC);
   s.rbuf = reinterpret_cast<double*>(s.ctl + 1);
 
+  // DSMEM may only be touched once every CTA of the cluster is running: one
+  // cluster barrier before the first remote ticket write (racecheck finding).
+  if constexpr (CL > 1) cl.sync();
+
   int par = 0;
   for (;;) {
     if (cl.rank == 0 && tid == 0) {
