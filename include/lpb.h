@@ -149,9 +149,13 @@ int lpb_create(lpb_ctx** out, int64_t batch, int32_t m, int32_t n, int32_t kind,
                const lpb_options* o);
 
 /* Solve the context's batch (size given at create).  A must be NULL for LPB_HYPERBOX.
- * Host pointers (default): inputs are copied host->device through pinned staging in
- * n_chunks chunks on separate streams, each chunk's kernel overlapping the next chunk's copy
- * (PAPER.md:185-206).  With LPB_DEVICE_PTRS the kernels read the caller's device arrays.
+ * Host pointers (default): inputs are copied host->device straight from the caller's arrays
+ * in n_chunks chunks on separate streams, each chunk's kernel overlapping the next chunk's
+ * copy.  Pinned (page-locked) caller arrays give asynchronous, overlapped
+ * copies; pageable ones are staged by the driver and overlap less.  The device input buffers
+ * are allocated by the first host-pointer solve and kept by the context (one A and b -- one
+ * box -- for LPB_SHARED_AB / LPB_SHARED_BOX; grown if a later call needs per-LP arrays).
+ * With LPB_DEVICE_PTRS the kernels read the caller's device arrays.
  * Errors: LPB_EINVAL (NULL required pointer), LPB_ECUDA, LPB_ENOMEM. */
 int lpb_solve_batch(lpb_ctx* c, const double* A, const double* b, const double* cvec,
                     uint32_t flags);

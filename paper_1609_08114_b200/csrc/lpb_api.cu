@@ -53,6 +53,7 @@ struct lpb_ctx {
   double* d_A = nullptr;
   double* d_b = nullptr;
   double* d_c = nullptr;
+  int64_t d_A_elems = 0, d_b_elems = 0;  // allocated sizes (shared-constraint solves need one A, b)
   int* d_ticket = nullptr;  // one counter per chunk
   int* d_kmax = nullptr;
   int* h_kmax = nullptr;    // pinned
@@ -70,6 +71,7 @@ struct lpb_ctx {
   double* rec_T = nullptr;
   int* rec_ints = nullptr;  // rec_e[cap] | nbvar[n+kmax] | bkey[m] | info[4]
   int rec_cap = 0, rec_W = 0;
+  cudaEvent_t rec_ev = nullptr;  // host pipeline: the phase-I record is complete
   char err[256] = {0};
 };
 
@@ -209,6 +211,7 @@ extern "C" int lpb_destroy(lpb_ctx* c) {
   cudaFree(c->rec_rows);
   cudaFree(c->rec_T);
   cudaFree(c->rec_ints);
+  if (c->rec_ev) cudaEventDestroy(c->rec_ev);
   if (c->h_kmax) cudaFreeHost(c->h_kmax);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
@@ -289,9 +292,13 @@ static void fill_args(const lpb_ctx* c, SimplexArgs& a, int64_t lp0, int64_t cnt
 // The size class depends on kmax = max #{b_i < 0} (it sets the condensed width n + k):
 // when a register layout holds even the worst case k = m, no prepass is needed; otherwise
 // one tiny prepass kernel + a 4-byte D2H give kmax first.
+// rec_role (shared-constraint warm start only): REC_SELF records phase I and solves on s;
+// REC_FIRST also signals c->rec_ev after the record; REC_WAIT solves from the record made
+// by the REC_FIRST chunk (waits on rec_ev, no second record).
+enum { REC_SELF = 0, REC_FIRST = 1, REC_WAIT = 2 };
 static int run_general(lpb_ctx* c, cudaStream_t s, int64_t lp0, int64_t cnt, const double* A,
                        const double* b, const double* cv, bool nox, bool sab, int kmax_known,
-                       int* ticket, int* launches) {
+                       int* ticket, int* launches, int rec_role = REC_SELF) {
   int kmax = kmax_known;
   const int forced = c->opt.kernel_class;
   // S (thread per LP) wins on throughput once every SM has a few warps of LPs (measured: 3-4x
@@ -358,6 +365,7 @@ static int run_general(lpb_ctx* c, cudaStream_t s, int64_t lp0, int64_t cnt, con
     if (warm) {
       const int W = c->n + kmax + 1;
       const int cap = a.max_iter + c->m;
+      if (rec_role == REC_WAIT && (c->rec_cap < cap || c->rec_W < W)) return LPB_ESTATE;
       if (c->rec_cap < cap || c->rec_W < W) {
         cudaFree(c->rec_rows);
         cudaFree(c->rec_T);
@@ -379,12 +387,20 @@ static int run_general(lpb_ctx* c, cudaStream_t s, int64_t lp0, int64_t cnt, con
       a.rec_nbvar = c->rec_ints + c->rec_cap;
       a.rec_bkey = a.rec_nbvar + W;
       a.rec_info = a.rec_bkey + c->m;
-      SimplexArgs r = a;
-      r.mode = 1;
-      r.batch = 1;
-      LPB_CUDA(c, launch_simplex_block(cl, r, 0, s, &ctas));
+      if (rec_role == REC_WAIT) {
+        LPB_CUDA(c, cudaStreamWaitEvent(s, c->rec_ev, 0));
+      } else {
+        SimplexArgs r = a;
+        r.mode = 1;
+        r.batch = 1;
+        LPB_CUDA(c, launch_simplex_block(cl, r, 0, s, &ctas));
+        *launches += 1;
+        if (rec_role == REC_FIRST) {
+          if (!c->rec_ev) LPB_CUDA(c, cudaEventCreateWithFlags(&c->rec_ev, cudaEventDisableTiming));
+          LPB_CUDA(c, cudaEventRecord(c->rec_ev, s));
+        }
+      }
       a.mode = 2;
-      *launches += 1;
     }
     LPB_CUDA(c, launch_simplex_block(cl, a, c->opt.grid_ctas, s, &ctas));
   }
@@ -424,17 +440,28 @@ static int run_hyperbox(lpb_ctx* c, cudaStream_t s, int64_t lp0, int64_t cnt, co
   return LPB_OK;
 }
 
-static int ensure_host_path(lpb_ctx* c, int nch) {
+static int ensure_host_path(lpb_ctx* c, int nch, bool shared) {
   const int64_t B = c->batch;
-  if (c->kind == LPB_GENERAL && !c->d_A) {
-    LPB_CUDA(c, cudaMalloc(&c->d_A, sizeof(double) * B * (int64_t)c->m * c->n));
-    LPB_CUDA(c, cudaMalloc(&c->d_b, sizeof(double) * B * (int64_t)c->m));
-    LPB_CUDA(c, cudaMalloc(&c->d_c, sizeof(double) * B * (int64_t)c->n));
+  // LPB_SHARED_AB / LPB_SHARED_BOX stage one A, b (box); a later per-LP solve grows the buffers
+  const int64_t needb = (shared ? 1 : B) * (int64_t)c->m;
+  if (c->kind == LPB_GENERAL) {
+    const int64_t needA = (shared ? 1 : B) * (int64_t)c->m * c->n;
+    if (c->d_A_elems < needA) {
+      cudaFree(c->d_A);
+      c->d_A = nullptr;
+      c->d_A_elems = 0;
+      LPB_CUDA(c, cudaMalloc(&c->d_A, sizeof(double) * needA));
+      c->d_A_elems = needA;
+    }
   }
-  if (c->kind == LPB_HYPERBOX && !c->d_c) {
-    LPB_CUDA(c, cudaMalloc(&c->d_c, sizeof(double) * B * (int64_t)c->n));
-    LPB_CUDA(c, cudaMalloc(&c->d_b, sizeof(double) * B * (int64_t)c->m));
+  if (c->d_b_elems < needb) {
+    cudaFree(c->d_b);
+    c->d_b = nullptr;
+    c->d_b_elems = 0;
+    LPB_CUDA(c, cudaMalloc(&c->d_b, sizeof(double) * needb));
+    c->d_b_elems = needb;
   }
+  if (!c->d_c) LPB_CUDA(c, cudaMalloc(&c->d_c, sizeof(double) * B * (int64_t)c->n));
   while ((int)c->chunk_streams.size() < nch) {
     cudaStream_t s;
     cudaEvent_t ev;
@@ -496,7 +523,7 @@ static int solve_impl(lpb_ctx* c, const double* A, const double* b, const double
                                 : ((B > 100 && in_bytes >= (1 << 20)) ? 10 : 1);
   if (nch > 64) nch = 64;
   if (nch > B) nch = (int)B;
-  int rc = ensure_host_path(c, nch);
+  int rc = ensure_host_path(c, nch, general ? sab : shared);
   if (rc != LPB_OK) return rc;
   int kmax = -1;
   if (general) {  // kmax from the host copy of b (no device round trip inside the pipeline)
@@ -530,7 +557,8 @@ static int solve_impl(lpb_ctx* c, const double* A, const double* b, const double
       LPB_CUDA(c, cudaMemcpyAsync(c->d_c + lp0 * n, cv + lp0 * n, 8 * cnt * n,
                                   cudaMemcpyHostToDevice, s));
       rc = run_general(c, s, lp0, cnt, c->d_A + lp0 * sA, c->d_b + lp0 * sb, c->d_c + lp0 * n,
-                       nox, sab, kmax, c->d_ticket + q, &c->last_launches);
+                       nox, sab, kmax, c->d_ticket + q, &c->last_launches,
+                       sab ? (q == 0 ? REC_FIRST : REC_WAIT) : REC_SELF);
     } else {
       const int64_t bstride = shared ? 0 : 2 * (int64_t)n;
       if (q == 0 || !shared)
