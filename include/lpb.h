@@ -143,7 +143,8 @@ int lpb_default_options(lpb_options* o);
 
 /* Create a context for batches of up to `batch` LPs of size m x n of the given kind.
  * o may be NULL (defaults).  Allocates device result buffers for `batch` LPs.
- * Errors: LPB_EINVAL (batch <= 0, m/n <= 0, kind invalid, hyperbox with m != 2n),
+ * Errors: LPB_EINVAL (batch <= 0, m/n <= 0, kind invalid, hyperbox with m != 2n, a general
+ *         batch above 2^30 LPs -- split it over several calls / contexts),
  *         LPB_ETOOBIG (no size class holds m x n), LPB_ENOMEM, LPB_ECUDA. */
 int lpb_create(lpb_ctx** out, int64_t batch, int32_t m, int32_t n, int32_t kind,
                const lpb_options* o);

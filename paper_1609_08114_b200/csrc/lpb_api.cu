@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <climits>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -136,6 +137,8 @@ extern "C" int lpb_create(lpb_ctx** out, int64_t batch, int32_t m, int32_t n, in
   if (batch <= 0 || m <= 0 || n <= 0) return LPB_EINVAL;
   if (kind != LPB_GENERAL && kind != LPB_HYPERBOX) return LPB_EINVAL;
   if (kind == LPB_HYPERBOX && m != 2 * n) return LPB_EINVAL;
+  // the simplex kernels hand out LPs with 32-bit ticket counters
+  if (kind == LPB_GENERAL && batch > (int64_t)(INT_MAX / 2)) return LPB_EINVAL;
   lpb_options opt;
   lpb_default_options(&opt);
   if (o) {

@@ -93,3 +93,16 @@ def test_option_validation_without_gpu(lib):
     o = lpb.default_options()
     o.struct_size = 8  # an older / foreign layout
     assert lib.lpb_create(ctypes.byref(ctx), 10, 5, 5, 0, ctypes.byref(o)) == -1
+
+
+def test_create_argument_validation_without_gpu(lib):
+    """Shape / kind errors are LPB_EINVAL and sizes no class holds are LPB_ETOOBIG, decided
+    before any CUDA call (include/lpb.h, lpb_create)."""
+    ctx = ctypes.c_void_p()
+    lib.lpb_create.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
+                               ctypes.c_int32, ctypes.c_void_p]
+    for B, m, n, kind in ((0, 5, 5, 0), (10, 0, 5, 0), (10, 5, -1, 0), (10, 5, 5, 7),
+                          (10, 5, 5, 1), (2 ** 31, 5, 5, 0)):
+        assert lib.lpb_create(ctypes.byref(ctx), B, m, n, kind, None) == -1, (B, m, n, kind)
+    assert lib.lpb_create(ctypes.byref(ctx), 10, 600, 600, 0, None) == -5
+    assert lib.lpb_create(None, 10, 5, 5, 0, None) == -1
