@@ -36,10 +36,10 @@ UNIT = "LPs/s"
 # Paper numbers for the exact workload (GeForce GTX 670): hyperbox only.
 PAPER_LPS = {"cfg4": 4001000 / 0.406, "cfg5": 6003000 / 2.388}
 # oracle sample per reference step (bounded CPU work)
-REF_SAMPLE = {"cfg1": 1000, "cfg2": 240, "cfg3": 8, "cfg4": 4001000, "cfg5": 1000000,
+REF_SAMPLE = {"cfg1": 1000, "cfg1m": 1000000, "cfg2": 240, "cfg3": 8, "cfg4": 4001000, "cfg5": 1000000,
               "cfg2s": 240, "cfg3s": 8, "cfg2r": 160, "cfg6": 32, "cfg7": 16, "cfg8": 4,
               "cfg9": 20000, "cfg10": 4000}
-CPU_SAMPLE = {"cfg1": 1000, "cfg2": 1200, "cfg3": 24, "cfg4": 4001000, "cfg5": 6003000,
+CPU_SAMPLE = {"cfg1": 1000, "cfg1m": 1000000, "cfg2": 1200, "cfg3": 24, "cfg4": 4001000, "cfg5": 6003000,
               "cfg2s": 1200, "cfg3s": 24, "cfg2r": 800, "cfg6": 160, "cfg7": 32, "cfg8": 16,
               "cfg9": 50000, "cfg10": 20000}
 L2_BYTES = 126 * 1024 * 1024
@@ -347,6 +347,7 @@ def main():
             print(f"bench: result gather failed: {ex}", file=sys.stderr)
     p = peaks()
     roof_smem = None
+    roof_alu = None
     if hyper:
         traffic_alg = B * (8 * n + 8 * n + 8 + 4)  # read l, write x, obj, status
         achieved = traffic_alg / (kmean / 1e3) / 1e9
@@ -375,6 +376,20 @@ def main():
                 "peak_src": "FP64 unit count x clock: 148 SM x 64 DFMA/clk x 2 x "
                             f"{p['sm_max_mhz']:.0f} MHz (DESIGN.md)",
                 "algorithmic_flops_per_launch": flops}
+        if klass == "S":
+            # thread per LP (tiny LPs): a few hundred flops per LP against its 8(mn+m+n) input
+            # and 8n+20 output bytes -- HBM is the binding roofline (SURVEY §8(d) cfg1 row:
+            # the scaled 1M-LP run); the FP64 figure is kept beside it
+            lp_bytes = 8 * (m * n + m + n) + 8 * n + 8 + 4 + 8
+            if sab:
+                lp_bytes -= 8 * (m * n + m)
+            hb = float(B * lp_bytes)
+            hach = hb / (kmean / 1e3) / 1e9
+            roof_alu = roof
+            roof = {"bound": "hbm", "achieved": hach, "peak": p["hbm_gbs"], "unit": "GB/s",
+                    "frac": hach / p["hbm_gbs"], "traffic": traffic_per_launch(name, B),
+                    "kernel": "simplex (S class)", "peak_src": p["src"],
+                    "algorithmic_bytes_per_launch": hb}
         if klass in ("M", "L"):
             # SMEM-resident tableau (SURVEY §8(d) "%SMEM"): every updated element is one 8-byte
             # SMEM read + one write; peak = 148 SMs x 128 B/clk (one shared wavefront per
@@ -436,6 +451,7 @@ def main():
                        "pivot_rule": lpgen.CONFIGS[name].get("rule", "LPC")},
             "roofline": roof,
             **({"roofline_smem": roof_smem} if roof_smem else {}),
+            **({"roofline_alu": roof_alu} if roof_alu else {}),
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,

@@ -266,6 +266,9 @@ CONFIGS = {
     # 300, 500) at its largest batch
     "cfg9": dict(kind="general", gen="G1", B=50000, m=28, n=28, seed=9),
     "cfg10": dict(kind="general", gen="G1", B=50000, m=50, n=50, seed=10),
+    # cfg1's generator scaled to 1M LPs, where thread-per-LP (S) runs
+    # and the HBM roofline is the relevant bound
+    "cfg1m": dict(kind="general", gen="G1", B=1000000, m=5, n=5, seed=1),
 }
 
 

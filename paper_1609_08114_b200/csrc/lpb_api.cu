@@ -57,6 +57,8 @@ struct lpb_ctx {
   int64_t d_A_elems = 0, d_b_elems = 0;  // allocated sizes (shared-constraint solves need one A, b)
   int* d_ticket = nullptr;  // one counter per chunk
   int* d_kmax = nullptr;
+  int* d_defer = nullptr;      // S class register kernel: deferred (two-phase) LPs, [batch]
+  int* d_defer_cnt = nullptr;  // one counter per chunk
   int* h_kmax = nullptr;    // pinned
   std::vector<cudaStream_t> chunk_streams;
   std::vector<cudaEvent_t> chunk_done;
@@ -211,6 +213,8 @@ extern "C" int lpb_destroy(lpb_ctx* c) {
   cudaFree(c->d_c);
   cudaFree(c->d_ticket);
   cudaFree(c->d_kmax);
+  cudaFree(c->d_defer);
+  cudaFree(c->d_defer_cnt);
   cudaFree(c->rec_rows);
   cudaFree(c->rec_T);
   cudaFree(c->rec_ints);
@@ -283,6 +287,8 @@ static void fill_args(const lpb_ctx* c, SimplexArgs& a, int64_t lp0, int64_t cnt
   a.rpc = c->opt.pivot_rule == LPB_RULE_RPC ? 1 : 0;
   a.rpc_seed = c->opt.rpc_seed;
   a.lp_base = c->opt.lp_index_base + lp0;
+  a.defer_list = nullptr;
+  a.defer_cnt = nullptr;
   // bulk-copy prefetch needs every LP's A to start 16-byte aligned and be a multiple of 16
   // bytes (m*n even), and to fit SMEM next to the register layouts' small SMEM state
   const int64_t bytes = (int64_t)m * n * 8;
@@ -312,14 +318,24 @@ static int run_general(lpb_ctx* c, cudaStream_t s, int64_t lp0, int64_t cnt, con
     if (!thread_fits(c->m, c->n)) return LPB_ETOOBIG;
     SimplexArgs a;  // worst-case width reserved: no prepass
     fill_args(c, a, lp0, cnt, A, b, cv, nox, c->m, ticket, sab);
+    // m, n <= 6: the register kernel, which defers two-phase LPs to the SMEM-slice kernel
+    const bool tiny = tiny_fits(c->m, c->n) && getenv("LPB_NO_TINY") == nullptr;
+    if (tiny) {
+      if (!c->d_defer) {
+        LPB_CUDA(c, cudaMalloc(&c->d_defer, sizeof(int) * c->batch));
+        LPB_CUDA(c, cudaMalloc(&c->d_defer_cnt, sizeof(int) * 64));
+      }
+      a.defer_list = c->d_defer + lp0;
+      a.defer_cnt = c->d_defer_cnt + (ticket - c->d_ticket);  // the chunk's own counter
+    }
     const bool timed = (s == c->stream) && !c->no_timing;
     if (timed) LPB_CUDA(c, cudaEventRecord(c->kev0, s));
-    LPB_CUDA(c, launch_simplex_thread(a, s));
+    LPB_CUDA(c, tiny ? launch_simplex_tiny(a, s) : launch_simplex_thread(a, s));
     if (timed) {
       LPB_CUDA(c, cudaEventRecord(c->kev1, s));
       c->kev_valid = true;
     }
-    *launches += 1;
+    *launches += tiny ? 2 : 1;
     c->last_class = CLASS_S;
     c->last_cluster = 0;
     c->last_grid = 0;

@@ -48,6 +48,11 @@ struct SimplexArgs {
   int* rec_nbvar;      // [n + kmax] position -> nonbasic variable (DEAD: left artificial)
   int* rec_bkey;       // [m] row -> basic-variable key
   int* rec_info;       // {status after phase I (-1: phase II follows), it1, pivots, k}
+  // S class (thread per LP): the register kernel (type-1 LPs) appends the LPs it cannot hold
+  // (b has a negative entry) to defer_list; the SMEM-slice kernel then solves exactly those
+  // (list mode when defer_cnt != nullptr).
+  int* defer_list;     // [batch] launch-relative LP indices
+  int* defer_cnt;      // number of entries, zeroed before the register kernel
 };
 
 struct HyperboxArgs {
@@ -70,6 +75,10 @@ cudaError_t launch_simplex_block(int cl, const SimplexArgs& a, int grid_override
 // ---- S class: one LP per thread (tiny LPs), tableau in a thread-private SMEM slice ----
 bool thread_fits(int m, int n);
 cudaError_t launch_simplex_thread(const SimplexArgs& a, cudaStream_t s);
+// register variant for m, n <= 6: type-1 LPs in registers, the rest deferred to the SMEM-slice
+// kernel (a.defer_list / a.defer_cnt must be set; two launches, the count memset first)
+bool tiny_fits(int m, int n);
+cudaError_t launch_simplex_tiny(const SimplexArgs& a, cudaStream_t s);
 
 // ---- T class: one LP per CTA, one tableau row per thread, rows resident in registers ----
 bool row_fits(int m, int n, int kmax);

@@ -8,6 +8,7 @@
 // lock step (the batch-interleaved SIMT the paper's one-thread-per-LP hyperbox kernel uses,
 // PAPER.md:303).  The worst-case width n+m+1 is reserved, so no prepass is needed.
 // Arithmetic is the oracle's, element for element (same division, fma and sum order).
+#include <algorithm>
 #include <climits>
 
 #include "lpb_fp64.cuh"
@@ -27,14 +28,11 @@ __device__ __forceinline__ double sdiv(double a, double b) {
   return slow ? __ddiv_rn(a, b) : q;
 }
 
-__global__ void __launch_bounds__(S_NT) simplex_thread_kernel(SimplexArgs a) {
-  extern __shared__ __align__(16) double ssm[];
+// Solve LP `lp` of the launch on thread `tid`'s SMEM slice.
+__device__ __forceinline__ void s_solve(const SimplexArgs& a, int64_t lp, int tid, double* ssm) {
   const int m = a.m, n = a.n;
   const int W = n + m + 1;     // positions n+m (worst case k = m) + RHS
   const int S = ((m + 2) * W) | 1;
-  const int tid = threadIdx.x;
-  const int64_t lp = (int64_t)blockIdx.x * S_NT + tid;
-  if (lp >= a.batch) return;
   double* T = ssm + (size_t)tid * S;                                // (m+2) x W, row stride W
   int* ib = reinterpret_cast<int*>(ssm + (size_t)S_NT * S) + tid;  // int slices, stride S_NT
   // int arrays (interleaved across threads: element q of thread t at ib[q * S_NT])
@@ -188,6 +186,21 @@ __global__ void __launch_bounds__(S_NT) simplex_thread_kernel(SimplexArgs a) {
   }
 }
 
+// One LP per thread; in list mode (a.defer_cnt set) a grid-stride loop over the LPs the
+// register kernel (simplex_tiny.cu) deferred.
+__global__ void __launch_bounds__(S_NT) simplex_thread_kernel(SimplexArgs a) {
+  extern __shared__ __align__(16) double ssm[];
+  const int tid = threadIdx.x;
+  if (a.defer_cnt != nullptr) {
+    const int cnt = *a.defer_cnt;
+    for (int64_t q = (int64_t)blockIdx.x * S_NT + tid; q < cnt; q += (int64_t)gridDim.x * S_NT)
+      s_solve(a, a.defer_list[q], tid, ssm);
+    return;
+  }
+  const int64_t lp = (int64_t)blockIdx.x * S_NT + tid;
+  if (lp < a.batch) s_solve(a, lp, tid, ssm);
+}
+
 size_t thread_smem_bytes(int m, int n) {
   const int S = ((m + 2) * (n + m + 1)) | 1;
   return (size_t)S_NT * S * 8 + (size_t)S_NT * (2 * S_MAXM + S_MAXN + S_MAXM) * 4;
@@ -210,7 +223,9 @@ cudaError_t launch_simplex_thread(const SimplexArgs& a, cudaStream_t s) {
     cached = smem;
     cached_dev = dev;
   }
-  const int64_t grid = (a.batch + S_NT - 1) / S_NT;
+  int64_t grid = (a.batch + S_NT - 1) / S_NT;
+  // list mode: the deferred count is only known on the device; a few CTAs per SM cover it
+  if (a.defer_cnt != nullptr) grid = std::min<int64_t>(grid, (int64_t)device_sm_count() * 4);
   simplex_thread_kernel<<<(unsigned)grid, S_NT, smem, s>>>(a);
   return cudaGetLastError();
 }

@@ -1,0 +1,228 @@
+// simplex_tiny.cu — S class, register variant: one LP per THREAD with the whole condensed
+// tableau in registers, for type-1 LPs (b >= 0) of m, n <= 6 (cfg1 is 5x5).
+//
+// The SMEM-slice kernel (simplex_thread.cu) keeps each thread's tableau in shared memory so
+// that the dynamic pivot row / column are plain indexed loads; its occupancy is set by the
+// slice size (~10 warps per SM at 5x5) and every step of the pivot chain waits on SMEM.
+// Here the tableau is a C x C register array (C = compile-time capacity, padded positions
+// hold -inf in the objective row and are never candidates) and the dynamic row l and column
+// e are picked with predicated selects over the fully unrolled array: per pivot C*C DFMAs
+// plus selects, no memory traffic, no barrier.  The pivot arithmetic is the SMEM kernel's
+// (and the oracle's) operation for operation: Step 1 over positions (
+// RPC P:133; Bland after K stalls, reading R6), ratio test by IEEE division,
+// pivot row divided by PE and fma(-f_i, prow_j, T_ij) elsewhere (Listing 1).
+//
+// An LP with some b_i < 0 needs the two-phase method and up to m more
+// positions: the thread appends it to a.defer_list and the SMEM-slice kernel, launched next
+// in list mode, solves exactly those LPs (none for cfg1's type-1 batch).
+#include <algorithm>
+#include <climits>
+
+#include "lpb_fp64.cuh"
+#include "lpb_internal.cuh"
+#include "lpb_rng.cuh"
+
+namespace lpb {
+namespace {
+
+constexpr int TY_MAXC = 6;
+constexpr int DEADV = INT_MAX;
+
+__device__ __forceinline__ double ninf() { return __longlong_as_double(0xfff0000000000000ll); }
+
+template <int C, bool RPC>  // RPC: a separate instantiation keeps LPC's registers
+__global__ void __launch_bounds__(128) simplex_tiny_kernel(SimplexArgs a) {
+  const int64_t lp = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (lp >= a.batch) return;
+  const int m = a.m, n = a.n;
+  const double* __restrict__ Ak = a.A + lp * a.sA;
+  const double* __restrict__ bk = a.b + lp * a.sb;
+  const double* __restrict__ ck = a.c + lp * (int64_t)n;
+
+  // ---- build (type 1: slack basis, R7 with k = 0) ----
+  double rhs[C];
+  bool neg = false;
+#pragma unroll
+  for (int i = 0; i < C; ++i) {
+    rhs[i] = (i < m) ? __ldg(bk + i) : 0.0;
+    neg |= rhs[i] < 0.0;
+  }
+  if (neg) {  // two-phase LP: the SMEM-slice kernel takes it
+    a.defer_list[atomicAdd(a.defer_cnt, 1)] = (int)lp;
+    return;
+  }
+  double T[C][C], d[C];
+  int bkey[C], nbv[C];
+#pragma unroll
+  for (int i = 0; i < C; ++i) {
+#pragma unroll
+    for (int j = 0; j < C; ++j) T[i][j] = (i < m && j < n) ? __ldg(Ak + i * n + j) : 0.0;
+    bkey[i] = n + i;
+  }
+#pragma unroll
+  for (int j = 0; j < C; ++j) {
+    d[j] = (j < n) ? __ldg(ck + j) : ninf();
+    nbv[j] = (j < n) ? j : DEADV;
+  }
+  double z = 0.0;  // objective row's RHS cell (obj = -z, reading R3)
+
+  int st = -1, it2 = 0, stall = 0;
+  const uint64_t lpkey = RPC ? rpc_lp_key(a.rpc_seed, a.lp_base + lp) : 0ull;
+  for (;;) {
+    const bool bland = a.bland_K > 0 && stall >= a.bland_K;
+    const bool rpc = RPC && !bland;
+    // Step 1: entering position (LPC: max d, lowest variable on ties; Bland: lowest variable;
+    // RPC: largest counter-based score, include/lpb.h)
+    const uint64_t pkey = rpc ? rpc_pivot_key(lpkey, it2) : 0ull;
+    int e = -1, ev = INT_MAX;
+    double best = 0.0;
+    uint64_t ub = 0ull;
+#pragma unroll
+    for (int j = 0; j < C; ++j) {
+      const int var = nbv[j];
+      const double dj = d[j];
+      const bool cand = var != DEADV && dj > a.eps_enter;
+      bool take;
+      if (rpc) {
+        const uint64_t u = rpc_score(pkey, var);
+        take = cand && (e < 0 || u > ub || (u == ub && var < ev));
+        ub = take ? u : ub;
+      } else if (bland) {
+        take = cand && var < ev;
+      } else {
+        take = cand && (e < 0 || dj > best || (dj == best && var < ev));
+      }
+      e = take ? j : e;
+      ev = take ? var : ev;
+      best = take ? dj : best;
+    }
+    if (e < 0) { st = ST_OPTIMAL; break; }
+    if (it2 >= a.max_iter) { st = ST_ITER_LIMIT; break; }
+
+    // Step 2: ratio test over rows i < m with T[i][e] > eps_piv (R1, R2, R5)
+    double col[C];
+#pragma unroll
+    for (int i = 0; i < C; ++i) {
+      double v = T[i][0];
+#pragma unroll
+      for (int j = 1; j < C; ++j) v = (e == j) ? T[i][j] : v;
+      col[i] = v;
+    }
+    int l = -1, lkey = INT_MAX;
+    double theta = 0.0;
+#pragma unroll
+    for (int i = 0; i < C; ++i) {
+      const bool val = i < m && col[i] > a.eps_piv;
+      bool slow;
+      double rr = div_fast(rhs[i], val ? col[i] : 1.0, slow);
+      if (slow) rr = ddiv_slow(rhs[i], val ? col[i] : 1.0);
+      const int key = bland ? bkey[i] : i;
+      const bool take = val && (l < 0 || rr < theta || (rr == theta && key < lkey));
+      l = take ? i : l;
+      lkey = take ? key : lkey;
+      theta = take ? rr : theta;
+    }
+    if (l < 0) { st = ST_UNBOUNDED; break; }
+
+    // Step 3: pivot row / PE (IEEE division, R12), fma update of every other row incl. the
+    // objective; position e becomes the leaving variable's column (R13)
+    double pe = col[0], prr = rhs[0];
+    double prow[C];
+#pragma unroll
+    for (int j = 0; j < C; ++j) prow[j] = T[0][j];
+#pragma unroll
+    for (int i = 1; i < C; ++i) {
+      const bool s_ = (l == i);
+      pe = s_ ? col[i] : pe;
+      prr = s_ ? rhs[i] : prr;
+#pragma unroll
+      for (int j = 0; j < C; ++j) prow[j] = s_ ? T[i][j] : prow[j];
+    }
+    const double r = recip_of(pe);
+    double pv[C];
+    bool slow_any = false;
+#pragma unroll
+    for (int j = 0; j < C; ++j) {
+      bool sl;
+      pv[j] = div_with((j == e) ? 1.0 : prow[j], pe, r, sl);
+      slow_any |= sl;
+    }
+    bool slr;
+    double pr = div_with(prr, pe, r, slr);
+    if (slow_any || slr) {  // rare: outside div_with's fast range -> IEEE __ddiv_rn
+#pragma unroll
+      for (int j = 0; j < C; ++j) pv[j] = ddiv_slow((j == e) ? 1.0 : prow[j], pe);
+      pr = ddiv_slow(prr, pe);
+    }
+#pragma unroll
+    for (int i = 0; i < C; ++i) {
+      const bool piv = (i == l);
+      const double f = -col[i];
+#pragma unroll
+      for (int j = 0; j < C; ++j)
+        T[i][j] = piv ? pv[j] : __fma_rn(f, pv[j], (j == e) ? 0.0 : T[i][j]);
+      rhs[i] = piv ? pr : __fma_rn(f, pr, rhs[i]);
+    }
+    double fd = d[0];
+#pragma unroll
+    for (int j = 1; j < C; ++j) fd = (e == j) ? d[j] : fd;
+    fd = -fd;
+#pragma unroll
+    for (int j = 0; j < C; ++j) d[j] = __fma_rn(fd, pv[j], (j == e) ? 0.0 : d[j]);
+    z = __fma_rn(fd, pr, z);
+    // basis swap: row l's basic variable leaves into position e
+    int leaving = bkey[0];
+#pragma unroll
+    for (int i = 1; i < C; ++i) leaving = (l == i) ? bkey[i] : leaving;
+#pragma unroll
+    for (int i = 0; i < C; ++i) bkey[i] = (l == i) ? ev : bkey[i];
+#pragma unroll
+    for (int j = 0; j < C; ++j) nbv[j] = (e == j) ? leaving : nbv[j];
+    ++it2;
+    stall = (theta > 0.0) ? 0 : stall + 1;
+  }
+
+  // ---- extract (R10) ----
+  a.status[lp] = st;
+  a.iters[2 * lp] = 0;
+  a.iters[2 * lp + 1] = it2;
+  a.obj[lp] = (st == ST_OPTIMAL) ? -z
+            : (st == ST_UNBOUNDED) ? __longlong_as_double(0x7ff0000000000000ll)
+                                   : __longlong_as_double(0x7ff8000000000000ll);
+  if (a.x) {
+    double* xk = a.x + lp * (int64_t)n;
+    const double fill = (st == ST_OPTIMAL) ? 0.0 : __longlong_as_double(0x7ff8000000000000ll);
+    for (int j = 0; j < n; ++j) xk[j] = fill;
+    if (st == ST_OPTIMAL) {
+#pragma unroll
+      for (int i = 0; i < C; ++i)
+        if (i < m && bkey[i] < n) xk[bkey[i]] = rhs[i];
+    }
+  }
+}
+
+}  // namespace
+
+bool tiny_fits(int m, int n) { return m <= TY_MAXC && n <= TY_MAXC; }
+
+cudaError_t launch_simplex_tiny(const SimplexArgs& a, cudaStream_t s) {
+  cudaError_t e = cudaMemsetAsync(a.defer_cnt, 0, sizeof(int), s);
+  if (e != cudaSuccess) return e;
+  const int c = std::max(a.m, a.n);
+  // 32-thread CTAs spread a small batch over many SMs; 128 once every SM has a few warps
+  const int nt = a.batch >= (int64_t)device_sm_count() * 128 ? 128 : 32;
+  const unsigned grid = (unsigned)((a.batch + nt - 1) / nt);
+#define LPB_TINY_GO(CC)                                                   \
+  (a.rpc ? simplex_tiny_kernel<CC, true><<<grid, nt, 0, s>>>(a)            \
+         : simplex_tiny_kernel<CC, false><<<grid, nt, 0, s>>>(a))
+  if (c <= 3) LPB_TINY_GO(3);
+  else if (c == 4) LPB_TINY_GO(4);
+  else if (c == 5) LPB_TINY_GO(5);
+  else LPB_TINY_GO(6);
+#undef LPB_TINY_GO
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  return launch_simplex_thread(a, s);  // list mode: the deferred two-phase LPs
+}
+
+}  // namespace lpb

@@ -7,7 +7,7 @@ mkdir -p $OUT
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $OUT/gpu.txt
 timeout 1500 python -m pytest tests -m gpu -q > $OUT/pytest_gpu.txt 2>&1
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.txt 2>&1
-for cf in cfg2 cfg1 cfg4 cfg5 cfg2s cfg2r cfg9 cfg10; do
+for cf in cfg2 cfg1 cfg1m cfg4 cfg5 cfg2s cfg2r cfg9 cfg10; do
   timeout 900 python bench.py --config $cf > $OUT/bench_$cf.json 2> $OUT/bench_$cf.err
 done
 for cf in cfg3 cfg3s; do
@@ -18,7 +18,7 @@ for cf in cfg6 cfg8 cfg7; do
 done
 timeout 300 python bench.py --impl reference --config cfg2 --steps 3 --warmup 1 > $OUT/ref_cfg2.json 2>&1
 # launch lists (cold-cache, serialised: compare shares, not absolutes)
-for cf in cfg2 cfg5 cfg1; do
+for cf in cfg2 cfg5 cfg1 cfg1m; do
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_$cf.csv \
     python bench.py --config $cf --steps 2 --warmup 1 --e2e-steps 0 --no-cpu-baseline > /dev/null 2>&1
 done
@@ -27,6 +27,8 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:simp
   python bench.py --config cfg2 --steps 1 --warmup 0 --e2e-steps 0 --no-cpu-baseline > /dev/null 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:hyperbox -c 1 -o $OUT/full_cfg5 \
   python bench.py --config cfg5 --steps 1 --warmup 0 --e2e-steps 0 --no-cpu-baseline > /dev/null 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:simplex_tiny -c 1 -o $OUT/full_cfg1m \
+  python bench.py --config cfg1m --steps 1 --warmup 0 --e2e-steps 0 --no-cpu-baseline > /dev/null 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:simplex_block -c 1 -o $OUT/full_cfg3 \
   python scripts/prof_one.py cfg3:444 1 > /dev/null 2>&1
 ls -la $OUT

@@ -44,7 +44,8 @@ def test_hyperbox_full_size(name):
 
 @pytest.mark.parametrize("name,sample", [("cfg2r", 300), ("cfg2s", 300), ("cfg3s", 8),
                                          ("cfg6", 24), ("cfg7", 4), ("cfg8", 4),
-                                         ("cfg9", 600), ("cfg10", 300)])
+                                         ("cfg9", 600), ("cfg10", 300),
+                                         ("cfg1m", 3000)])
 def test_next_rows_full_size_sampled(name, sample):
     """The §8(f) rows' bench configs at full size in bench.py's launch configuration (device
     pointers, auto size class, the config's entering rule; shared configs use LPB_SHARED_AB

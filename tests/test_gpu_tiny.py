@@ -1,0 +1,86 @@
+"""GPU parity of the S class's register kernel (csrc/simplex_tiny.cu: one LP per thread, the
+tableau of a type-1 LP with m, n <= 6 in registers; two-phase LPs deferred to the SMEM-slice
+kernel in list mode) against the oracle, element by element, and against the SMEM-slice
+kernel alone (LPB_NO_TINY) bit for bit."""
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+import lpgen
+import oracle
+from gpu_util import compare, gpu_solve
+
+pytestmark = pytest.mark.gpu
+
+SHAPES = [(1, 1), (1, 6), (6, 1), (2, 3), (3, 3), (4, 4), (4, 6), (5, 5), (6, 4), (6, 6)]
+
+
+@pytest.mark.parametrize("m,n", SHAPES)
+@pytest.mark.parametrize("gen", ["G1", "mix", "mixneg", "degneg"])
+def test_tiny_register_kernel_parity(m, n, gen):
+    B = 5000
+    if gen == "G1":
+        A, b, c = lpgen.signed_bounded(B, m, n, 400 + 7 * m + n)
+    elif gen == "degneg":
+        A, b, c = lpgen.degenerate(B, m, n, 401 + 7 * m + n, negative_b=True)
+    else:
+        A, b, c = lpgen.status_mix(B, m, n, 402 + 7 * m + n, infeasible_start=gen == "mixneg")
+    kw = dict(bland_after=2) if gen == "degneg" else {}
+    o = oracle.solve(A, b, c, **kw)
+    g = gpu_solve(A, b, c, kernel_class="S", **kw)
+    compare(A, b, c, g, o)
+    assert g["launch"]["launches"] == 2  # register kernel + the deferred-list kernel
+    gh = gpu_solve(A, b, c, path="host", kernel_class="S", n_chunks=3, **kw)
+    compare(A, b, c, gh, o)
+
+
+@pytest.mark.parametrize("B", [1, 31, 1000, 40000])
+def test_tiny_batch_sizes_and_cta_shapes(B):
+    """32-thread CTAs for small batches, 128 above 148 x 128 LPs; ragged last CTA."""
+    A, b, c = lpgen.status_mix(B, 5, 5, 410, infeasible_start=True)
+    o = oracle.solve(A, b, c)
+    compare(A, b, c, gpu_solve(A, b, c, kernel_class="S"), o)
+
+
+def test_tiny_rpc_iteration_limit_and_no_x():
+    A, b, c = lpgen.status_mix(6000, 6, 5, 411, infeasible_start=True)
+    o = oracle.solve(A, b, c, pivot_rule="RPC", rpc_seed=12)
+    compare(A, b, c, gpu_solve(A, b, c, kernel_class="S", pivot_rule="RPC", rpc_seed=12), o)
+    o = oracle.solve(A, b, c, max_iter=2)
+    g = gpu_solve(A, b, c, kernel_class="S", max_iter=2)
+    compare(A, b, c, g, o)
+    assert np.any(g["status"] == oracle.ITER_LIMIT)
+    g = gpu_solve(A, b, c, kernel_class="S", want_x=False)
+    o = oracle.solve(A, b, c)
+    assert np.array_equal(g["status"], o["status"]) and np.array_equal(g["iters"], o["iters"])
+    assert np.array_equal(g["obj"], o["obj"], equal_nan=True)
+
+
+_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, {root!r}); sys.path.insert(0, {tests!r})
+import lpgen
+from gpu_util import gpu_solve
+A, b, c = lpgen.status_mix(20000, 5, 5, 412, infeasible_start=True)
+g = gpu_solve(A, b, c, kernel_class="S")
+np.savez({out!r}, **{{k: v for k, v in g.items() if k != "launch"}})
+"""
+
+
+def test_tiny_equals_smem_slice_kernel(tmp_path):
+    """The register kernel and the SMEM-slice kernel (LPB_NO_TINY=1) agree bit for bit."""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for env_extra in ({}, {"LPB_NO_TINY": "1"}):
+        out = str(tmp_path / f"r{len(outs)}.npz")
+        env = dict(os.environ, **env_extra)
+        code = _SCRIPT.format(root=root, tests=os.path.join(root, "tests"), out=out)
+        subprocess.run([sys.executable, "-c", code], check=True, env=env, timeout=600)
+        outs.append(np.load(out))
+    for k in ("status", "iters"):
+        assert np.array_equal(outs[0][k], outs[1][k])
+    for k in ("obj", "x"):
+        assert np.array_equal(outs[0][k], outs[1][k], equal_nan=True)
