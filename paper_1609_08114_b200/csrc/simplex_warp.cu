@@ -48,6 +48,123 @@ __device__ __forceinline__ int w_argmax(bool valid, unsigned long long key, unsi
   return __ffs(__ballot_sync(WFULL, c2 && tie == mt)) - 1;
 }
 
+// ---- element layout: type-1 LPs with m, n <= 7, one tableau element (two rows) per lane ----
+// lane = 8r + j owns T[r][j] (v0) and T[r+4][j] (v1): rows 0..6 are the constraints, row 7 the
+// objective row; columns 0..6 are positions, column 7 the RHS.  Every exchange of a pivot is
+// one shuffle (column e, pivot row l, PE), so the chain is Step 1 (one REDUX argmax), one
+// division per RHS lane + one REDUX argmin, PE's reciprocal, one div_with and one fma per
+// element -- the generic layout's switches and per-slot shuffles drop out.  The arithmetic is
+// the oracle's operation for operation (Step 1 PAPER.md:93/132, ratio test P:97/126, pivot
+// P:163-172, R5/R6/R12/R13/R15 in DESIGN.md).
+constexpr int EL_CAP = 7;
+
+template <bool RPC>
+__device__ __forceinline__ void solve_elem(const SimplexArgs& a, int64_t lp, int lane) {
+  const int m = a.m, n = a.n;
+  const int r = lane >> 3, j = lane & 7;
+  const int i0 = r, i1 = r + 4;  // the lane's rows (i1 == 7: the objective row)
+  const double* __restrict__ Ak = a.A + lp * a.sA;
+  const double* __restrict__ bk = a.b + lp * a.sb;
+  const double* __restrict__ ck = a.c + lp * (int64_t)n;
+  double v0, v1;
+  if (j < 7) {
+    v0 = (i0 < m && j < n) ? __ldg(Ak + i0 * n + j) : 0.0;
+    v1 = (i1 == 7) ? ((j < n) ? __ldg(ck + j) : w_neg_inf())
+                   : ((i1 < m && j < n) ? __ldg(Ak + i1 * n + j) : 0.0);
+  } else {  // RHS column; the objective row's RHS cell z starts at 0 (obj = -z, R3)
+    v0 = (i0 < m) ? __ldg(bk + i0) : 0.0;
+    v1 = (i1 < m) ? __ldg(bk + i1) : 0.0;
+  }
+  int bk0 = n + i0, bk1 = n + i1;       // basic variables of the lane's rows (slack basis)
+  int nbv = (j < n) ? j : DEADW;        // nonbasic variable of the lane's position
+  int st = -1, it2 = 0, stall = 0;
+  const uint64_t lpkey = RPC ? rpc_lp_key(a.rpc_seed, a.lp_base + lp) : 0ull;
+  for (;;) {
+    const bool bland = a.bland_K > 0 && stall >= a.bland_K;
+    // Step 1 over the objective row (lanes 24..30)
+    const bool cand = r == 3 && nbv != DEADW && v1 > a.eps_enter;
+    int wl;
+    if (bland) {
+      wl = warp_argmin(cand, 0ull, (unsigned)nbv);
+    } else if (RPC) {
+      const uint64_t u = rpc_score(rpc_pivot_key(lpkey, it2), nbv);
+      wl = w_argmax(cand, u, (unsigned)nbv);
+    } else {
+      wl = w_argmax(cand, okey(v1), (unsigned)nbv);
+    }
+    if (wl < 0) { st = ST_OPTIMAL; break; }
+    if (it2 >= a.max_iter) { st = ST_ITER_LIMIT; break; }
+    const int e = wl & 7;
+    const int ev = __shfl_sync(WFULL, nbv, wl);
+    // column e for the lane's rows
+    const double c0 = __shfl_sync(WFULL, v0, (r << 3) | e);
+    const double c1 = __shfl_sync(WFULL, v1, (r << 3) | e);
+    // Step 2: the RHS lanes (j == 7) divide their two rows, keep the better, REDUX argmin
+    bool val = false;
+    double rr = 0.0;
+    int li = -1, key = 0;
+    if (j == 7) {
+      const bool ok0 = i0 < m && c0 > a.eps_piv, ok1 = i1 < m && c1 > a.eps_piv;
+      bool s0, s1;
+      double q0 = div_fast(v0, ok0 ? c0 : 1.0, s0);
+      double q1 = div_fast(v1, ok1 ? c1 : 1.0, s1);
+      if (s0) q0 = ddiv_slow(v0, ok0 ? c0 : 1.0);
+      if (s1) q1 = ddiv_slow(v1, ok1 ? c1 : 1.0);
+      const int k0 = bland ? bk0 : i0, k1 = bland ? bk1 : i1;
+      const bool take1 = ok1 && (!ok0 || q1 < q0 || (q1 == q0 && k1 < k0));
+      val = ok0 || ok1;
+      rr = take1 ? q1 : q0;
+      li = take1 ? i1 : i0;
+      key = take1 ? k1 : k0;
+    }
+    const int wr = warp_argmin(val, okey(rr), ikey(key));
+    if (wr < 0) { st = ST_UNBOUNDED; break; }
+    const int l = __shfl_sync(WFULL, li, wr);
+    const double theta = __shfl_sync(WFULL, rr, wr);
+    // Step 3: row l's entries for the lane's position (PE at position e), divided by PE
+    const bool hi = l >= 4;
+    const double srcv = hi ? v1 : v0;
+    const int lbase = (l & 3) << 3;
+    const double pe = __shfl_sync(WFULL, srcv, lbase | e);
+    const double prow = __shfl_sync(WFULL, srcv, lbase | j);
+    const int leaving = __shfl_sync(WFULL, hi ? bk1 : bk0, lbase);
+    const double rp = recip_of(pe);
+    const double num = (j == e) ? 1.0 : prow;
+    bool sl;
+    double pv = div_with(num, pe, rp, sl);
+    if (sl) pv = ddiv_slow(num, pe);
+    const bool ze = j == e;
+    v0 = (i0 == l) ? pv : __fma_rn(-c0, pv, ze ? 0.0 : v0);
+    v1 = (i1 == l) ? pv : __fma_rn(-c1, pv, ze ? 0.0 : v1);
+    // basis swap: row l's variable leaves into position e
+    if (i0 == l) bk0 = ev;
+    if (i1 == l) bk1 = ev;
+    if (ze) nbv = leaving;
+    ++it2;
+    stall = (theta > 0.0) ? 0 : stall + 1;
+  }
+  // ---- extract (R10) ----
+  if (lane == 0) {
+    a.status[lp] = st;
+    a.iters[2 * lp] = 0;
+    a.iters[2 * lp + 1] = it2;
+  }
+  if (lane == 31)  // holds z (row 7, RHS column)
+    a.obj[lp] = (st == ST_OPTIMAL) ? -v1
+              : (st == ST_UNBOUNDED) ? __longlong_as_double(0x7ff0000000000000ll)
+                                     : __longlong_as_double(0x7ff8000000000000ll);
+  if (a.x) {
+    double* xk = a.x + lp * (int64_t)n;
+    const double fill = (st == ST_OPTIMAL) ? 0.0 : __longlong_as_double(0x7ff8000000000000ll);
+    if (lane < n) xk[lane] = fill;
+    __syncwarp();
+    if (st == ST_OPTIMAL && j == 7) {
+      if (i0 < m && bk0 < n) xk[bk0] = v0;
+      if (i1 < m && bk1 < n) xk[bk1] = v1;
+    }
+  }
+}
+
 // Optional phase profiler (-DLPB_PROFILE, scripts/wphase_prof.py): warp 0 of the grid adds
 // clock64() deltas per phase into prof[phase]; prof[15] counts pivots.
 #ifdef LPB_PROFILE
@@ -61,7 +178,7 @@ __device__ __forceinline__ int w_argmax(bool valid, unsigned long long key, unsi
 #define W_MARK(ph)
 #endif
 
-template <int A, int BC, bool TWO, bool RPC>
+template <int A, int BC, bool TWO, bool RPC, bool EL>
 __global__ void __launch_bounds__(32 * W_WARPS) simplex_warp_kernel(SimplexArgs a) {
   const int lane = threadIdx.x & 31;
 #ifdef LPB_PROFILE
@@ -106,6 +223,19 @@ __global__ void __launch_bounds__(32 * W_WARPS) simplex_warp_kernel(SimplexArgs 
     const bool negL = rowL && bL < 0.0;
     const unsigned negmask = __ballot_sync(WFULL, negL);
     const int k = __popc(negmask);
+    if constexpr (EL) {  // a type-1 LP up to 7 x 7: the element layout (solve_elem)
+      if (k == 0 && m <= EL_CAP && n <= EL_CAP) {
+        solve_elem<RPC>(a, lp, lane);
+        lp = lp_next;
+        if (!direct && lp < a.batch) {
+          lp_next = take_ticket();
+          prefetch_lp(lp_next);
+        } else {
+          lp_next = lp + nw;
+        }
+        continue;
+      }
+    }
     const int npos = n + k;
     double binf = fabs(bL);
 #pragma unroll
@@ -530,7 +660,9 @@ struct WarpCfg {
 
 template <int A, int BC, bool TWO, bool RPC>
 cudaError_t launch_w(const SimplexArgs& a, int grid_override, cudaStream_t s, int* ctas) {
-  auto kern = simplex_warp_kernel<A, BC, TWO, RPC>;
+  // the smallest layout also carries the element layout for type-1 LPs up to 7 x 7
+  constexpr bool EL = (A == 1) && (BC == 3);
+  auto kern = simplex_warp_kernel<A, BC, TWO, RPC, EL>;
   static int cached_dev = -1, per_sm = 0;
   int dev = 0;
   cudaGetDevice(&dev);
