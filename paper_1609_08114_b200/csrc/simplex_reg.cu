@@ -15,7 +15,9 @@
 //     lazily, each row by exactly one lane), and the winning lane writes the warp's partial
 //     -> barrier 1 -> every thread scans the partials;
 //   * Step 3: the owners of row l publish the RAW row -> barrier 2 ->
-//     every thread divides its own positions by PE and applies T_ip = fma(f_i, prow_p, T_ip)
+//     every thread divides its own positions by PE (with PE's reciprocal, which the winning
+//     ratio lane computed for its own division and passed along in its partial) and applies
+//     T_ip = fma(f_i, prow_p, T_ip)
 //     to its registers (A*BC DFMAs with no per-element branch).  Row l and position e were
 //     zeroed when they were read, so the same fma produces the pivot row (f_l = 1) and the
 //     leaving variable's column.
@@ -59,6 +61,7 @@ struct Part {  // a (value, tie, index) reduction partial
   double v;
   int tie;
   int idx;
+  double rc;  // ratio test: recip_of(T[idx][e]), i.e. PE's reciprocal if this row wins
 };
 
 template <int TR, int TC, int AT, int BC>
@@ -337,7 +340,7 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
         }
         if (lane == 0) sm.part[w] = pw;
         gsync<NT>();
-        const Part q = (lane < NWARP) ? sm.part[lane] : Part{0.0, INT_MAX, -1};
+        const Part q = (lane < NWARP) ? sm.part[lane] : Part{0.0, INT_MAX, -1, 1.0};
         const int ql = warp_argmax(q.idx >= 0, okey(q.v), (unsigned)q.tie);
         gsync<NT>();
         if (ql < 0) continue;  // redundant row: the artificial stays basic at 0
@@ -481,6 +484,7 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
       {
         bool val = false;
         double ratio = 0.0;
+        double rc = 1.0;
         int tie = INT_MAX;
         const int i = rrow;
         if (rlane) {
@@ -495,7 +499,8 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
             if (!drive) {
               val = v > a.eps_piv;
               bool slow;
-              ratio = div_fast(r, val ? v : 1.0, slow);
+              rc = recip_of(val ? v : 1.0);
+              ratio = div_with(r, val ? v : 1.0, rc, slow);  // == div_fast(r, v)
               if (slow) ratio = ddiv_slow(r, val ? v : 1.0);  // rare: outside the fast range
               tie = bland ? sm.bkey[i] : i;
             }
@@ -504,14 +509,15 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
         if (!drive) {
           // the winning lane writes the warp's partial itself (no shuffles)
           const int wl = warp_argmin(val, okey(ratio), ikey(tie));
-          if (lane == (wl < 0 ? 0 : wl)) sm.part[w] = wl < 0 ? Part{0.0, INT_MAX, -1}
-                                                             : Part{ratio, tie, i};
+          if (lane == (wl < 0 ? 0 : wl)) sm.part[w] = wl < 0 ? Part{0.0, INT_MAX, -1, 1.0}
+                                                             : Part{ratio, tie, i, rc};
         }
       }
       LPB_PROF_MARK(2)
       gsync<NT>();  // barrier 1
       LPB_PROF_MARK(3)
       double theta = 0.0;
+      double qrc = 1.0;
       if (!drive) {  // Step 2c: every thread scans the NWARP warp partials (ascending warp)
         Part q = sm.part[0];
 #pragma unroll
@@ -523,6 +529,7 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
         if (q.idx < 0) { st = (phase == 2) ? ST_UNBOUNDED : ST_NUMERICAL; break; }
         l = q.idx;
         theta = q.v;
+        qrc = q.rc;
       }
 
       LPB_PROF_MARK(4)
@@ -561,7 +568,7 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
           }
         }
       }
-      const double rpe = recip_of(pe);
+      const double rpe = drive ? recip_of(pe) : qrc;  // the winning ratio lane's reciprocal
       const double rhs_l = sm.rhs[l];  // current: its lane applied the lazy update in Step 2b
       LPB_PROF_MARK(5)
       gsync<NT>();  // barrier 2

@@ -100,20 +100,25 @@ __device__ __forceinline__ void solve_elem(const SimplexArgs& a, int64_t lp, int
     const double c0 = __shfl_sync(WFULL, v0, (r << 3) | e);
     const double c1 = __shfl_sync(WFULL, v1, (r << 3) | e);
     // Step 2: the RHS lanes (j == 7) divide their two rows, keep the better, REDUX argmin
+    // (div_with with recip_of(c) is div_fast(v, c); the winner's reciprocal is PE's, so it
+    // travels with the partial instead of being recomputed after the argmin)
     bool val = false;
-    double rr = 0.0;
+    double rr = 0.0, rc = 1.0;
     int li = -1, key = 0;
     if (j == 7) {
       const bool ok0 = i0 < m && c0 > a.eps_piv, ok1 = i1 < m && c1 > a.eps_piv;
+      const double d0 = ok0 ? c0 : 1.0, d1 = ok1 ? c1 : 1.0;
+      const double rc0 = recip_of(d0), rc1 = recip_of(d1);
       bool s0, s1;
-      double q0 = div_fast(v0, ok0 ? c0 : 1.0, s0);
-      double q1 = div_fast(v1, ok1 ? c1 : 1.0, s1);
-      if (s0) q0 = ddiv_slow(v0, ok0 ? c0 : 1.0);
-      if (s1) q1 = ddiv_slow(v1, ok1 ? c1 : 1.0);
+      double q0 = div_with(v0, d0, rc0, s0);
+      double q1 = div_with(v1, d1, rc1, s1);
+      if (s0) q0 = ddiv_slow(v0, d0);
+      if (s1) q1 = ddiv_slow(v1, d1);
       const int k0 = bland ? bk0 : i0, k1 = bland ? bk1 : i1;
       const bool take1 = ok1 && (!ok0 || q1 < q0 || (q1 == q0 && k1 < k0));
       val = ok0 || ok1;
       rr = take1 ? q1 : q0;
+      rc = take1 ? rc1 : rc0;
       li = take1 ? i1 : i0;
       key = take1 ? k1 : k0;
     }
@@ -121,6 +126,7 @@ __device__ __forceinline__ void solve_elem(const SimplexArgs& a, int64_t lp, int
     if (wr < 0) { st = ST_UNBOUNDED; break; }
     const int l = __shfl_sync(WFULL, li, wr);
     const double theta = __shfl_sync(WFULL, rr, wr);
+    const double rp = __shfl_sync(WFULL, rc, wr);  // recip_of(PE)
     // Step 3: row l's entries for the lane's position (PE at position e), divided by PE
     const bool hi = l >= 4;
     const double srcv = hi ? v1 : v0;
@@ -128,7 +134,6 @@ __device__ __forceinline__ void solve_elem(const SimplexArgs& a, int64_t lp, int
     const double pe = __shfl_sync(WFULL, srcv, lbase | e);
     const double prow = __shfl_sync(WFULL, srcv, lbase | j);
     const int leaving = __shfl_sync(WFULL, hi ? bk1 : bk0, lbase);
-    const double rp = recip_of(pe);
     const double num = (j == e) ? 1.0 : prow;
     bool sl;
     double pv = div_with(num, pe, rp, sl);
