@@ -265,19 +265,15 @@ static cudaError_t launch_hyperbox_plain(const HyperboxArgs& a, cudaStream_t s) 
   const int S = a.n | 1;
   const size_t smem = sizeof(double) * ((size_t)HB_NT * S + 2 * (size_t)a.n);
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
-  static int cached_dev = -1, per_sm = 0;
-  static size_t cached_smem = (size_t)-1;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (dev != cached_dev || smem != cached_smem) {
+  static LaunchMemo memo;
+  int per_sm = 0;
+  const cudaError_t em = memo.get(smem, &per_sm, [&](int& v) {
     cudaError_t e = cudaFuncSetAttribute(hyperbox_kernel,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, hyperbox_kernel, HB_NT, smem);
-    if (e != cudaSuccess) return e;
-    cached_dev = dev;
-    cached_smem = smem;
-  }
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, hyperbox_kernel, HB_NT, smem);
+  });
+  if (em != cudaSuccess) return em;
   const int64_t ntiles = (a.batch + HB_NT - 1) / HB_NT;
   int64_t grid = (int64_t)per_sm * device_sm_count();
   if (grid > ntiles) grid = ntiles;
@@ -310,17 +306,14 @@ cudaError_t launch_hyperbox(const HyperboxArgs& a, cudaStream_t s) {
     const int bulk_x = (a.x != nullptr && (reinterpret_cast<uintptr_t>(a.x) & 15) == 0 &&
                         getenv("LPB_NO_BULK_X") == nullptr) ? 1 : 0;
     const size_t smem = 16 * 8 + 16 * (size_t)((2 * n + 2 + 1) / 2) + 16 + stages * tile_bytes;
-    static size_t cached_smem = (size_t)-1;
-    static int cached_dev = -1;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (smem != cached_smem || dev != cached_dev) {
-      cudaError_t e = cudaFuncSetAttribute(hyperbox_tma_kernel,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e != cudaSuccess) return e;
-      cached_smem = smem;
-      cached_dev = dev;
-    }
+    static LaunchMemo memo;
+    int ok = 0;
+    const cudaError_t em = memo.get(smem, &ok, [&](int& v) {
+      v = 1;
+      return cudaFuncSetAttribute(hyperbox_tma_kernel,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    });
+    if (em != cudaSuccess) return em;
     int64_t grid = device_sm_count();
     if (grid > nfull) grid = nfull;
     hyperbox_tma_kernel<<<(unsigned)grid, HB_NT, smem, s>>>(a, lpt, stages, bulk_x);

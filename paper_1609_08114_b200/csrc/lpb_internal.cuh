@@ -5,6 +5,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include <mutex>
+
 namespace lpb {
 
 // Per-LP status codes (must equal LPB_OPTIMAL.. in include/lpb.h).
@@ -105,5 +107,49 @@ cudaError_t launch_count_art(const double* b, int64_t batch, int m, int* kmax_de
 cudaError_t launch_hyperbox(const HyperboxArgs& a, cudaStream_t s);
 
 int device_sm_count();
+
+// Thread-safe memo of a launch-configuration query per (device, key) -- function attributes
+// and occupancy are host round trips worth doing once; compute(v) runs under the lock, so
+// host threads driving different GPUs never see a half-written entry.  One key per device is
+// kept (a new key recomputes).
+class LaunchMemo {
+ public:
+  template <class F>
+  cudaError_t get(size_t key, int* out, F&& compute) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> g(mu_);
+    if (dev < 0 || dev >= kDevs) {  // beyond the table: no memo
+      int v = 0;
+      e = compute(v);
+      *out = v;
+      return e;
+    }
+    Entry& en = ent_[dev];
+    if (en.valid && en.key == key) {
+      *out = en.val;
+      return cudaSuccess;
+    }
+    int v = 0;
+    e = compute(v);
+    if (e != cudaSuccess) return e;
+    en.valid = true;
+    en.key = key;
+    en.val = v;
+    *out = v;
+    return cudaSuccess;
+  }
+
+ private:
+  struct Entry {
+    bool valid = false;
+    size_t key = 0;
+    int val = 0;
+  };
+  static constexpr int kDevs = 64;
+  std::mutex mu_;
+  Entry ent_[kDevs];
+};
 
 }  // namespace lpb

@@ -654,12 +654,10 @@ static cudaError_t launch_cl(const SimplexArgs& a, int grid_override, cudaStream
     cfg.attrs = attr;
     cfg.numAttrs = 1;
   }
-  // attribute + occupancy queries are host round trips: cache per (device, smem size)
-  static int cached_dev = -1, resident = 0;
-  static size_t cached_smem = (size_t)-1;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (dev != cached_dev || smem != cached_smem) {
+  // attribute + occupancy queries are host round trips: memo per (device, smem size)
+  static LaunchMemo memo;
+  int resident = 0;
+  const cudaError_t em = memo.get(smem, &resident, [&](int& v) {
     cudaError_t e = cudaFuncSetAttribute(simplex_block_kernel<CL>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -672,18 +670,18 @@ static cudaError_t launch_cl(const SimplexArgs& a, int grid_override, cudaStream
       int per_sm = 0;
       e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, simplex_block_kernel<1>, NT,
                                                         smem);
-      if (e != cudaSuccess) return e;
-      resident = per_sm * sms;
+      v = per_sm * sms;
+      return e;
     } else {
-      cfg.gridDim = dim3(CL * sms);
+      cudaLaunchConfig_t q = cfg;
+      q.gridDim = dim3(CL * sms);
       int clusters = 0;
-      e = cudaOccupancyMaxActiveClusters(&clusters, simplex_block_kernel<CL>, &cfg);
-      if (e != cudaSuccess) return e;
-      resident = clusters * CL;
+      e = cudaOccupancyMaxActiveClusters(&clusters, simplex_block_kernel<CL>, &q);
+      v = clusters * CL;
+      return e;
     }
-    cached_dev = dev;
-    cached_smem = smem;
-  }
+  });
+  if (em != cudaSuccess) return em;
   if (resident <= 0) return cudaErrorInvalidConfiguration;
   int64_t want = a.batch * CL;
   int grid = (int)(want < resident ? want : resident);

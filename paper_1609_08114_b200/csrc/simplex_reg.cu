@@ -754,18 +754,14 @@ cudaError_t launch_one(const SimplexArgs& a, int grid_override, cudaStream_t s, 
   const size_t dsm = AS > 0 ? (size_t)AS * ((BC + 1) / 2) * TR * TC * 16
                             : (a.prefetch ? (size_t)a.m * a.n * 8 : 0);
   // attribute + occupancy queries are host round trips: cache them per (device, smem size)
-  static int cached_dev = -1, per_sm = 0;
-  static size_t cached_dsm = (size_t)-1;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (dev != cached_dev || dsm != cached_dsm) {
+  static LaunchMemo memo;
+  int per_sm = 0;
+  const cudaError_t em = memo.get(dsm, &per_sm, [&](int& v) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm);
     if (e != cudaSuccess) return e;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TR * TC, dsm);
-    if (e != cudaSuccess) return e;
-    cached_dev = dev;
-    cached_dsm = dsm;
-  }
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, kern, TR * TC, dsm);
+  });
+  if (em != cudaSuccess) return em;
   int64_t grid = (int64_t)(per_sm < 1 ? 1 : per_sm) * device_sm_count();
   SimplexArgs d = a;
   if (a.batch <= grid && grid_override <= 0) {

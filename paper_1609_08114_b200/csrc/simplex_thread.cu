@@ -212,17 +212,14 @@ bool thread_fits(int m, int n) { return m <= S_MAXM && n <= S_MAXN; }
 
 cudaError_t launch_simplex_thread(const SimplexArgs& a, cudaStream_t s) {
   const size_t smem = thread_smem_bytes(a.m, a.n);
-  static size_t cached = (size_t)-1;
-  static int cached_dev = -1;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (smem != cached || dev != cached_dev) {
-    cudaError_t e = cudaFuncSetAttribute(simplex_thread_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    cached = smem;
-    cached_dev = dev;
-  }
+  static LaunchMemo memo;
+  int ok = 0;
+  const cudaError_t em = memo.get(smem, &ok, [&](int& v) {
+    v = 1;
+    return cudaFuncSetAttribute(simplex_thread_kernel,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  });
+  if (em != cudaSuccess) return em;
   int64_t grid = (a.batch + S_NT - 1) / S_NT;
   // list mode: the deferred count is only known on the device; a few CTAs per SM cover it
   if (a.defer_cnt != nullptr) grid = std::min<int64_t>(grid, (int64_t)device_sm_count() * 4);

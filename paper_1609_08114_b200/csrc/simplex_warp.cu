@@ -668,15 +668,12 @@ cudaError_t launch_w(const SimplexArgs& a, int grid_override, cudaStream_t s, in
   // the smallest layout also carries the element layout for type-1 LPs up to 7 x 7
   constexpr bool EL = (A == 1) && (BC == 3);
   auto kern = simplex_warp_kernel<A, BC, TWO, RPC, EL>;
-  static int cached_dev = -1, per_sm = 0;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (dev != cached_dev) {
-    const cudaError_t e =
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * W_WARPS, 0);
-    if (e != cudaSuccess) return e;
-    cached_dev = dev;
-  }
+  static LaunchMemo memo;
+  int per_sm = 0;
+  const cudaError_t em = memo.get(0, &per_sm, [&](int& v) {
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, kern, 32 * W_WARPS, 0);
+  });
+  if (em != cudaSuccess) return em;
   const int64_t resident = (int64_t)(per_sm < 1 ? 1 : per_sm) * device_sm_count();
   const int64_t need = (a.batch + W_WARPS - 1) / W_WARPS;
   SimplexArgs d = a;

@@ -283,3 +283,35 @@ def test_extreme_magnitudes(klass, scale_a, scale_b):
     compare(A, b, c, g, o, check_x=False)
     ok = o["status"] == oracle.OPTIMAL
     assert np.array_equal(g["x"][ok], o["x"][ok])
+
+
+def test_concurrent_host_threads_share_the_library():
+    """Host threads driving their own contexts at once (ctypes drops the GIL inside the C
+    ABI): the launchers' memoised attribute / occupancy queries are thread-safe and every
+    thread's results equal a solo run's."""
+    import threading
+
+    cases = [("G1", 5, 5, 3000, "S"), ("G1", 28, 28, 400, "W"), ("G1", 60, 60, 200, "R"),
+             ("G2", 40, 40, 120, "M"), ("G2", 60, 60, 60, "L"), ("mixneg", 20, 20, 500, "T")]
+    inputs = [_gen(g, B, m, n, 500 + m) for g, m, n, B, _ in cases]
+    solo = [gpu_solve(*inp, kernel_class=k) for inp, (*_, k) in zip(inputs, cases)]
+    out = [None] * len(cases)
+    errs = []
+
+    def run(t):
+        try:
+            for _ in range(3):
+                out[t] = gpu_solve(*inputs[t], kernel_class=cases[t][-1])
+        except Exception as ex:  # surfaced below
+            errs.append(ex)
+
+    th = [threading.Thread(target=run, args=(t,)) for t in range(len(cases))]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs, errs
+    for a_, b_ in zip(solo, out):
+        for k in ("status", "iters"):
+            assert np.array_equal(a_[k], b_[k])
+        assert np.array_equal(a_["obj"], b_["obj"], equal_nan=True)
