@@ -8,7 +8,7 @@
  * lpb_options.pivot_rule; ratio test PAPER.md:97,126; pivot PAPER.md:163-172), the two-phase
  * method when the slack basis is infeasible, and the closed-form hyperbox LP
  * (Eq. 6).  One LP per CUDA thread block (or thread-block cluster, or
- * thread), as in PAPER.md:114 ("We assign a CUDA block of threads to solve an LP").
+ * warp, or thread), as in PAPER.md:114 ("We assign a CUDA block of threads to solve an LP").
  *
  * Conventions
  *   - Every call returns int: LPB_OK (0) or a negative error code.  No C++ exception crosses

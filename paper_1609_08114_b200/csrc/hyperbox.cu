@@ -15,6 +15,8 @@
 #include <cstdlib>
 
 #include "lpb_async.cuh"
+#include <algorithm>
+
 #include "lpb_internal.cuh"
 
 namespace lpb {
@@ -290,11 +292,14 @@ cudaError_t launch_hyperbox(const HyperboxArgs& a, cudaStream_t s) {
   // tiles of ~20-56 KB: measured best on cfg4 (n=5: 2x256 LPs, 20 KB, 0.070 vs 0.076 ms at
   // 40 KB and 0.087 ms at 10 KB) and cfg5 (n=28: 256 LPs, 56 KB, 3 stages)
   while (lpt < 8 && (size_t)(2 * lpt) * HB_NT * n * 8 <= 32 * 1024) lpt *= 2;
-  if (const char* v = getenv("LPB_HB_LPT")) lpt = atoi(v);  // tuning hook
+  if (const char* v = getenv("LPB_HB_LPT")) {  // tuning hook: a power of two in [1, 8]
+    const int q = atoi(v);
+    lpt = q >= 8 ? 8 : q >= 4 ? 4 : q >= 2 ? 2 : 1;
+  }
   const size_t tile_bytes = (size_t)lpt * HB_NT * n * 8;
   int stages = (int)((200 * 1024) / tile_bytes);
   int smax = 4;
-  if (const char* v = getenv("LPB_HB_STAGES")) smax = atoi(v);  // tuning hook
+  if (const char* v = getenv("LPB_HB_STAGES")) smax = std::max(2, std::min(8, atoi(v)));  // tuning hook
   if (stages > smax) stages = smax;
   const bool tma = a.shared_box && stages >= 2 && (tile_bytes % 16) == 0 &&
                    (reinterpret_cast<uintptr_t>(a.l) & 15) == 0 && getenv("LPB_NO_TMA") == nullptr;
