@@ -12,10 +12,10 @@
 // The box (2n fp64) is shared by the batch (LPB_SHARED_BOX, the paper's experiment,
 // PAPER.md:313) and lives in SMEM; a per-LP box is read from global memory.
 // This kernel is HBM-bound: 8n bytes in + (8n + 12) bytes out per LP.
+#include <algorithm>
 #include <cstdlib>
 
 #include "lpb_async.cuh"
-#include <algorithm>
 
 #include "lpb_internal.cuh"
 
