@@ -1,4 +1,4 @@
-"""GPU parity of the S class's register kernel (csrc/simplex_tiny.cu: one LP per thread, the
+"""GPU parity of the tiny-LP layouts: the S class's register kernel (csrc/simplex_tiny.cu: one LP per thread, the
 tableau of a type-1 LP with m, n <= 6 in registers; two-phase LPs deferred to the SMEM-slice
 kernel in list mode) against the oracle, element by element, and against the SMEM-slice
 kernel alone (LPB_NO_TINY) bit for bit."""
@@ -84,3 +84,28 @@ def test_tiny_equals_smem_slice_kernel(tmp_path):
         assert np.array_equal(outs[0][k], outs[1][k])
     for k in ("obj", "x"):
         assert np.array_equal(outs[0][k], outs[1][k], equal_nan=True)
+
+
+@pytest.mark.parametrize("m,n", [(1, 1), (2, 2), (3, 7), (7, 3), (5, 5), (7, 7)])
+@pytest.mark.parametrize("gen", ["G1", "mixneg", "deg"])
+def test_warp_element_layout_parity(m, n, gen):
+    """The W class's element layout (type-1 LPs up to 7 x 7, one tableau element pair per
+    lane; two-phase LPs of the same launch take the generic warp layout) against the oracle:
+    LPC, Bland (bland_after=2 on degenerate LPs) and RPC."""
+    B = 3000
+    if gen == "G1":
+        A, b, c = lpgen.signed_bounded(B, m, n, 420 + 7 * m + n)
+    elif gen == "deg":
+        A, b, c = lpgen.degenerate(B, m, n, 421 + 7 * m + n, negative_b=False)
+    else:
+        A, b, c = lpgen.status_mix(B, m, n, 422 + 7 * m + n, infeasible_start=True)
+    kw = dict(bland_after=2) if gen == "deg" else {}
+    o = oracle.solve(A, b, c, **kw)
+    g = gpu_solve(A, b, c, kernel_class="W", **kw)
+    compare(A, b, c, g, o)
+    assert g["launch"]["class"] == "W"
+    o = oracle.solve(A, b, c, pivot_rule="RPC", rpc_seed=m + n)
+    g = gpu_solve(A, b, c, kernel_class="W", pivot_rule="RPC", rpc_seed=m + n)
+    compare(A, b, c, g, o)
+    o = oracle.solve(A, b, c, max_iter=1)
+    compare(A, b, c, gpu_solve(A, b, c, kernel_class="W", max_iter=1), o)
