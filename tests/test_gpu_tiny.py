@@ -1,7 +1,8 @@
-"""GPU parity of the tiny-LP layouts: the S class's register kernel (csrc/simplex_tiny.cu: one LP per thread, the
-tableau of a type-1 LP with m, n <= 6 in registers; two-phase LPs deferred to the SMEM-slice
-kernel in list mode) against the oracle, element by element, and against the SMEM-slice
-kernel alone (LPB_NO_TINY) bit for bit."""
+"""GPU parity of the tiny-LP layouts against the oracle, element by element: the S class's
+register kernel (csrc/simplex_tiny.cu: one LP per thread, a type-1 LP of m, n <= 6 in
+registers, two-phase LPs deferred to the SMEM-slice kernel in list mode; also bit-identical
+to the SMEM-slice kernel alone, LPB_NO_TINY) and the W class's element layout
+(csrc/simplex_warp.cu, type-1 LPs up to 7 x 7)."""
 import os
 import subprocess
 import sys
