@@ -90,13 +90,38 @@ def traffic_per_launch(name, B):
         return None
 
 
+def _measured_hbm(m):
+    """HBM GB/s from the driver-written MEASURED_PEAKS.json: `hbm_gbs`, else any numeric
+    entry under an `hbm` key, preferring the burst figure (our kernels are timed per launch),
+    then sustained; TB/s-sized values are scaled to GB/s."""
+    if isinstance(m.get("hbm_gbs"), (int, float)):
+        return float(m["hbm_gbs"])
+    found = []
+
+    def walk(o, path):
+        if isinstance(o, dict):
+            for k, v in o.items():
+                walk(v, path + (str(k).lower(),))
+        elif isinstance(o, (int, float)) and not isinstance(o, bool) and any("hbm" in t for t in path):
+            found.append((path, float(o)))
+    walk(m, ())
+    for pref in ("burst", "sustained", ""):
+        for path, v in found:
+            if pref in " ".join(path):
+                return v * 1000.0 if v < 100.0 else v
+    return None
+
+
 def peaks():
     p = {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0, "src": "fallback (B200_PROFILING.md)"}
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             m = json.load(f)
-        p.update(hbm_gbs=float(m["hbm_gbs"]), sm_max_mhz=float(m.get("sm_max_mhz", 1965.0)),
-                 src="measured (MEASURED_PEAKS.json)")
+        hbm = _measured_hbm(m)
+        if hbm:
+            p.update(hbm_gbs=hbm, src="measured (MEASURED_PEAKS.json)")
+        if isinstance(m.get("sm_max_mhz"), (int, float)):
+            p["sm_max_mhz"] = float(m["sm_max_mhz"])
     except Exception:
         pass
     # FP64 vector peak from unit counts (DESIGN.md): 148 SMs x 64 FP64 FMA lanes x 2 flop
