@@ -23,9 +23,16 @@ def run(A, b, c, **kw):
 
 
 A, b, c = lpgen.status_mix(64, 6, 6, 1, infeasible_start=True)
+# S: register kernel + deferred two-phase LPs in list mode; W: element layout + generic warps
 for kl in ("S", "W", "R", "T", "M", "L"):
     st, li = run(A, b, c, kernel_class=kl)
     print(kl, li, np.bincount(st, minlength=5))
+A, b, c = lpgen.status_mix(20000, 5, 5, 7, infeasible_start=True)  # 128-thread S CTAs
+st, li = run(A, b, c, kernel_class="S")
+print("S 20000", li, np.bincount(st, minlength=5))
+A, b, c = lpgen.signed_bounded(300, 7, 7, 8)  # W element layout only
+st, li = run(A, b, c, kernel_class="W", pivot_rule="RPC", rpc_seed=1)
+print("W elem RPC", li, np.bincount(st, minlength=5))
 A, b, c = lpgen.twophase_signed(4, 40, 40, 2)
 for cl in (2, 4, 8, 16):
     st, li = run(A, b, c, kernel_class="L", cluster_ctas=cl)
