@@ -76,7 +76,10 @@ def build(verbose: bool = False, force: bool = False, defines: list[str] | None 
 
 
 if __name__ == "__main__":
-    defs = [a for a in sys.argv[1:] if a.startswith("-D")]
+    # -D... defines and -X... / --extra nvcc flags (A/B variants); --variant/--verbose/--force
+    # are this script's own
+    defs = [a for a in sys.argv[1:] if a.startswith("-D") or a.startswith("-X")
+            or (a.startswith("--") and a not in ("--variant", "--verbose", "--force"))]
     if "--variant" in sys.argv:
         import shutil
         vdir = os.path.join(os.path.abspath(sys.argv[sys.argv.index("--variant") + 1]),
