@@ -17,17 +17,25 @@ __device__ __forceinline__ unsigned long long okey(double d) {
 }
 __device__ __forceinline__ unsigned ikey(int t) { return (unsigned)t ^ 0x80000000u; }
 
+// The candidate lanes' lowest and highest lane ids by two independent REDUX (≈ 22 cycles each,
+// issued back to back) instead of VOTE.ballot + FLO (≈ 60 cycles as a dependent pair on
+// sm_100, scripts/ubench/lat_ops.cu): none if lo == 32, unique if lo == hi.
+#define LPB_FIRST_LANE(c1, none_ret)                                                  \
+  const unsigned lane_ = threadIdx.x & 31u;                                          \
+  const unsigned l1 = __reduce_min_sync(kFullMask, (c1) ? lane_ : 32u);              \
+  const unsigned l2 = __reduce_max_sync(kFullMask, (c1) ? lane_ : 0u);               \
+  if (l1 == 32u) return none_ret;                                                    \
+  if (l1 == l2) return (int)l1;
+
 // Warp argmax of (key desc, tie asc) over lanes with `valid`; returns the winner lane or -1.
-// Must be called by all 32 lanes.  Fast path: one REDUX on the key's high word; only when
-// several lanes share it (rare for real-valued data) are the low word and the tie key
-// reduced as well.
+// Must be called by all 32 lanes.  Fast path: one REDUX on the key's high word (+ the lane
+// REDUXes above); only when several lanes share it (rare for real-valued data) are the low
+// word and the tie key reduced as well.
 __device__ __forceinline__ int warp_argmax(bool valid, unsigned long long k, unsigned tie) {
   const unsigned hi = valid ? (unsigned)(k >> 32) : 0u;
   const unsigned mhi = __reduce_max_sync(kFullMask, hi);
   const bool c1 = valid && hi == mhi;
-  const unsigned b1 = __ballot_sync(kFullMask, c1);
-  if (b1 == 0u) return -1;
-  if ((b1 & (b1 - 1u)) == 0u) return __ffs(b1) - 1;
+  LPB_FIRST_LANE(c1, -1)
   const unsigned lo = c1 ? (unsigned)k : 0u;
   const unsigned mlo = __reduce_max_sync(kFullMask, lo);
   const bool c2 = c1 && (unsigned)k == mlo;
@@ -41,9 +49,7 @@ __device__ __forceinline__ int warp_argmin(bool valid, unsigned long long k, uns
   const unsigned hi = valid ? (unsigned)(k >> 32) : 0xffffffffu;
   const unsigned mhi = __reduce_min_sync(kFullMask, hi);
   const bool c1 = valid && hi == mhi;
-  const unsigned b1 = __ballot_sync(kFullMask, c1);
-  if (b1 == 0u) return -1;
-  if ((b1 & (b1 - 1u)) == 0u) return __ffs(b1) - 1;
+  LPB_FIRST_LANE(c1, -1)
   const unsigned lo = c1 ? (unsigned)k : 0xffffffffu;
   const unsigned mlo = __reduce_min_sync(kFullMask, lo);
   const bool c2 = c1 && (unsigned)k == mlo;

@@ -38,9 +38,7 @@ __device__ __forceinline__ int w_argmax(bool valid, unsigned long long key, unsi
   const unsigned hi = valid ? (unsigned)(key >> 32) : 0u;
   const unsigned mhi = __reduce_max_sync(WFULL, hi);
   const bool c1 = valid && hi == mhi;
-  const unsigned b1 = __ballot_sync(WFULL, c1);
-  if (b1 == 0u) return -1;
-  if ((b1 & (b1 - 1u)) == 0u) return __ffs(b1) - 1;
+  LPB_FIRST_LANE(c1, -1)
   const unsigned lo = c1 ? (unsigned)key : 0u;
   const unsigned mlo = __reduce_max_sync(WFULL, lo);
   const bool c2 = c1 && (unsigned)key == mlo;
