@@ -136,10 +136,19 @@ struct Cluster {
 
 // Block-wide (value,key) reduction; result identical in every thread.
 template <int MODE>
+__device__ __forceinline__ int warp_winner(const Cand& c) {
+  const bool valid = c.pos >= 0;
+  if (MODE == MAX_V) return warp_argmax(valid, okey(c.v), (unsigned)c.key);
+  if (MODE == MIN_KEY) return warp_argmin(valid, 0ull, ikey(c.key));
+  return warp_argmin(valid, okey(c.v), ikey(c.key));
+}
+
+template <int MODE>
 __device__ __forceinline__ Cand block_reduce(Cand c, Cand* slots) {
-  c = warp_reduce<MODE>(c);
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (lane == 0) slots[w] = c;
+  // the warp's winning lane writes the partial itself (no shuffles before the barrier)
+  const int wl = warp_winner<MODE>(c);
+  if (lane == (wl < 0 ? 0 : wl)) slots[w] = wl < 0 ? Cand{0.0, 0, -1} : c;
   __syncthreads();
   Cand r{0.0, 0, -1};
   if (lane < NW) r = slots[lane];
