@@ -59,7 +59,9 @@ enum { /* per-LP status (data, not an error) */
   LPB_UNBOUNDED = 1,  /* no leaving variable in phase II                       */
   LPB_INFEASIBLE = 2, /* phase-I optimum w* > eps_phase1*max(1,|b|_inf)         */
   LPB_ITER_LIMIT = 3, /* phase-I + phase-II pivots reached max_iter                           */
-  LPB_NUMERICAL = 4   /* phase I reported unbounded (impossible in exact arithmetic)          */
+  LPB_NUMERICAL = 4,  /* phase I reported unbounded (impossible in exact arithmetic)          */
+  LPB_BAD_HINT = 5    /* not solved: the LP has more b_i < 0 than lpb_options.kmax_hint
+                         promised (obj = NaN, x = NaN, iters = 0)                            */
 };
 
 enum { /* call errors */
@@ -101,9 +103,10 @@ typedef struct {
                           inputs cannot pay for per-chunk copy latency)                       */
   int32_t kernel_class;/* 0 auto; 1 S (thread/LP, m,n <= 8), 2 M (block/LP, SMEM tableau),
                           3 L (2/4-CTA cluster/LP, DSMEM), 4 R (block or warp/LP, register-
-                          resident tableau tiles), 6 T (block/LP, one register-resident row
-                          per thread), 7 W (warp/LP, m <= 32 and n + k <= 32, tableau in
-                          registers, shuffle exchanges); for tests / benches               */
+                          resident tableau tiles), 7 W (warp/LP, m <= 32 and n + k <= 32,
+                          tableau in registers, shuffle exchanges); for tests / benches.
+                          Hyperbox contexts accept 0 or 5 (H).  Any other value (or a class
+                          of the other kind) is LPB_EINVAL at lpb_create                    */
   int32_t grid_ctas;   /* 0 auto; persistent grid size override (scheduling-invariance tests) */
   int32_t cluster_ctas;/* L class cluster size: 0 auto (the smallest of 2/4/8/16 CTAs whose
                           distributed SMEM holds the tableau); 2/4/8/16 forces that size when
@@ -123,6 +126,18 @@ typedef struct {
                           its carried objective row rebuilt by replaying the recorded pivots
                           (bit-identical to solving each LP from scratch; M/L classes, LPC).
                           -1: solve every LP from scratch                                     */
+  int32_t kmax_hint;   /* -1 (default): unknown.  >= 0: the caller promises that no LP of a
+                          solve has more than kmax_hint rows with b_i < 0 -- the paper's LP
+                          "type" (type 1 = feasible slack basis, b >= 0, is
+                          kmax_hint 0; type 2 = infeasible basis, two-phase).  The size class
+                          and register layout depend on k (the condensed width is n + k + 1),
+                          so without a hint a device-pointer solve whose layout depends on k
+                          first runs a tiny prepass kernel and reads its 4-byte result back
+                          (the only host synchronisation inside an LPB_ASYNC solve); with a
+                          hint the solve is ONE kernel launch and never blocks.  An LP that
+                          breaks the promise is not solved: status LPB_BAD_HINT.  Host-pointer
+                          solves scan the host b instead (inside the e2e time) when no hint
+                          is given.  Must be in [-1, m]; else LPB_EINVAL at lpb_create.       */
 } lpb_options;
 
 /* Entering rules (lpb_options.pivot_rule).

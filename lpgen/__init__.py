@@ -34,6 +34,7 @@ __all__ = [
     "shared_polytope",
     "CONFIGS",
     "make_config",
+    "kmax_bound",
 ]
 
 
@@ -270,6 +271,20 @@ CONFIGS = {
     # and the HBM roofline is the relevant bound
     "cfg1m": dict(kind="general", gen="G1", B=1000000, m=5, n=5, seed=1),
 }
+
+
+def kmax_bound(name: str) -> int:
+    """The most rows with b_i < 0 any LP of config `name` can have, by construction of its
+    generator -- the LP "type" the paper's application knows in advance: G1
+    draws b ~ U[1,100) (type 1: 0); G2 draws exactly kk = min(ceil(m/4), m-1) covering rows
+    (type 2).  Passed to the solver as lpb_options.kmax_hint."""
+    cfg = CONFIGS[name]
+    if cfg["kind"] != "general":
+        return -1
+    if cfg["gen"] == "G1":
+        return 0
+    m = cfg["m"]
+    return min(int(math.ceil(m / 4)), m - 1)
 
 
 def make_config(name: str, B: int | None = None):

@@ -3,7 +3,13 @@
     python paper_1609_08114_b200/build.py [--verbose] [--force]
 (run it by path: importing the package first would load a possibly stale liblpb.so)
 
-Development variants (never the product library):
+Development build (never the product library):
+    python paper_1609_08114_b200/build.py --dev
+builds devbuild/paper_1609_08114_b200/ (a copy of the package whose liblpb.so is compiled
+with -DLPB_DEV_HOOKS -- environment switches for A/B experiments and tests of alternative
+paths, lpb_set_profile_buffer -- plus the diagnostic kernels of devsrc/, declared in
+include/dev/lpb_selftest.h).  The product liblpb.so reads no environment variable and
+exports only include/lpb.h.  Other variants:
     python paper_1609_08114_b200/build.py --variant ab/prof -DLPB_PROFILE
 builds a copy of the package under ab/prof/paper_1609_08114_b200/ with extra defines
 (scripts/phase_prof.py and scripts/ab_time.py import it from there).
@@ -26,8 +32,10 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
+DEVSRC = os.path.join(HERE, "devsrc")
 OUT = os.path.join(HERE, "liblpb.so")
 OBJ = os.path.join(HERE, "build_obj")
+DEV_DIR = os.path.join(ROOT, "devbuild", os.path.basename(HERE))
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-Xcompiler", "-fPIC",
@@ -42,11 +50,15 @@ def _stale(obj: str, deps: list[str]) -> bool:
 
 
 def build(verbose: bool = False, force: bool = False, defines: list[str] | None = None,
-          out: str = OUT, obj: str = OBJ) -> str:
+          out: str = OUT, obj: str = OBJ, dev: bool = False) -> str:
     OUT, OBJ = out, obj
     os.makedirs(OBJ, exist_ok=True)
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
-    hdrs = sorted(glob.glob(os.path.join(CSRC, "*.cuh"))) + [os.path.join(ROOT, "include", "lpb.h")]
+    if dev:
+        srcs += sorted(glob.glob(os.path.join(DEVSRC, "*.cu")))
+        defines = ["-DLPB_DEV_HOOKS", *(defines or [])]
+    hdrs = (sorted(glob.glob(os.path.join(CSRC, "*.cuh"))) +
+            sorted(glob.glob(os.path.join(ROOT, "include", "**", "*.h"), recursive=True)))
     objs = []
     jobs = []
     for s in srcs:
@@ -75,12 +87,24 @@ def build(verbose: bool = False, force: bool = False, defines: list[str] | None 
     return OUT
 
 
+def build_dev(verbose: bool = False, force: bool = False) -> str:
+    """The development build (see the module docstring) under devbuild/."""
+    import shutil
+    os.makedirs(DEV_DIR, exist_ok=True)
+    for f in glob.glob(os.path.join(HERE, "*.py")):
+        shutil.copy(f, DEV_DIR)
+    return build(verbose=verbose, force=force, out=os.path.join(DEV_DIR, "liblpb.so"),
+                 obj=os.path.join(DEV_DIR, "build_obj"), dev=True)
+
+
 if __name__ == "__main__":
     # -D... defines and -X... / --extra nvcc flags (A/B variants); --variant/--verbose/--force
     # are this script's own
     defs = [a for a in sys.argv[1:] if a.startswith("-D") or a.startswith("-X")
-            or (a.startswith("--") and a not in ("--variant", "--verbose", "--force"))]
-    if "--variant" in sys.argv:
+            or (a.startswith("--") and a not in ("--variant", "--verbose", "--force", "--dev"))]
+    if "--dev" in sys.argv:
+        print(build_dev(verbose="--verbose" in sys.argv, force="--force" in sys.argv))
+    elif "--variant" in sys.argv:
         import shutil
         vdir = os.path.join(os.path.abspath(sys.argv[sys.argv.index("--variant") + 1]),
                             os.path.basename(HERE))
@@ -88,6 +112,7 @@ if __name__ == "__main__":
         for f in glob.glob(os.path.join(HERE, "*.py")):
             shutil.copy(f, vdir)
         print(build(verbose="--verbose" in sys.argv, force=True, defines=defs,
-                    out=os.path.join(vdir, "liblpb.so"), obj=os.path.join(vdir, "build_obj")))
+                    out=os.path.join(vdir, "liblpb.so"), obj=os.path.join(vdir, "build_obj"),
+                    dev=True))
     else:
         print(build(verbose="--verbose" in sys.argv, force="--force" in sys.argv, defines=defs))

@@ -269,9 +269,9 @@ static cudaError_t launch_hyperbox_plain(const HyperboxArgs& a, cudaStream_t s) 
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
   static LaunchMemo memo;
   int per_sm = 0;
-  const cudaError_t em = memo.get(smem, &per_sm, [&](int& v) {
+  const cudaError_t em = memo.get(smem, &per_sm, [&](int& v, size_t attr) {
     cudaError_t e = cudaFuncSetAttribute(hyperbox_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)attr);
     if (e != cudaSuccess) return e;
     return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, hyperbox_kernel, HB_NT, smem);
   });
@@ -292,31 +292,35 @@ cudaError_t launch_hyperbox(const HyperboxArgs& a, cudaStream_t s) {
   // tiles of ~20-56 KB: measured best on cfg4 (n=5: 2x256 LPs, 20 KB, 0.070 vs 0.076 ms at
   // 40 KB and 0.087 ms at 10 KB) and cfg5 (n=28: 256 LPs, 56 KB, 3 stages)
   while (lpt < 8 && (size_t)(2 * lpt) * HB_NT * n * 8 <= 32 * 1024) lpt *= 2;
+#ifdef LPB_DEV_HOOKS
   if (const char* v = getenv("LPB_HB_LPT")) {  // tuning hook: a power of two in [1, 8]
     const int q = atoi(v);
     lpt = q >= 8 ? 8 : q >= 4 ? 4 : q >= 2 ? 2 : 1;
   }
+#endif
   const size_t tile_bytes = (size_t)lpt * HB_NT * n * 8;
   int stages = (int)((200 * 1024) / tile_bytes);
   int smax = 4;
+#ifdef LPB_DEV_HOOKS
   if (const char* v = getenv("LPB_HB_STAGES")) smax = std::max(2, std::min(8, atoi(v)));  // tuning hook
+#endif
   if (stages > smax) stages = smax;
   const bool tma = a.shared_box && stages >= 2 && (tile_bytes % 16) == 0 &&
-                   (reinterpret_cast<uintptr_t>(a.l) & 15) == 0 && getenv("LPB_NO_TMA") == nullptr;
+                   (reinterpret_cast<uintptr_t>(a.l) & 15) == 0 && !dev_flag("LPB_NO_TMA");
   const int64_t tile_lps = (int64_t)lpt * HB_NT;
   const int64_t nfull = tma ? a.batch / tile_lps : 0;
   if (nfull > 0) {
     // x leaves by bulk store when its tiles are 16-byte aligned (always for cudaMalloc'd x
     // and tile-aligned chunks); otherwise by coalesced per-thread stores
     const int bulk_x = (a.x != nullptr && (reinterpret_cast<uintptr_t>(a.x) & 15) == 0 &&
-                        getenv("LPB_NO_BULK_X") == nullptr) ? 1 : 0;
+                        !dev_flag("LPB_NO_BULK_X")) ? 1 : 0;
     const size_t smem = 16 * 8 + 16 * (size_t)((2 * n + 2 + 1) / 2) + 16 + stages * tile_bytes;
     static LaunchMemo memo;
     int ok = 0;
-    const cudaError_t em = memo.get(smem, &ok, [&](int& v) {
+    const cudaError_t em = memo.get(smem, &ok, [&](int& v, size_t attr) {
       v = 1;
       return cudaFuncSetAttribute(hyperbox_tma_kernel,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)attr);
     });
     if (em != cudaSuccess) return em;
     int64_t grid = device_sm_count();

@@ -110,6 +110,7 @@ extern "C" int lpb_default_options(lpb_options* o) {
   o->rpc_seed = 0;
   o->lp_index_base = 0;
   o->warm_start = 0;
+  o->kmax_hint = -1;
   return LPB_OK;
 }
 
@@ -154,6 +155,15 @@ extern "C" int lpb_create(lpb_ctx** out, int64_t batch, int32_t m, int32_t n, in
   if (opt.cluster_ctas != 0 && opt.cluster_ctas != 2 && opt.cluster_ctas != 4 &&
       opt.cluster_ctas != 8 && opt.cluster_ctas != 16)
     return LPB_EINVAL;
+  if (opt.kmax_hint < -1 || opt.kmax_hint > m) return LPB_EINVAL;
+  {  // kernel_class: a defined class of this kind (an unknown value would silently run auto)
+    const int k = opt.kernel_class;
+    const bool ok = kind == LPB_GENERAL
+                        ? (k == CLASS_AUTO || k == CLASS_S || k == CLASS_M || k == CLASS_L ||
+                           k == CLASS_R || k == CLASS_W)
+                        : (k == CLASS_AUTO || k == CLASS_H);
+    if (!ok) return LPB_EINVAL;
+  }
   if (kind == LPB_GENERAL && !general_fits_any(m, n)) return LPB_ETOOBIG;
   if (kind == LPB_HYPERBOX && (size_t)(n | 1) * 256 * 8 > 200 * 1024) return LPB_ETOOBIG;
 
@@ -183,6 +193,8 @@ extern "C" int lpb_create(lpb_ctx** out, int64_t batch, int32_t m, int32_t n, in
   if (e == cudaSuccess) e = cudaMalloc(&c->d_obj, sizeof(double) * batch);
   if (e == cudaSuccess) e = cudaMalloc(&c->d_x, sizeof(double) * batch * (int64_t)n);
   if (e == cudaSuccess) e = cudaMalloc(&c->d_iters, sizeof(int32_t) * 2 * batch);
+  // hyperbox LPs take no pivots: their iteration counts read as 0 (never uninitialised)
+  if (e == cudaSuccess && kind == LPB_HYPERBOX) e = cudaMemset(c->d_iters, 0, sizeof(int32_t) * 2 * batch);
   if (e == cudaSuccess) e = cudaMalloc(&c->d_ticket, sizeof(int) * 64);
   if (e == cudaSuccess) e = cudaMalloc(&c->d_kmax, sizeof(int));
   if (e == cudaSuccess) e = cudaMallocHost(&c->h_kmax, sizeof(int));
@@ -238,7 +250,6 @@ static int choose_class(const lpb_ctx* c, int kmax, int* cl) {
   *cl = 1;
   if (forced == CLASS_W) return warp_fits(m, n, kmax) ? CLASS_W : -1;
   if (forced == CLASS_R) return reg_fits(m, n, kmax) ? CLASS_R : -1;
-  if (forced == CLASS_T) return row_fits(m, n, kmax) ? CLASS_T : -1;
   if (forced == CLASS_M) return block_fits(1, m, n, kmax) ? CLASS_M : -1;
   const int fcl = c->opt.cluster_ctas;
   if (fcl > 0 && (forced == CLASS_L || forced == CLASS_AUTO)) {
@@ -281,6 +292,7 @@ static void fill_args(const lpb_ctx* c, SimplexArgs& a, int64_t lp0, int64_t cnt
   a.max_iter = c->opt.max_iter > 0 ? c->opt.max_iter : 50 * (n + m);
   a.bland_K = c->opt.bland_after == 0 ? n + m : c->opt.bland_after;
   a.kmax = kmax;
+  a.khint = c->opt.kmax_hint;
   a.ticket = ticket;
   a.mode = 0;
   a.rec_cap = 0;
@@ -296,7 +308,7 @@ static void fill_args(const lpb_ctx* c, SimplexArgs& a, int64_t lp0, int64_t cnt
   const int64_t bytes = (int64_t)m * n * 8;
   a.prof = c->prof;
   a.prefetch = (((uintptr_t)A & 15) == 0 && (m * (int64_t)n) % 2 == 0 && bytes <= 100 * 1024 &&
-                getenv("LPB_NO_PREFETCH") == nullptr) ? 1 : 0;
+                !dev_flag("LPB_NO_PREFETCH")) ? 1 : 0;
 }
 
 // Enqueue the general-LP kernels for one resident chunk on stream s.
@@ -310,7 +322,7 @@ enum { REC_SELF = 0, REC_FIRST = 1, REC_WAIT = 2 };
 static int run_general(lpb_ctx* c, cudaStream_t s, int64_t lp0, int64_t cnt, const double* A,
                        const double* b, const double* cv, bool nox, bool sab, int kmax_known,
                        int* ticket, int* launches, int rec_role = REC_SELF) {
-  int kmax = kmax_known;
+  int kmax = kmax_known >= 0 ? kmax_known : c->opt.kmax_hint;  // the hint: no prepass
   const int forced = c->opt.kernel_class;
   // S (thread per LP) wins on throughput once every SM has a few warps of LPs (measured: 3-4x
   // over the warp-per-LP register layout at 1e5-1e6 LPs of 5x5); below that the warp-per-LP
@@ -321,7 +333,7 @@ static int run_general(lpb_ctx* c, cudaStream_t s, int64_t lp0, int64_t cnt, con
     SimplexArgs a;  // worst-case width reserved: no prepass
     fill_args(c, a, lp0, cnt, A, b, cv, nox, c->m, ticket, sab);
     // m, n <= 6: the register kernel, which defers two-phase LPs to the SMEM-slice kernel
-    const bool tiny = tiny_fits(c->m, c->n) && getenv("LPB_NO_TINY") == nullptr;
+    const bool tiny = tiny_fits(c->m, c->n) && !dev_flag("LPB_NO_TINY");
     if (tiny) {
       if (!c->d_defer) {
         LPB_CUDA(c, cudaMalloc(&c->d_defer, sizeof(int) * c->batch));
@@ -374,8 +386,6 @@ static int run_general(lpb_ctx* c, cudaStream_t s, int64_t lp0, int64_t cnt, con
     LPB_CUDA(c, launch_simplex_warp(a, c->opt.grid_ctas, s, &ctas));
   } else if (klass == CLASS_R) {
     LPB_CUDA(c, launch_simplex_reg(a, c->opt.grid_ctas, s, &ctas));
-  } else if (klass == CLASS_T) {
-    LPB_CUDA(c, launch_simplex_row(a, c->opt.grid_ctas, s, &ctas));
   } else {
     // Shared constraints with an infeasible slack basis (LPB_SHARED_AB, k > 0): phase I
     // depends on A and b only, so it is solved once (mode 1, LP 0) and every LP starts at
@@ -546,8 +556,11 @@ static int solve_impl(lpb_ctx* c, const double* A, const double* b, const double
   if (nch > B) nch = (int)B;
   int rc = ensure_host_path(c, nch, general ? sab : shared);
   if (rc != LPB_OK) return rc;
-  int kmax = -1;
-  if (general) {  // kmax from the host copy of b (no device round trip inside the pipeline)
+  // e2e time starts here: the host scan of b below (when there is no kmax_hint) is part of
+  // the end-to-end solve
+  LPB_CUDA(c, cudaEventRecord(c->ev0, c->stream));
+  int kmax = c->opt.kmax_hint;
+  if (general && kmax < 0) {  // kmax from the host copy of b (no device round trip inside the pipeline)
     int best = 0;
     for (int64_t k = 0; k < (sab ? 1 : B); ++k) {
       int cnt = 0;
@@ -557,7 +570,6 @@ static int solve_impl(lpb_ctx* c, const double* A, const double* b, const double
     }
     kmax = best;
   }
-  LPB_CUDA(c, cudaEventRecord(c->ev0, c->stream));
   for (int q = 0; q < nch; ++q) {
     const int64_t lp0 = B * q / nch, lp1 = B * (q + 1) / nch, cnt = lp1 - lp0;
     cudaStream_t s = c->chunk_streams[q];
@@ -665,11 +677,13 @@ extern "C" int lpb_last_timing(lpb_ctx* c, double* solve_ms, double* e2e_ms) {
   return LPB_OK;
 }
 
+#ifdef LPB_DEV_HOOKS  // development build only (include/dev/lpb_selftest.h)
 extern "C" int lpb_set_profile_buffer(lpb_ctx* c, long long* dev_buf) {
   if (!c) return LPB_EINVAL;
   c->prof = dev_buf;
   return LPB_OK;
 }
+#endif
 
 extern "C" int lpb_last_kernel_timing(lpb_ctx* c, double* kernel_ms) {
   if (!c || !kernel_ms) return LPB_EINVAL;

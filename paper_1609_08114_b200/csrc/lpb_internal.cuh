@@ -3,6 +3,7 @@
 #pragma once
 #include <cstddef>
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include <mutex>
@@ -11,11 +12,13 @@ namespace lpb {
 
 // Per-LP status codes (must equal LPB_OPTIMAL.. in include/lpb.h).
 enum : int32_t { ST_OPTIMAL = 0, ST_UNBOUNDED = 1, ST_INFEASIBLE = 2, ST_ITER_LIMIT = 3,
-                 ST_NUMERICAL = 4 };
+                 ST_NUMERICAL = 4, ST_BAD_HINT = 5 };
 
 // Size classes (lpb_options.kernel_class / lpb_last_launch_info).
+// (6 was a row-per-thread register class, removed in round 2: never auto-selected and
+// measured 6 % slower than R on its only candidate sizes; the value stays unused)
 enum : int32_t { CLASS_AUTO = 0, CLASS_S = 1, CLASS_M = 2, CLASS_L = 3, CLASS_R = 4,
-                 CLASS_H = 5, CLASS_T = 6, CLASS_W = 7 };
+                 CLASS_H = 5, CLASS_W = 7 };
 
 struct SimplexArgs {
   int64_t batch;
@@ -32,6 +35,8 @@ struct SimplexArgs {
   int max_iter;     // > 0
   int bland_K;      // > 0: Bland mode after K consecutive degenerate pivots; <= 0: never
   int kmax;         // layout capacity for artificial (b_i < 0) rows
+  int khint;        // lpb_options.kmax_hint (-1: none): an LP with more b_i < 0 reports
+                    // ST_BAD_HINT unsolved (the caller broke its promise)
   int* ticket;      // persistent-scheduler counter, zeroed before each launch
   int prefetch;     // R class: A (m*n*8 bytes, 16-B aligned per LP) is bulk-prefetched to SMEM
   long long* prof;  // optional per-CTA phase cycle counters (diagnostics), normally null
@@ -82,11 +87,6 @@ cudaError_t launch_simplex_thread(const SimplexArgs& a, cudaStream_t s);
 bool tiny_fits(int m, int n);
 cudaError_t launch_simplex_tiny(const SimplexArgs& a, cudaStream_t s);
 
-// ---- T class: one LP per CTA, one tableau row per thread, rows resident in registers ----
-bool row_fits(int m, int n, int kmax);
-cudaError_t launch_simplex_row(const SimplexArgs& a, int grid_override, cudaStream_t s,
-                               int* ctas_out);
-
 // ---- R class: one LP per CTA (one warp for small LPs), tableau resident in registers ----
 bool reg_fits(int m, int n, int kmax);
 int reg_layout(int m, int n, int kmax);  // the layout id the R class would use (-1: none)
@@ -108,10 +108,23 @@ cudaError_t launch_hyperbox(const HyperboxArgs& a, cudaStream_t s);
 
 int device_sm_count();
 
-// Thread-safe memo of a launch-configuration query per (device, key) -- function attributes
-// and occupancy are host round trips worth doing once; compute(v) runs under the lock, so
-// host threads driving different GPUs never see a half-written entry.  One key per device is
-// kept (a new key recomputes).
+// Development-build switches (A/B experiments, tests of alternative paths): read from the
+// environment only when compiled with -DLPB_DEV_HOOKS (build.py --dev); the product library
+// never reads the environment.
+#ifdef LPB_DEV_HOOKS
+inline bool dev_flag(const char* name) { return std::getenv(name) != nullptr; }
+#else
+inline constexpr bool dev_flag(const char*) { return false; }
+#endif
+
+// Thread-safe memo of a launch-configuration query per (device, key): function attributes
+// and occupancy are host round trips worth doing once.  compute(v, attr) runs under the lock
+// and must set cudaFuncAttributeMaxDynamicSharedMemorySize to `attr`, which is the largest
+// key (dynamic SMEM size) this memo has seen on the device: the attribute is only ever RAISED,
+// so a launch that another host thread configured for a larger size is never invalidated by
+// a concurrent smaller one (the launch itself happens after the lock is released).  The
+// occupancy result is computed for the key's own size.  Up to kSlots keys per device are
+// kept (round-robin replacement).
 class LaunchMemo {
  public:
   template <class F>
@@ -120,20 +133,27 @@ class LaunchMemo {
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
     std::lock_guard<std::mutex> g(mu_);
-    if (dev < 0 || dev >= kDevs) {  // beyond the table: no memo
+    if (dev < 0 || dev >= kDevs) {  // beyond the table: no memo (the attribute still only grows)
+      size_t& mx = spill_attr_;
+      if (key > mx) mx = key;
       int v = 0;
-      e = compute(v);
+      e = compute(v, mx);
       *out = v;
       return e;
     }
-    Entry& en = ent_[dev];
-    if (en.valid && en.key == key) {
-      *out = en.val;
-      return cudaSuccess;
-    }
+    Dev& d = dev_[dev];
+    for (const Entry& en : d.ent)
+      if (en.valid && en.key == key) {
+        *out = en.val;
+        return cudaSuccess;
+      }
+    const size_t attr = key > d.attr_max ? key : d.attr_max;
     int v = 0;
-    e = compute(v);
+    e = compute(v, attr);
     if (e != cudaSuccess) return e;
+    d.attr_max = attr;
+    Entry& en = d.ent[d.next];
+    d.next = (d.next + 1) % kSlots;
     en.valid = true;
     en.key = key;
     en.val = v;
@@ -147,9 +167,15 @@ class LaunchMemo {
     size_t key = 0;
     int val = 0;
   };
-  static constexpr int kDevs = 64;
+  static constexpr int kDevs = 64, kSlots = 8;
+  struct Dev {
+    Entry ent[kSlots];
+    int next = 0;
+    size_t attr_max = 0;
+  };
   std::mutex mu_;
-  Entry ent_[kDevs];
+  size_t spill_attr_ = 0;
+  Dev dev_[kDevs];
 };
 
 }  // namespace lpb

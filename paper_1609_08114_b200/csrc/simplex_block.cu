@@ -360,7 +360,8 @@ __global__ void __launch_bounds__(NT) simplex_block_kernel(SimplexArgs a) {
     const int Wa = cnt + 1;                               // + RHS at local column cnt
     const int Wp = (Wa + 1) & ~1;                         // whole 128-bit pairs
     const int g0 = cl.rank * Q;
-    if (k > a.kmax) st = ST_NUMERICAL;  // cannot happen: kmax comes from the prepass
+    if (k > a.kmax) st = ST_NUMERICAL;  // cannot happen: kmax comes from the prepass / hint
+    if (a.khint >= 0 && k > a.khint) st = ST_BAD_HINT;
     const int npos = n + k, Wr = npos + 1;              // record row: positions, then RHS
     int phase = (k > 0) ? 1 : 2;
 
@@ -666,9 +667,9 @@ static cudaError_t launch_cl(const SimplexArgs& a, int grid_override, cudaStream
   // attribute + occupancy queries are host round trips: memo per (device, smem size)
   static LaunchMemo memo;
   int resident = 0;
-  const cudaError_t em = memo.get(smem, &resident, [&](int& v) {
+  const cudaError_t em = memo.get(smem, &resident, [&](int& v, size_t attr) {
     cudaError_t e = cudaFuncSetAttribute(simplex_block_kernel<CL>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)attr);
     if (e != cudaSuccess) return e;
     if constexpr (CL > 8) {  // 16-CTA clusters are a non-portable (opt-in) size on sm_100
       e = cudaFuncSetAttribute(simplex_block_kernel<CL>,

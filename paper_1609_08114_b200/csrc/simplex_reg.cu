@@ -196,7 +196,8 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
 #pragma unroll
     for (int q = 0; q < NWARP; ++q) binf = fmax(binf, sm.part[q].v);
     const int npos = n + k;
-    int st = (m > RCAP || npos > CCAP || (!TWO && k > 0)) ? ST_NUMERICAL : -1;
+    int st = (a.khint >= 0 && k > a.khint) ? ST_BAD_HINT
+           : (m > RCAP || npos > CCAP || (!TWO && k > 0)) ? ST_NUMERICAL : -1;
     for (int p = tid; p < CCAP; p += NT)
       sm.nbvar[p] = (p < n) ? p : (p < npos ? n + sm.negrows[p - n] : DEADV);
     for (int i = m + tid; i < RCAP; i += NT) sm.rhs[i] = 0.0;
@@ -756,8 +757,8 @@ cudaError_t launch_one(const SimplexArgs& a, int grid_override, cudaStream_t s, 
   // attribute + occupancy queries are host round trips: cache them per (device, smem size)
   static LaunchMemo memo;
   int per_sm = 0;
-  const cudaError_t em = memo.get(dsm, &per_sm, [&](int& v) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm);
+  const cudaError_t em = memo.get(dsm, &per_sm, [&](int& v, size_t attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)attr);
     if (e != cudaSuccess) return e;
     return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, kern, TR * TC, dsm);
   });
@@ -788,12 +789,14 @@ static const RegCfg kCfgs[] = {
 };
 
 static int pick_cfg(int m, int n, int kmax) {
-  // experiment hook: LPB_REG_CFG=<id> forces one layout when it fits
+#ifdef LPB_DEV_HOOKS
+  // experiment hook (development build): LPB_REG_CFG=<id> forces one layout when it fits
   if (const char* f = getenv("LPB_REG_CFG")) {
     const int id = atoi(f);
     for (const RegCfg& c : kCfgs)
       if (c.id == id && m <= c.rcap && n + kmax <= c.ccap && (kmax == 0 || c.two)) return id;
   }
+#endif
   for (const RegCfg& c : kCfgs) {
     if (m > c.rcap || n + kmax > c.ccap) continue;
     if (kmax > 0 && !c.two) continue;

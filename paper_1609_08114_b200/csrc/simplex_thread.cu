@@ -57,6 +57,7 @@ __device__ __forceinline__ void s_solve(const SimplexArgs& a, int64_t lp, int ti
     }
   }
   const int npos = n + k, rhs = npos;  // RHS at column npos
+  const bool bad_hint = a.khint >= 0 && k > a.khint;
   for (int i = 0; i < m; ++i) {
     const bool ng = bkey(i) < 0;
     double* row = T + i * W;
@@ -77,7 +78,7 @@ __device__ __forceinline__ void s_solve(const SimplexArgs& a, int64_t lp, int ti
       T[(m + 1) * W + j] = acc;
     }
 
-  int st = -1, it1 = 0, it2 = 0, stall = 0, phase = k > 0 ? 1 : 2;
+  int st = bad_hint ? ST_BAD_HINT : -1, it1 = 0, it2 = 0, stall = 0, phase = k > 0 ? 1 : 2;
   const uint64_t lpkey = a.rpc ? rpc_lp_key(a.rpc_seed, a.lp_base + lp) : 0ull;
   auto pivot = [&](int l, int e, int nrow) {
     const double pe = T[l * W + e];
@@ -214,10 +215,10 @@ cudaError_t launch_simplex_thread(const SimplexArgs& a, cudaStream_t s) {
   const size_t smem = thread_smem_bytes(a.m, a.n);
   static LaunchMemo memo;
   int ok = 0;
-  const cudaError_t em = memo.get(smem, &ok, [&](int& v) {
+  const cudaError_t em = memo.get(smem, &ok, [&](int& v, size_t attr) {
     v = 1;
     return cudaFuncSetAttribute(simplex_thread_kernel,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)attr);
   });
   if (em != cudaSuccess) return em;
   int64_t grid = (a.batch + S_NT - 1) / S_NT;

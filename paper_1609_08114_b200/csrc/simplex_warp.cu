@@ -243,7 +243,8 @@ __global__ void __launch_bounds__(32 * W_WARPS) simplex_warp_kernel(SimplexArgs 
     double binf = fabs(bL);
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) binf = fmax(binf, __shfl_xor_sync(WFULL, binf, off));
-    int st = (m > 8 * A || npos > 4 * BC || (!TWO && k > 0)) ? ST_NUMERICAL : -1;
+    int st = (a.khint >= 0 && k > a.khint) ? ST_BAD_HINT
+           : (m > 8 * A || npos > 4 * BC || (!TWO && k > 0)) ? ST_NUMERICAL : -1;
     double rhs = negL ? -bL : bL;                 // RHS of row `lane`
     int bkey = negL ? (lane - m) : (n + lane);    // key of row `lane`'s basic variable
     double T[A][BC];
@@ -668,7 +669,7 @@ cudaError_t launch_w(const SimplexArgs& a, int grid_override, cudaStream_t s, in
   auto kern = simplex_warp_kernel<A, BC, TWO, RPC, EL>;
   static LaunchMemo memo;
   int per_sm = 0;
-  const cudaError_t em = memo.get(0, &per_sm, [&](int& v) {
+  const cudaError_t em = memo.get(0, &per_sm, [&](int& v, size_t) {
     return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, kern, 32 * W_WARPS, 0);
   });
   if (em != cudaSuccess) return em;

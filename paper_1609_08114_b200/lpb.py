@@ -24,10 +24,10 @@ if not os.path.exists(LIB_PATH):
 _lib = ctypes.CDLL(LIB_PATH)
 
 GENERAL, HYPERBOX = 0, 1
-OPTIMAL, UNBOUNDED, INFEASIBLE, ITER_LIMIT, NUMERICAL = range(5)
+OPTIMAL, UNBOUNDED, INFEASIBLE, ITER_LIMIT, NUMERICAL, BAD_HINT = range(6)
 OK, EINVAL, ENOMEM, ECUDA, ESTATE, ETOOBIG = 0, -1, -2, -3, -4, -5
 DEVICE_PTRS, SHARED_BOX, NO_X, ASYNC, SHARED_AB, NO_TIMING = 1, 2, 4, 8, 16, 32
-CLASS_NAMES = {0: "auto", 1: "S", 2: "M", 3: "L", 4: "R", 5: "H", 6: "T", 7: "W"}
+CLASS_NAMES = {0: "auto", 1: "S", 2: "M", 3: "L", 4: "R", 5: "H", 7: "W"}
 CLASS_IDS = {v: k for k, v in CLASS_NAMES.items()}
 RULE_LPC, RULE_RPC = 0, 1  # lpb_options.pivot_rule
 RULE_IDS = {"LPC": RULE_LPC, "RPC": RULE_RPC}
@@ -51,6 +51,7 @@ class Options(ctypes.Structure):
         ("rpc_seed", ctypes.c_uint64),
         ("lp_index_base", ctypes.c_int64),
         ("warm_start", ctypes.c_int32),
+        ("kmax_hint", ctypes.c_int32),
     ]
 
 
@@ -74,8 +75,6 @@ _lib.lpb_last_launch_shape.argtypes = [P, ctypes.POINTER(ctypes.c_int32),
 _lib.lpb_destroy.argtypes = [P]
 _lib.lpb_strerror.argtypes = [ctypes.c_int]
 _lib.lpb_strerror.restype = ctypes.c_char_p
-_lib.lpb_selftest_div.argtypes = [P, P, P, ctypes.c_int64, ctypes.POINTER(ctypes.c_int64)]
-_lib.lpb_selftest_div.restype = ctypes.c_int
 _lib.lpb_last_error.argtypes = [P]
 _lib.lpb_last_error.restype = ctypes.c_char_p
 for _f in ("lpb_default_options", "lpb_create", "lpb_solve_batch", "lpb_solve_batch_into",

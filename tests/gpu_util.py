@@ -11,6 +11,25 @@ TOL_OBJ = 1e-9  # BASELINE.json north_star: objective within 1e-9 * max(1, |obj|
 TOL_RES = 1e-9  # primal residual (absolute; scaled form as documented fallback, C20)
 
 
+def dev_lib():
+    """The development build of the library (devbuild/, build.py --dev): the product
+    liblpb.so plus diagnostic entry points (include/dev/lpb_selftest.h) and the A/B switches
+    read from the environment.  Tests use it only for those diagnostics."""
+    import ctypes
+    import os
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    path = os.path.join(root, "devbuild", "paper_1609_08114_b200", "liblpb.so")
+    assert os.path.exists(path), "development build missing: python paper_1609_08114_b200/build.py --dev"
+    lib = ctypes.CDLL(path)
+    P = ctypes.c_void_p
+    lib.lpb_selftest_div.argtypes = [P, P, P, ctypes.c_int64, ctypes.POINTER(ctypes.c_int64)]
+    lib.lpb_selftest_div.restype = ctypes.c_int
+    return lib
+
+
+DEV_ROOT = "devbuild"  # sys.path entry (relative to the repo) whose package is the dev build
+
+
 def gpu_solve(A, b, c, *, path="device", want_x=True, **opts):
     import torch
 

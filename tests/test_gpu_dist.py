@@ -38,3 +38,17 @@ def test_two_rank_bench_line(config, extra):
     assert d["config"]["parallelism"].startswith("dp2")
     assert d["gather_ms"] is not None and d["gather_ms"] > 0
     assert d["e2e"]["value"] > 0 and d["cpu_baseline"] is None  # baseline at N = 1 only
+
+
+@pytest.mark.parametrize("case", ["G1", "G2", "cfg2r", "cfg5"])
+def test_two_rank_sharded_parity(case):
+    """N = 2 (two ranks sharing the test box's GPU over gloo): each rank solves its
+    contiguous shard through the C ABI, the gathered results equal the N = 1 solve of the
+    whole batch bit for bit and the oracle on a sample (tests/dist_parity_worker.py)."""
+    env = dict(os.environ, LPB_DIST_BACKEND="gloo")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_port()),
+           os.path.join("tests", "dist_parity_worker.py"), case]
+    r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
+    assert f"PARITY-OK {case}" in r.stdout, r.stdout

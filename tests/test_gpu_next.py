@@ -14,7 +14,7 @@ from gpu_util import compare, gpu_solve
 
 pytestmark = pytest.mark.gpu
 
-CLASSES = ["S", "W", "R", "M", "L", "T"]
+CLASSES = ["S", "W", "R", "M", "L"]
 
 
 @pytest.mark.parametrize("gen,m,n,B,cl", [
@@ -67,8 +67,6 @@ def test_rpc_parity(klass, gen, m, n, B):
         pytest.skip("the thread-per-LP class holds m, n <= 8")
     if klass == "W" and (m > 32 or n + k > 32):
         pytest.skip("the warp-per-LP class holds m <= 32, n + k <= 32")
-    if klass == "T" and not (m <= 128 and n + k <= 100):
-        pytest.skip("no row-per-thread layout for this size")
     if klass == "R" and not (m <= 112 and n + k <= 112):
         pytest.skip("no register layout for this size")
     seed = 0xC0FFEE + m

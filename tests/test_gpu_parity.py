@@ -16,19 +16,12 @@ from gpu_util import compare, gpu_solve
 pytestmark = pytest.mark.gpu
 
 GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "lp_fixtures.json")))
-CLASSES = ["S", "W", "R", "M", "L", "T"]
-
-
-def _row_fits(m, n, k):
-    # mirrors the instantiated row-per-thread layouts in csrc/simplex_row.cu
-    return m <= 128 and n + k <= 100
+CLASSES = ["S", "W", "R", "M", "L"]
 
 
 def _skip_class(klass, m, n, k):
     if klass == "R" and not _reg_fits(m, n, k):
         pytest.skip("no register layout for this size")
-    if klass == "T" and not _row_fits(m, n, k):
-        pytest.skip("no row-per-thread layout for this size")
     if klass == "S" and (m > 8 or n > 8):
         pytest.skip("the thread-per-LP class holds m, n <= 8")
     if klass == "W" and (m > 32 or n + k > 32):
@@ -292,7 +285,7 @@ def test_concurrent_host_threads_share_the_library():
     import threading
 
     cases = [("G1", 5, 5, 3000, "S"), ("G1", 28, 28, 400, "W"), ("G1", 60, 60, 200, "R"),
-             ("G2", 40, 40, 120, "M"), ("G2", 60, 60, 60, "L"), ("mixneg", 20, 20, 500, "T")]
+             ("G2", 40, 40, 120, "M"), ("G2", 60, 60, 60, "L"), ("mixneg", 20, 20, 500, "R")]
     inputs = [_gen(g, B, m, n, 500 + m) for g, m, n, B, _ in cases]
     solo = [gpu_solve(*inp, kernel_class=k) for inp, (*_, k) in zip(inputs, cases)]
     out = [None] * len(cases)

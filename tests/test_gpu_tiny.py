@@ -62,25 +62,29 @@ def test_tiny_rpc_iteration_limit_and_no_x():
 
 _SCRIPT = r"""
 import sys, numpy as np
-sys.path.insert(0, {root!r}); sys.path.insert(0, {tests!r})
+sys.path.insert(0, {root!r}); sys.path.insert(0, {tests!r}); sys.path.insert(0, {dev!r})
 import lpgen
 from gpu_util import gpu_solve
 A, b, c = lpgen.status_mix(20000, 5, 5, 412, infeasible_start=True)
 g = gpu_solve(A, b, c, kernel_class="S")
-np.savez({out!r}, **{{k: v for k, v in g.items() if k != "launch"}})
+from paper_1609_08114_b200 import lpb
+np.savez({out!r}, lib=lpb.LIB_PATH, **{{k: v for k, v in g.items() if k != "launch"}})
 """
 
 
 def test_tiny_equals_smem_slice_kernel(tmp_path):
-    """The register kernel and the SMEM-slice kernel (LPB_NO_TINY=1) agree bit for bit."""
+    """The register kernel and the SMEM-slice kernel (LPB_NO_TINY=1, a switch of the
+    development build) agree bit for bit."""
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     outs = []
     for env_extra in ({}, {"LPB_NO_TINY": "1"}):
         out = str(tmp_path / f"r{len(outs)}.npz")
         env = dict(os.environ, **env_extra)
-        code = _SCRIPT.format(root=root, tests=os.path.join(root, "tests"), out=out)
+        code = _SCRIPT.format(root=root, tests=os.path.join(root, "tests"), out=out,
+                              dev=os.path.join(root, "devbuild"))
         subprocess.run([sys.executable, "-c", code], check=True, env=env, timeout=600)
         outs.append(np.load(out))
+    assert all("devbuild" in str(o["lib"]) for o in outs)
     for k in ("status", "iters"):
         assert np.array_equal(outs[0][k], outs[1][k])
     for k in ("obj", "x"):

@@ -93,3 +93,17 @@ def test_hyperbox_shards_cross_blocks():
                                                                                lpgen.hyperbox_dirs(n, 9, lo, hi))
         assert np.array_equal(d, full[lo:hi])
     assert np.array_equal(lpgen.hyperbox(B, n, 9)[2], full)  # deterministic
+
+
+def test_kmax_bound_holds():
+    """lpgen.kmax_bound (the solver's kmax_hint in bench.py) bounds #{b_i < 0} of every LP its
+    generator draws: G1 has none (type 1), G2 exactly ceil(m/4) (type 2)."""
+    import numpy as np
+    for name in ("cfg1", "cfg2", "cfg3", "cfg8", "cfg2s", "cfg3s", "cfg9"):
+        A, b, c = lpgen.make_config(name, 300)
+        kb = lpgen.kmax_bound(name)
+        k = (np.atleast_2d(b) < 0).sum(axis=-1)
+        assert k.max() <= kb, name
+        if lpgen.CONFIGS[name]["gen"] == "G2":
+            assert k.min() == kb, name
+    assert lpgen.kmax_bound("cfg4") == -1
