@@ -77,6 +77,10 @@ struct lpb_ctx {
   int* rec_ints = nullptr;  // rec_e[cap] | nbvar[n+kmax] | bkey[m] | info[4]
   int rec_cap = 0, rec_W = 0;
   cudaEvent_t rec_ev = nullptr;  // host pipeline: the phase-I record is complete
+  // development build: per-chunk event timeline of the host pipeline (lpb_set_timeline)
+  std::vector<cudaEvent_t> tl;
+  bool tl_on = false;
+  int tl_n = 0;
   char err[256] = {0};
 };
 
@@ -218,6 +222,7 @@ extern "C" int lpb_destroy(lpb_ctx* c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   for (auto s : c->chunk_streams) { cudaStreamSynchronize(s); cudaStreamDestroy(s); }
   for (auto ev : c->chunk_done) cudaEventDestroy(ev);
+  for (auto ev : c->tl) cudaEventDestroy(ev);
   cudaFree(c->d_status);
   cudaFree(c->d_obj);
   cudaFree(c->d_x);
@@ -570,10 +575,26 @@ static int solve_impl(lpb_ctx* c, const double* A, const double* b, const double
     }
     kmax = best;
   }
+#ifdef LPB_DEV_HOOKS
+  // timeline marks per chunk: [0] before its H2D, [1] H2D done, [2] kernel done, [3] D2H done
+#define LPB_TL(q, k) \
+  if (c->tl_on) LPB_CUDA(c, cudaEventRecord(c->tl[4 * (q) + (k)], s))
+  if (c->tl_on) {
+    while ((int)c->tl.size() < 4 * nch) {
+      cudaEvent_t ev;
+      LPB_CUDA(c, cudaEventCreate(&ev));
+      c->tl.push_back(ev);
+    }
+    c->tl_n = nch;
+  }
+#else
+#define LPB_TL(q, k)
+#endif
   for (int q = 0; q < nch; ++q) {
     const int64_t lp0 = B * q / nch, lp1 = B * (q + 1) / nch, cnt = lp1 - lp0;
     cudaStream_t s = c->chunk_streams[q];
     LPB_CUDA(c, cudaStreamWaitEvent(s, c->ev0, 0));
+    LPB_TL(q, 0);
     if (general) {
       // shared constraints (LPB_SHARED_AB): A and b cross PCIe once, on the first chunk's
       // stream; the other chunks wait for that copy
@@ -589,6 +610,7 @@ static int solve_impl(lpb_ctx* c, const double* A, const double* b, const double
       if (sab && q > 0) LPB_CUDA(c, cudaStreamWaitEvent(s, c->chunk_done[0], 0));
       LPB_CUDA(c, cudaMemcpyAsync(c->d_c + lp0 * n, cv + lp0 * n, 8 * cnt * n,
                                   cudaMemcpyHostToDevice, s));
+      LPB_TL(q, 1);
       rc = run_general(c, s, lp0, cnt, c->d_A + lp0 * sA, c->d_b + lp0 * sb, c->d_c + lp0 * n,
                        nox, sab, kmax, c->d_ticket + q, &c->last_launches,
                        sab ? (q == 0 ? REC_FIRST : REC_WAIT) : REC_SELF);
@@ -602,14 +624,17 @@ static int solve_impl(lpb_ctx* c, const double* A, const double* b, const double
       if (shared && q > 0) LPB_CUDA(c, cudaStreamWaitEvent(s, c->chunk_done[0], 0));
       LPB_CUDA(c, cudaMemcpyAsync(c->d_c + lp0 * n, cv + lp0 * n, 8 * cnt * n,
                                   cudaMemcpyHostToDevice, s));
+      LPB_TL(q, 1);
       rc = run_hyperbox(c, s, lp0, cnt, c->d_c + lp0 * n, c->d_b + lp0 * bstride, shared, nox,
                         &c->last_launches);
     }
     if (rc != LPB_OK) return rc;
+    LPB_TL(q, 2);
     if (o_status) LPB_CUDA(c, cudaMemcpyAsync(o_status + lp0, c->d_status + lp0, 4 * cnt, cudaMemcpyDefault, s));
     if (o_obj) LPB_CUDA(c, cudaMemcpyAsync(o_obj + lp0, c->d_obj + lp0, 8 * cnt, cudaMemcpyDefault, s));
     if (o_x) LPB_CUDA(c, cudaMemcpyAsync(o_x + lp0 * n, c->d_x + lp0 * n, 8 * cnt * (int64_t)n, cudaMemcpyDefault, s));
     if (o_iters) LPB_CUDA(c, cudaMemcpyAsync(o_iters + 2 * lp0, c->d_iters + 2 * lp0, 8 * cnt, cudaMemcpyDefault, s));
+    LPB_TL(q, 3);
     cudaEvent_t done;
     LPB_CUDA(c, cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
     LPB_CUDA(c, cudaEventRecord(done, s));
@@ -678,6 +703,25 @@ extern "C" int lpb_last_timing(lpb_ctx* c, double* solve_ms, double* e2e_ms) {
 }
 
 #ifdef LPB_DEV_HOOKS  // development build only (include/dev/lpb_selftest.h)
+extern "C" int lpb_set_timeline(lpb_ctx* c, int on) {
+  if (!c) return LPB_EINVAL;
+  c->tl_on = on != 0;
+  return LPB_OK;
+}
+
+extern "C" int lpb_last_timeline(lpb_ctx* c, float* out, int max_chunks, int* n_chunks) {
+  if (!c || !out || !n_chunks) return LPB_EINVAL;
+  if (!c->solved || !c->host_path || !c->tl_on) return LPB_ESTATE;
+  LPB_CUDA(c, cudaSetDevice(c->device));
+  LPB_CUDA(c, cudaEventSynchronize(c->ev1));
+  const int nq = std::min(c->tl_n, max_chunks);
+  for (int q = 0; q < nq; ++q)
+    for (int k = 0; k < 4; ++k)
+      LPB_CUDA(c, cudaEventElapsedTime(out + 4 * q + k, c->ev0, c->tl[4 * q + k]));
+  *n_chunks = nq;
+  return LPB_OK;
+}
+
 extern "C" int lpb_set_profile_buffer(lpb_ctx* c, long long* dev_buf) {
   if (!c) return LPB_EINVAL;
   c->prof = dev_buf;

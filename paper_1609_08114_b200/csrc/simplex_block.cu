@@ -275,6 +275,57 @@ __device__ __forceinline__ void pivot_local(const Smem& s, const double* colE, i
   __syncthreads();
 }
 
+// Phase-II compaction ("dead positions and the phase-I row skipped"; the
+// artificials are dropped after phase I).  Once phase I is over, the positions
+// whose nonbasic variable is a left artificial (nbvar == DEAD) can never enter again, so each
+// CTA moves its live columns (and the RHS) left, in order, and phase II updates cnt' + 1
+// columns instead of cnt + 1.  Row-local moves: every warp owns whole rows, so a row is read
+// into registers, then written back shifted.  Positions keep their global numbering
+// g0 + local column (the owner CTA of a position is still pos / Q).  Returns the new count.
+__device__ __forceinline__ int compact_live(const Smem& s, int S, int cnt, int nrows) {
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int j = tid;  // cnt <= Q <= 255 < NT: one column per thread
+  const bool live = j < cnt && s.nbvar[j] != DEAD;
+  const int var = j < cnt ? s.nbvar[j] : DEAD;
+  const unsigned bal = __ballot_sync(FULL, live);
+  if (lane == 0) s.wcount[w] = __popc(bal);
+  __syncthreads();
+  int off = 0, tot = 0;
+#pragma unroll
+  for (int q = 0; q < NW; ++q) {
+    const int cq = s.wcount[q];
+    if (q < w) off += cq;
+    tot += cq;
+  }
+  if (tot == cnt) {  // nothing dead on this CTA
+    __syncthreads();
+    return cnt;
+  }
+  int* map = reinterpret_cast<int*>(s.prow);  // scratch: prow holds S >= cnt + 1 doubles
+  if (j < cnt) map[j] = live ? off + __popc(bal & ((1u << lane) - 1u)) : -1;
+  if (j == cnt) map[j] = tot;  // the RHS column
+  __syncthreads();
+  if (live) s.nbvar[map[j]] = var;
+  constexpr int CH = (NT + 31) / 32;  // column chunks of a row (cnt + 1 <= NT)
+  for (int i = w; i < nrows; i += NW) {
+    double v[CH];
+    int dst[CH];
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {
+      const int jj = lane + 32 * c;
+      dst[c] = jj <= cnt ? map[jj] : -1;
+      v[c] = dst[c] >= 0 ? s.T[i * S + jj] : 0.0;
+    }
+    __syncwarp();
+#pragma unroll
+    for (int c = 0; c < CH; ++c)
+      if (dst[c] >= 0) s.T[i * S + dst[c]] = v[c];
+    __syncwarp();
+  }
+  __syncthreads();
+  return tot;
+}
+
 template <int CL>
 __global__ void __launch_bounds__(NT) simplex_block_kernel(SimplexArgs a) {
   constexpr bool PULL = CL >= 8;
@@ -356,9 +407,9 @@ __global__ void __launch_bounds__(NT) simplex_block_kernel(SimplexArgs a) {
 
     int st = -1, it1 = 0, it2 = 0;
     const uint64_t lpkey = a.rpc ? rpc_lp_key(a.rpc_seed, a.lp_base + lp) : 0ull;
-    const int cnt = max(0, min(Q, n + k - cl.rank * Q));  // live local positions
-    const int Wa = cnt + 1;                               // + RHS at local column cnt
-    const int Wp = (Wa + 1) & ~1;                         // whole 128-bit pairs
+    int cnt = max(0, min(Q, n + k - cl.rank * Q));  // live local positions
+    int Wa = cnt + 1;                               // + RHS at local column cnt
+    const int Wp = (Wa + 1) & ~1;                   // whole 128-bit pairs (build)
     const int g0 = cl.rank * Q;
     if (k > a.kmax) st = ST_NUMERICAL;  // cannot happen: kmax comes from the prepass / hint
     if (a.khint >= 0 && k > a.khint) st = ST_BAD_HINT;
@@ -400,6 +451,8 @@ __global__ void __launch_bounds__(NT) simplex_block_kernel(SimplexArgs a) {
         for (int j = tid; j < Wp; j += NT)
           s.T[m * S + j] = (j < cnt) ? cur[g0 + j] : (j == cnt ? cur[npos] : 0.0);
         __syncthreads();
+        cnt = compact_live(s, S, cnt, m + 1);  // phase II from here on: drop dead positions
+        Wa = cnt + 1;
       }
     } else if (st < 0) {
       for (int i = w; i < m; i += NW) {
@@ -548,6 +601,10 @@ __global__ void __launch_bounds__(NT) simplex_block_kernel(SimplexArgs a) {
         phase = 2;
         stall = 0;
         pp ^= 1;  // the proposal slots of this round may still be read by a peer CTA
+        if (!record) {  // phase II never touches the dead (left artificial) positions
+          cnt = compact_live(s, S, cnt, m + 1);
+          Wa = cnt + 1;
+        }
         if (record) {  // phase I recorded: dump the tableau it leaves, then stop (mode 1)
           for (int i = w; i < m; i += NW)
             for (int j = lane; j < Wa; j += 32) {

@@ -52,3 +52,35 @@ def test_two_rank_sharded_parity(case):
     r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
     assert f"PARITY-OK {case}" in r.stdout, r.stdout
+
+
+def test_two_rank_strong_scaling_bench():
+    """--scaling strong: the config's fixed batch is sharded over the ranks (SURVEY §8(e),
+    cfg5's 6,003,000 LPs over 1/2/4/8 GPUs); the gathered results are consistent."""
+    env = dict(os.environ, LPB_DIST_BACKEND="gloo")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_port()), "bench.py", "--gpus",
+           "2", "--config", "cfg5", "--scaling", "strong", "--batch", "300001", "--steps", "3",
+           "--warmup", "3", "--e2e-steps", "1"]
+    r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["scaling"] == "strong" and d["n_gpus"] == 2
+    assert d["config"]["batch_total"] == 300001 and d["config"]["batch_per_gpu"] == 150000
+    assert d["gather_check"].startswith("ok"), d["gather_check"]
+
+
+@pytest.mark.parametrize("config,extra", [("cfg4", ["--batch", "200000"]),
+                                          ("cfg1", [])])
+def test_bench_cuda_graph_mode(config, extra):
+    """--graph: each step replays one captured CUDA graph of the solve (one kernel launch per
+    step, the library's own launch path captured on the bench's stream)."""
+    cmd = [sys.executable, "bench.py", "--config", config, "--graph", "--steps", "5",
+           "--warmup", "3", "--e2e-steps", "0", "--no-cpu-baseline", *extra]
+    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    d = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][0])
+    assert d["config"]["cuda_graph"] is True and d["value"] > 0
+    assert d["gpu_launches"] == 5
