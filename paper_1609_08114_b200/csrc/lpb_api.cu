@@ -354,7 +354,7 @@ static int run_general(lpb_ctx* c, cudaStream_t s, int64_t lp0, int64_t cnt, con
       LPB_CUDA(c, cudaEventRecord(c->kev1, s));
       c->kev_valid = true;
     }
-    *launches += tiny ? 2 : 1;
+    *launches += (tiny && c->opt.kmax_hint != 0) ? 2 : 1;  // + list-mode two-phase kernel
     c->last_class = CLASS_S;
     c->last_cluster = 0;
     c->last_grid = 0;

@@ -326,9 +326,10 @@ __device__ __forceinline__ int compact_live(const Smem& s, int S, int cnt, int n
   return tot;
 }
 
-template <int CL>
+// PULL (proposal columns read over DSMEM after the barrier) is used for CL >= 8, and for
+// CL = 2/4 whenever its smaller SMEM footprint fits more CTAs per SM than PUSH (launch_cl).
+template <int CL, bool PULL>
 __global__ void __launch_bounds__(NT) simplex_block_kernel(SimplexArgs a) {
-  constexpr bool PULL = CL >= 8;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const Cluster<CL> cl;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
@@ -344,8 +345,9 @@ __global__ void __launch_bounds__(NT) simplex_block_kernel(SimplexArgs a) {
   s.prow = s.fcol + RC;
   s.nbvar = reinterpret_cast<int*>(s.prow + S);
   s.bkey = s.nbvar + (Q + 1);
-  s.negrows = s.bkey + m;
-  s.wcount = s.negrows + m;
+  // negrows is needed only while the LP is built, before colE is first written: alias
+  s.negrows = reinterpret_cast<int*>(s.colE);
+  s.wcount = s.bkey + m;
   uintptr_t p = reinterpret_cast<uintptr_t>(s.wcount + NW);
   p = (p + 15) & ~uintptr_t(15);
   s.wslots = reinterpret_cast<Cand*>(p);
@@ -353,7 +355,7 @@ __global__ void __launch_bounds__(NT) simplex_block_kernel(SimplexArgs a) {
   s.rec = reinterpret_cast<Rec*>(s.cslots + 2 * CL);
   s.colC = reinterpret_cast<double*>(s.rec + 2 * CL);
   s.ctl = reinterpret_cast<Ctl*>(s.colC + 2 * (PULL ? 1 : CL) * RC);
-  s.rbuf = reinterpret_cast<double*>(s.ctl + 1);
+  s.rbuf = reinterpret_cast<double*>(s.ctl + 1);  // allocated for mode 2 (warm start) only
 
   // DSMEM may only be touched once every CTA of the cluster is running: one
   // cluster barrier before the first remote ticket write (racecheck finding).
@@ -685,29 +687,69 @@ __global__ void __launch_bounds__(NT) simplex_block_kernel(SimplexArgs a) {
 
 }  // namespace
 
-size_t block_smem_bytes(int cl, int m, int n, int kmax) {
+static size_t smem_bytes(int cl, int m, int n, int kmax, bool pull, bool warm) {
   const int Q = (n + kmax + cl - 1) / cl;
   const int S = row_stride(Q);
   size_t bytes = sizeof(double) * ((size_t)(m + 2) * S + 2 * (size_t)(m + 2) + S);
-  bytes += sizeof(int) * ((size_t)(Q + 1) + 2 * (size_t)m + NW);
+  bytes += sizeof(int) * ((size_t)(Q + 1) + (size_t)m + NW);  // nbvar, bkey, wcount
   bytes = (bytes + 15) & ~size_t(15);
-  const size_t ncol = cl >= 8 ? 1 : (size_t)cl;  // proposal columns per parity (PUSH: cl)
+  const size_t ncol = pull ? 1 : (size_t)cl;  // proposal columns per parity (PUSH: cl)
   bytes += sizeof(Cand) * (2 * NW + 2 * cl) + sizeof(Rec) * 2 * cl +
            sizeof(double) * 2 * ncol * (m + 2) + sizeof(Ctl);
-  bytes += sizeof(double) * 2 * ((size_t)n + kmax + 1);  // warm-start replay buffer
+  if (warm) bytes += sizeof(double) * 2 * ((size_t)n + kmax + 1);  // warm-start replay buffer
   return bytes;
 }
-
+size_t block_smem_bytes(int cl, int m, int n, int kmax) {
+  return smem_bytes(cl, m, n, kmax, cl >= 8, true);
+}
 bool block_fits(int cl, int m, int n, int kmax) {
   const int Q = (n + kmax + cl - 1) / cl;  // pivot_local keeps <= 8 columns per lane
-  return Q + 1 <= 256 && block_smem_bytes(cl, m, n, kmax) <= 227 * 1024;
+  return Q + 1 <= 256 && smem_bytes(cl, m, n, kmax, true, true) <= 227 * 1024;
 }
 
-template <int CL>
-static cudaError_t launch_cl(const SimplexArgs& a, int grid_override, cudaStream_t s,
-                             int* ctas_out) {
-  const size_t smem = block_smem_bytes(CL, a.m, a.n, a.kmax);
+// Resident CTAs of one (CL, PULL) variant for this launch's SMEM size (memoised).
+template <int CL, bool PULL>
+static cudaError_t resident_ctas(const SimplexArgs& a, size_t smem, int* out) {
   const int sms = device_sm_count();
+  static LaunchMemo memo;
+  return memo.get(smem, out, [&](int& v, size_t attr) {
+    cudaError_t e = cudaFuncSetAttribute(simplex_block_kernel<CL, PULL>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)attr);
+    if (e != cudaSuccess) return e;
+    if constexpr (CL > 8) {  // 16-CTA clusters are a non-portable (opt-in) size on sm_100
+      e = cudaFuncSetAttribute(simplex_block_kernel<CL, PULL>,
+                               cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      if (e != cudaSuccess) return e;
+    }
+    if constexpr (CL == 1) {
+      int per_sm = 0;
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, simplex_block_kernel<1, PULL>,
+                                                        NT, smem);
+      v = per_sm * sms;
+      return e;
+    } else {
+      cudaLaunchConfig_t q = {};
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = CL;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      q.attrs = at;
+      q.numAttrs = 1;
+      q.blockDim = dim3(NT);
+      q.dynamicSmemBytes = smem;
+      q.gridDim = dim3(CL * sms);
+      int clusters = 0;
+      e = cudaOccupancyMaxActiveClusters(&clusters, simplex_block_kernel<CL, PULL>, &q);
+      v = clusters * CL;
+      return e;
+    }
+  });
+}
+
+template <int CL, bool PULL>
+static cudaError_t launch_variant(const SimplexArgs& a, size_t smem, int resident,
+                                  int grid_override, cudaStream_t s, int* ctas_out) {
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute attr[1];
   cfg.blockDim = dim3(NT);
@@ -721,34 +763,6 @@ static cudaError_t launch_cl(const SimplexArgs& a, int grid_override, cudaStream
     cfg.attrs = attr;
     cfg.numAttrs = 1;
   }
-  // attribute + occupancy queries are host round trips: memo per (device, smem size)
-  static LaunchMemo memo;
-  int resident = 0;
-  const cudaError_t em = memo.get(smem, &resident, [&](int& v, size_t attr) {
-    cudaError_t e = cudaFuncSetAttribute(simplex_block_kernel<CL>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)attr);
-    if (e != cudaSuccess) return e;
-    if constexpr (CL > 8) {  // 16-CTA clusters are a non-portable (opt-in) size on sm_100
-      e = cudaFuncSetAttribute(simplex_block_kernel<CL>,
-                               cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-      if (e != cudaSuccess) return e;
-    }
-    if constexpr (CL == 1) {
-      int per_sm = 0;
-      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, simplex_block_kernel<1>, NT,
-                                                        smem);
-      v = per_sm * sms;
-      return e;
-    } else {
-      cudaLaunchConfig_t q = cfg;
-      q.gridDim = dim3(CL * sms);
-      int clusters = 0;
-      e = cudaOccupancyMaxActiveClusters(&clusters, simplex_block_kernel<CL>, &q);
-      v = clusters * CL;
-      return e;
-    }
-  });
-  if (em != cudaSuccess) return em;
   if (resident <= 0) return cudaErrorInvalidConfiguration;
   int64_t want = a.batch * CL;
   int grid = (int)(want < resident ? want : resident);
@@ -759,7 +773,31 @@ static cudaError_t launch_cl(const SimplexArgs& a, int grid_override, cudaStream
   if (ctas_out) *ctas_out = grid;
   const cudaError_t e = cudaMemsetAsync(a.ticket, 0, sizeof(int), s);  // persistent LP ticket
   if (e != cudaSuccess) return e;
-  return cudaLaunchKernelEx(&cfg, simplex_block_kernel<CL>, a);
+  return cudaLaunchKernelEx(&cfg, simplex_block_kernel<CL, PULL>, a);
+}
+
+// PUSH for CL <= 4 unless PULL's smaller footprint (one own proposal column per parity
+// instead of CL) fits more CTAs on an SM (e.g. 200x200 two-phase on 4-CTA clusters: 2 CTAs
+// per SM instead of 1); PULL for CL >= 8 (CL columns would not fit SMEM at m ~ 500).
+template <int CL>
+static cudaError_t launch_cl(const SimplexArgs& a, int grid_override, cudaStream_t s,
+                             int* ctas_out) {
+  const bool warm = a.mode == 2;
+  const size_t spull = smem_bytes(CL, a.m, a.n, a.kmax, true, warm);
+  int rpull = 0;
+  cudaError_t e = resident_ctas<CL, true>(a, spull, &rpull);
+  if (e != cudaSuccess) return e;
+  if constexpr (CL <= 4) {
+    const size_t spush = smem_bytes(CL, a.m, a.n, a.kmax, false, warm);
+    int rpush = 0;
+    if (spush <= 227 * 1024) {
+      e = resident_ctas<CL, false>(a, spush, &rpush);
+      if (e != cudaSuccess) return e;
+    }
+    if (rpush >= rpull)
+      return launch_variant<CL, false>(a, spush, rpush, grid_override, s, ctas_out);
+  }
+  return launch_variant<CL, true>(a, spull, rpull, grid_override, s, ctas_out);
 }
 
 cudaError_t launch_simplex_block(int cl, const SimplexArgs& a, int grid_override,

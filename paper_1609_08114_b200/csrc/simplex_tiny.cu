@@ -30,45 +30,87 @@ constexpr int DEADV = INT_MAX;
 
 __device__ __forceinline__ double ninf() { return __longlong_as_double(0xfff0000000000000ll); }
 
+// Persistent: every thread solves LP after LP, taking the next LP index from the launch's
+// ticket the moment its current LP ends (one atomicAdd per warp for all lanes that need one),
+// so a warp's lanes stay busy instead of idling until the slowest of 32 fixed LPs finishes
+// (pivot counts per LP vary 0..8 at 5x5, mean 1.9: the fixed mapping ran every warp for its
+// maximum).  Each loop iteration is one pivot of every busy lane; the build and the extract
+// of the lanes that start / finish an LP run as (divergent) branches of the same iteration.
+#ifndef LPB_TINY_MINB
+#define LPB_TINY_MINB 4  // 4 CTAs (16 warps) per SM: 128 registers (measured best of 1, 4, 5)
+#endif
 template <int C, bool RPC>  // RPC: a separate instantiation keeps LPC's registers
-__global__ void __launch_bounds__(128) simplex_tiny_kernel(SimplexArgs a) {
-  const int64_t lp = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (lp >= a.batch) return;
+__global__ void __launch_bounds__(128, LPB_TINY_MINB) simplex_tiny_kernel(SimplexArgs a) {
   const int m = a.m, n = a.n;
-  const double* __restrict__ Ak = a.A + lp * a.sA;
-  const double* __restrict__ bk = a.b + lp * a.sb;
-  const double* __restrict__ ck = a.c + lp * (int64_t)n;
-
-  // ---- build (type 1: slack basis, R7 with k = 0) ----
-  double rhs[C];
-  bool neg = false;
-#pragma unroll
-  for (int i = 0; i < C; ++i) {
-    rhs[i] = (i < m) ? __ldg(bk + i) : 0.0;
-    neg |= rhs[i] < 0.0;
-  }
-  if (neg) {  // two-phase LP: the SMEM-slice kernel takes it
-    a.defer_list[atomicAdd(a.defer_cnt, 1)] = (int)lp;
-    return;
-  }
-  double T[C][C], d[C];
+  const unsigned lane = threadIdx.x & 31u;
+  // kmax_hint = 0 (type-1 promise, include/lpb.h): an LP with some b_i < 0 is reported
+  // LPB_BAD_HINT here instead of being deferred to the two-phase SMEM-slice kernel
+  const bool hinted = a.khint == 0;
+  double T[C][C], d[C], rhs[C];
   int bkey[C], nbv[C];
-#pragma unroll
-  for (int i = 0; i < C; ++i) {
-#pragma unroll
-    for (int j = 0; j < C; ++j) T[i][j] = (i < m && j < n) ? __ldg(Ak + i * n + j) : 0.0;
-    bkey[i] = n + i;
-  }
-#pragma unroll
-  for (int j = 0; j < C; ++j) {
-    d[j] = (j < n) ? __ldg(ck + j) : ninf();
-    nbv[j] = (j < n) ? j : DEADV;
-  }
   double z = 0.0;  // objective row's RHS cell (obj = -z, reading R3)
-
-  int st = -1, it2 = 0, stall = 0;
-  const uint64_t lpkey = RPC ? rpc_lp_key(a.rpc_seed, a.lp_base + lp) : 0ull;
+  int it2 = 0, stall = 0;
+  int64_t lp = 0;
+  bool have = false;
+  uint64_t lpkey = 0ull;
   for (;;) {
+    // ---- refill: the lanes without an LP take consecutive tickets ----
+    {
+      const unsigned act = __activemask();
+      const unsigned need = __ballot_sync(act, !have);
+      if (need) {
+        const int leader = __ffs(need) - 1;
+        int base = 0;
+        if ((int)lane == leader) base = atomicAdd(a.ticket, __popc(need));
+        base = __shfl_sync(act, base, leader);
+        if (!have) lp = (int64_t)base + __popc(need & ((1u << lane) - 1u));
+      }
+    }
+    if (!have) {
+      if (lp >= a.batch) break;
+      // ---- build (type 1: slack basis, R7 with k = 0) ----
+      const double* __restrict__ Ak = a.A + lp * a.sA;
+      const double* __restrict__ bk = a.b + lp * a.sb;
+      const double* __restrict__ ck = a.c + lp * (int64_t)n;
+      bool neg = false;
+#pragma unroll
+      for (int i = 0; i < C; ++i) {
+        rhs[i] = (i < m) ? __ldg(bk + i) : 0.0;
+        neg |= rhs[i] < 0.0;
+      }
+      if (neg) {
+        if (hinted) {  // the caller's type-1 promise is broken: not solved
+          a.status[lp] = ST_BAD_HINT;
+          a.iters[2 * lp] = 0;
+          a.iters[2 * lp + 1] = 0;
+          a.obj[lp] = __longlong_as_double(0x7ff8000000000000ll);
+          if (a.x)
+            for (int j = 0; j < n; ++j) a.x[lp * n + j] = __longlong_as_double(0x7ff8000000000000ll);
+        } else {  // two-phase LP: the SMEM-slice kernel takes it
+          a.defer_list[atomicAdd(a.defer_cnt, 1)] = (int)lp;
+        }
+        continue;
+      }
+#pragma unroll
+      for (int i = 0; i < C; ++i) {
+#pragma unroll
+        for (int j = 0; j < C; ++j) T[i][j] = (i < m && j < n) ? __ldg(Ak + i * n + j) : 0.0;
+        bkey[i] = n + i;
+      }
+#pragma unroll
+      for (int j = 0; j < C; ++j) {
+        d[j] = (j < n) ? __ldg(ck + j) : ninf();
+        nbv[j] = (j < n) ? j : DEADV;
+      }
+      z = 0.0;
+      it2 = 0;
+      stall = 0;
+      lpkey = RPC ? rpc_lp_key(a.rpc_seed, a.lp_base + lp) : 0ull;
+      have = true;
+    }
+
+    // ---- one pivot ----
+    int st = -1;
     const bool bland = a.bland_K > 0 && stall >= a.bland_K;
     const bool rpc = RPC && !bland;
     // Step 1: entering position (LPC: max d, lowest variable on ties; Bland: lowest variable;
@@ -96,108 +138,115 @@ __global__ void __launch_bounds__(128) simplex_tiny_kernel(SimplexArgs a) {
       ev = take ? var : ev;
       best = take ? dj : best;
     }
-    if (e < 0) { st = ST_OPTIMAL; break; }
-    if (it2 >= a.max_iter) { st = ST_ITER_LIMIT; break; }
-
-    // Step 2: ratio test over rows i < m with T[i][e] > eps_piv (R1, R2, R5)
-    double col[C];
-#pragma unroll
-    for (int i = 0; i < C; ++i) {
-      double v = T[i][0];
-#pragma unroll
-      for (int j = 1; j < C; ++j) v = (e == j) ? T[i][j] : v;
-      col[i] = v;
-    }
-    int l = -1, lkey = INT_MAX;
     double theta = 0.0;
+    int l = -1;
+    double col[C];
+    if (e < 0) {
+      st = ST_OPTIMAL;
+    } else if (it2 >= a.max_iter) {
+      st = ST_ITER_LIMIT;
+    } else {
+      // Step 2: ratio test over rows i < m with T[i][e] > eps_piv (R1, R2, R5)
 #pragma unroll
-    for (int i = 0; i < C; ++i) {
-      const bool val = i < m && col[i] > a.eps_piv;
-      bool slow;
-      double rr = div_fast(rhs[i], val ? col[i] : 1.0, slow);
-      if (slow) rr = ddiv_slow(rhs[i], val ? col[i] : 1.0);
-      const int key = bland ? bkey[i] : i;
-      const bool take = val && (l < 0 || rr < theta || (rr == theta && key < lkey));
-      l = take ? i : l;
-      lkey = take ? key : lkey;
-      theta = take ? rr : theta;
+      for (int i = 0; i < C; ++i) {
+        double v = T[i][0];
+#pragma unroll
+        for (int j = 1; j < C; ++j) v = (e == j) ? T[i][j] : v;
+        col[i] = v;
+      }
+      int lkey = INT_MAX;
+#pragma unroll
+      for (int i = 0; i < C; ++i) {
+        const bool val = i < m && col[i] > a.eps_piv;
+        bool slow;
+        double rr = div_fast(rhs[i], val ? col[i] : 1.0, slow);
+        if (slow) rr = ddiv_slow(rhs[i], val ? col[i] : 1.0);
+        const int key = bland ? bkey[i] : i;
+        const bool take = val && (l < 0 || rr < theta || (rr == theta && key < lkey));
+        l = take ? i : l;
+        lkey = take ? key : lkey;
+        theta = take ? rr : theta;
+      }
+      if (l < 0) st = ST_UNBOUNDED;
     }
-    if (l < 0) { st = ST_UNBOUNDED; break; }
+    if (st < 0) {
+      // Step 3: pivot row / PE (IEEE division, R12), fma update of every other row incl. the
+      // objective; position e becomes the leaving variable's column (R13)
+      double pe = col[0], prr = rhs[0];
+      double prow[C];
+#pragma unroll
+      for (int j = 0; j < C; ++j) prow[j] = T[0][j];
+#pragma unroll
+      for (int i = 1; i < C; ++i) {
+        const bool s_ = (l == i);
+        pe = s_ ? col[i] : pe;
+        prr = s_ ? rhs[i] : prr;
+#pragma unroll
+        for (int j = 0; j < C; ++j) prow[j] = s_ ? T[i][j] : prow[j];
+      }
+      const double r = recip_of(pe);
+      double pv[C];
+      bool slow_any = false;
+#pragma unroll
+      for (int j = 0; j < C; ++j) {
+        bool sl;
+        pv[j] = div_with((j == e) ? 1.0 : prow[j], pe, r, sl);
+        slow_any |= sl;
+      }
+      bool slr;
+      double pr = div_with(prr, pe, r, slr);
+      if (slow_any || slr) {  // rare: outside div_with's fast range -> IEEE __ddiv_rn
+#pragma unroll
+        for (int j = 0; j < C; ++j) pv[j] = ddiv_slow((j == e) ? 1.0 : prow[j], pe);
+        pr = ddiv_slow(prr, pe);
+      }
+#pragma unroll
+      for (int i = 0; i < C; ++i) {
+        const bool piv = (i == l);
+        const double f = -col[i];
+#pragma unroll
+        for (int j = 0; j < C; ++j)
+          T[i][j] = piv ? pv[j] : __fma_rn(f, pv[j], (j == e) ? 0.0 : T[i][j]);
+        rhs[i] = piv ? pr : __fma_rn(f, pr, rhs[i]);
+      }
+      double fd = d[0];
+#pragma unroll
+      for (int j = 1; j < C; ++j) fd = (e == j) ? d[j] : fd;
+      fd = -fd;
+#pragma unroll
+      for (int j = 0; j < C; ++j) d[j] = __fma_rn(fd, pv[j], (j == e) ? 0.0 : d[j]);
+      z = __fma_rn(fd, pr, z);
+      // basis swap: row l's basic variable leaves into position e
+      int leaving = bkey[0];
+#pragma unroll
+      for (int i = 1; i < C; ++i) leaving = (l == i) ? bkey[i] : leaving;
+#pragma unroll
+      for (int i = 0; i < C; ++i) bkey[i] = (l == i) ? ev : bkey[i];
+#pragma unroll
+      for (int j = 0; j < C; ++j) nbv[j] = (e == j) ? leaving : nbv[j];
+      ++it2;
+      stall = (theta > 0.0) ? 0 : stall + 1;
+      continue;
+    }
 
-    // Step 3: pivot row / PE (IEEE division, R12), fma update of every other row incl. the
-    // objective; position e becomes the leaving variable's column (R13)
-    double pe = col[0], prr = rhs[0];
-    double prow[C];
+    // ---- extract (R10) ----
+    a.status[lp] = st;
+    a.iters[2 * lp] = 0;
+    a.iters[2 * lp + 1] = it2;
+    a.obj[lp] = (st == ST_OPTIMAL) ? -z
+              : (st == ST_UNBOUNDED) ? __longlong_as_double(0x7ff0000000000000ll)
+                                     : __longlong_as_double(0x7ff8000000000000ll);
+    if (a.x) {
+      double* xk = a.x + lp * (int64_t)n;
+      const double fill = (st == ST_OPTIMAL) ? 0.0 : __longlong_as_double(0x7ff8000000000000ll);
+      for (int j = 0; j < n; ++j) xk[j] = fill;
+      if (st == ST_OPTIMAL) {
 #pragma unroll
-    for (int j = 0; j < C; ++j) prow[j] = T[0][j];
-#pragma unroll
-    for (int i = 1; i < C; ++i) {
-      const bool s_ = (l == i);
-      pe = s_ ? col[i] : pe;
-      prr = s_ ? rhs[i] : prr;
-#pragma unroll
-      for (int j = 0; j < C; ++j) prow[j] = s_ ? T[i][j] : prow[j];
+        for (int i = 0; i < C; ++i)
+          if (i < m && bkey[i] < n) xk[bkey[i]] = rhs[i];
+      }
     }
-    const double r = recip_of(pe);
-    double pv[C];
-    bool slow_any = false;
-#pragma unroll
-    for (int j = 0; j < C; ++j) {
-      bool sl;
-      pv[j] = div_with((j == e) ? 1.0 : prow[j], pe, r, sl);
-      slow_any |= sl;
-    }
-    bool slr;
-    double pr = div_with(prr, pe, r, slr);
-    if (slow_any || slr) {  // rare: outside div_with's fast range -> IEEE __ddiv_rn
-#pragma unroll
-      for (int j = 0; j < C; ++j) pv[j] = ddiv_slow((j == e) ? 1.0 : prow[j], pe);
-      pr = ddiv_slow(prr, pe);
-    }
-#pragma unroll
-    for (int i = 0; i < C; ++i) {
-      const bool piv = (i == l);
-      const double f = -col[i];
-#pragma unroll
-      for (int j = 0; j < C; ++j)
-        T[i][j] = piv ? pv[j] : __fma_rn(f, pv[j], (j == e) ? 0.0 : T[i][j]);
-      rhs[i] = piv ? pr : __fma_rn(f, pr, rhs[i]);
-    }
-    double fd = d[0];
-#pragma unroll
-    for (int j = 1; j < C; ++j) fd = (e == j) ? d[j] : fd;
-    fd = -fd;
-#pragma unroll
-    for (int j = 0; j < C; ++j) d[j] = __fma_rn(fd, pv[j], (j == e) ? 0.0 : d[j]);
-    z = __fma_rn(fd, pr, z);
-    // basis swap: row l's basic variable leaves into position e
-    int leaving = bkey[0];
-#pragma unroll
-    for (int i = 1; i < C; ++i) leaving = (l == i) ? bkey[i] : leaving;
-#pragma unroll
-    for (int i = 0; i < C; ++i) bkey[i] = (l == i) ? ev : bkey[i];
-#pragma unroll
-    for (int j = 0; j < C; ++j) nbv[j] = (e == j) ? leaving : nbv[j];
-    ++it2;
-    stall = (theta > 0.0) ? 0 : stall + 1;
-  }
-
-  // ---- extract (R10) ----
-  a.status[lp] = st;
-  a.iters[2 * lp] = 0;
-  a.iters[2 * lp + 1] = it2;
-  a.obj[lp] = (st == ST_OPTIMAL) ? -z
-            : (st == ST_UNBOUNDED) ? __longlong_as_double(0x7ff0000000000000ll)
-                                   : __longlong_as_double(0x7ff8000000000000ll);
-  if (a.x) {
-    double* xk = a.x + lp * (int64_t)n;
-    const double fill = (st == ST_OPTIMAL) ? 0.0 : __longlong_as_double(0x7ff8000000000000ll);
-    for (int j = 0; j < n; ++j) xk[j] = fill;
-    if (st == ST_OPTIMAL) {
-#pragma unroll
-      for (int i = 0; i < C; ++i)
-        if (i < m && bkey[i] < n) xk[bkey[i]] = rhs[i];
-    }
+    have = false;
   }
 }
 
@@ -205,23 +254,42 @@ __global__ void __launch_bounds__(128) simplex_tiny_kernel(SimplexArgs a) {
 
 bool tiny_fits(int m, int n) { return m <= TY_MAXC && n <= TY_MAXC; }
 
-cudaError_t launch_simplex_tiny(const SimplexArgs& a, cudaStream_t s) {
-  cudaError_t e = cudaMemsetAsync(a.defer_cnt, 0, sizeof(int), s);
-  if (e != cudaSuccess) return e;
-  const int c = std::max(a.m, a.n);
-  // 32-thread CTAs spread a small batch over many SMs; 128 once every SM has a few warps
+template <int C, bool RPC>
+static cudaError_t launch_tiny(const SimplexArgs& a, cudaStream_t s) {
+  auto kern = simplex_tiny_kernel<C, RPC>;
+  static LaunchMemo memo;
+  int per_sm = 0;
+  const cudaError_t em = memo.get(0, &per_sm, [&](int& v, size_t) {
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, kern, 128, 0);
+  });
+  if (em != cudaSuccess) return em;
+  // persistent grid: the resident CTAs (or fewer 32-thread CTAs for a small batch, spread
+  // over the SMs)
   const int nt = a.batch >= (int64_t)device_sm_count() * 128 ? 128 : 32;
-  const unsigned grid = (unsigned)((a.batch + nt - 1) / nt);
-#define LPB_TINY_GO(CC)                                                   \
-  (a.rpc ? simplex_tiny_kernel<CC, true><<<grid, nt, 0, s>>>(a)            \
-         : simplex_tiny_kernel<CC, false><<<grid, nt, 0, s>>>(a))
+  const int64_t resident = (int64_t)(per_sm < 1 ? 1 : per_sm) * device_sm_count() * (128 / nt);
+  int64_t grid = (a.batch + nt - 1) / nt;
+  if (grid > resident) grid = resident;
+  kern<<<(unsigned)grid, nt, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_simplex_tiny(const SimplexArgs& a, cudaStream_t s) {
+  const bool hinted = a.khint == 0;  // type-1 promise: no deferred list, one launch
+  cudaError_t e = cudaMemsetAsync(a.ticket, 0, sizeof(int), s);
+  if (e != cudaSuccess) return e;
+  if (!hinted) {
+    e = cudaMemsetAsync(a.defer_cnt, 0, sizeof(int), s);
+    if (e != cudaSuccess) return e;
+  }
+  const int c = std::max(a.m, a.n);
+#define LPB_TINY_GO(CC) \
+  e = a.rpc ? launch_tiny<CC, true>(a, s) : launch_tiny<CC, false>(a, s)
   if (c <= 3) LPB_TINY_GO(3);
   else if (c == 4) LPB_TINY_GO(4);
   else if (c == 5) LPB_TINY_GO(5);
   else LPB_TINY_GO(6);
 #undef LPB_TINY_GO
-  e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
+  if (e != cudaSuccess || hinted) return e;
   return launch_simplex_thread(a, s);  // list mode: the deferred two-phase LPs
 }
 

@@ -22,14 +22,21 @@ for spec in {specs!r}:
     parts = spec.split(':')
     name = parts[0]; B = int(parts[1]) if len(parts) > 1 and parts[1] else None
     klass = parts[2] if len(parts) > 2 and parts[2] else None
+    clu = int(parts[3]) if len(parts) > 3 and parts[3] else 0
     A, b, c = lpgen.make_config(name, B)
     At, bt, ct = (torch.from_numpy(v).cuda() for v in (A, b, c))
     kw = dict(kernel_class=klass) if klass else {{}}
+    if clu: kw['cluster_ctas'] = clu
     kh = lpgen.kmax_bound(name)
     if 'kmax_hint' in [f[0] for f in lpb.Options._fields_]:
         kw['kmax_hint'] = kh
     s = lpb.Solver(c.shape[0], A.shape[-2], c.shape[1], lpb.GENERAL, **kw)
     f = lambda: s.solve_device(At, bt, ct, shared_ab=(A.ndim == 2), sync=True)
+    try:
+        f()
+    except Exception as ex:
+        print('skip', spec, ex, file=sys.stderr)
+        continue
     for _ in range(2): f()
     ts = []
     for _ in range(7):
@@ -37,7 +44,7 @@ for spec in {specs!r}:
     r = {{k: v.cpu().numpy() for k, v in s.device_results().items()}}
     h = hashlib.sha1(r['status'].tobytes() + r['iters'].tobytes() + r['obj'].tobytes()).hexdigest()[:12]
     piv = int(r['iters'].sum())
-    out.append(dict(spec=spec, min_ms=min(ts), med_ms=sorted(ts)[3], klass=s.launch_info()[1],
+    out.append(dict(spec=spec, min_ms=min(ts), med_ms=sorted(ts)[3], klass=s.launch_info()[1] + str(s.launch_shape()),
                     digest=h, pivots=piv))
     s.close()
 print('AB-JSON ' + json.dumps(out))

@@ -7,9 +7,19 @@ mkdir -p $OUT
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $OUT/gpu.txt
 timeout 1500 python -m pytest tests -m gpu -q > $OUT/pytest_gpu.txt 2>&1
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.txt 2>&1
-for cf in cfg2 cfg1 cfg1m cfg4 cfg5 cfg2s cfg2r cfg9 cfg10; do
+for cf in cfg2 cfg5; do  # with the n_chunks = 1 (no overlap) e2e control
+  timeout 900 python bench.py --config $cf --e2e-chunks1 > $OUT/bench_$cf.json 2> $OUT/bench_$cf.err
+done
+for cf in cfg1 cfg1m cfg4 cfg2s cfg2r cfg9 cfg10; do
   timeout 900 python bench.py --config $cf > $OUT/bench_$cf.json 2> $OUT/bench_$cf.err
 done
+# strong scaling line at N = 1 (the fixed cfg5 batch) and CUDA-graph replay of small solves
+timeout 900 python bench.py --config cfg5 --scaling strong --no-cpu-baseline > $OUT/bench_cfg5_strong.json 2>&1
+timeout 900 python bench.py --config cfg4 --graph --no-cpu-baseline > $OUT/bench_cfg4_graph.json 2>&1
+timeout 900 python bench.py --config cfg1 --graph --no-cpu-baseline > $OUT/bench_cfg1_graph.json 2>&1
+# host pipeline: per-chunk event timeline (10 vs 1 chunks) and ASan/UBSan of the host code
+timeout 900 python scripts/timeline.py cfg2 cfg5 > $OUT/timeline.txt 2>&1
+timeout 1200 bash scripts/sanitize_host.sh $OUT > /dev/null 2>&1
 for cf in cfg3 cfg3s; do
   timeout 900 python bench.py --config $cf --steps 3 --warmup 3 --e2e-steps 1 > $OUT/bench_$cf.json 2> $OUT/bench_$cf.err
 done

@@ -26,6 +26,16 @@ L.lpb_last_timeline.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_float),
                                 ctypes.POINTER(ctypes.c_int)]
 
 
+def merged(iv):
+    out = []
+    for a, b in sorted(iv):
+        if out and a <= out[-1][1]:
+            out[-1][1] = max(out[-1][1], b)
+        else:
+            out.append([a, b])
+    return out
+
+
 def union(iv):
     iv = sorted(iv)
     tot, cur = 0.0, None
@@ -75,8 +85,10 @@ def run(name, n_chunks):
     d2h = [(a, b) for a, b in t[:, 2:4]]
     ksum = sum(b - a for a, b in ker)
     hsum = sum(b - a for a, b in h2d)
-    # overlap: kernel time that runs while some chunk's H2D copy is in flight
-    over = sum(max(0.0, min(kb, hb) - max(ka, ha)) for ka, kb in ker for ha, hb in h2d)
+    # overlap: time during which some chunk's kernel interval and some chunk's H2D copy are
+    # both in flight (intersection of the two interval unions)
+    over = sum(max(0.0, min(kb, hb) - max(ka, ha))
+               for ka, kb in merged(ker) for ha, hb in merged(h2d))
     return {"config": name, "n_chunks": int(nq.value), "e2e_ms": e2e, "B": int(B),
             "h2d_busy_ms": union(h2d), "kernel_busy_ms": union(ker), "d2h_busy_ms": union(d2h),
             "h2d_sum_ms": hsum, "kernel_sum_ms": ksum,

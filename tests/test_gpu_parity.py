@@ -308,3 +308,65 @@ def test_concurrent_host_threads_share_the_library():
         for k in ("status", "iters"):
             assert np.array_equal(a_[k], b_[k])
         assert np.array_equal(a_["obj"], b_["obj"], equal_nan=True)
+
+
+def test_concurrent_same_class_different_smem():
+    """host threads launching the SAME kernel instantiation with DIFFERENT dynamic
+    SMEM sizes at once (M class at 24x24 .. 90x90) -- the launch memo only ever raises the
+    function's SMEM attribute, so no launch sees a limit lowered by another thread."""
+    import threading
+
+    sizes = [24, 90, 40, 80, 56, 70]
+    inputs = [_gen("G2", 40, m, m, 700 + m) for m in sizes]
+    solo = [gpu_solve(*inp, kernel_class="M") for inp in inputs]
+    out = [None] * len(sizes)
+    errs = []
+
+    def run(t):
+        try:
+            for _ in range(6):
+                out[t] = gpu_solve(*inputs[t], kernel_class="M")
+        except Exception as ex:  # surfaced below
+            errs.append(ex)
+
+    th = [threading.Thread(target=run, args=(t,)) for t in range(len(sizes))]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs, errs
+    for a_, b_ in zip(solo, out):
+        assert b_["launch"]["class"] == "M"
+        for k in ("status", "iters"):
+            assert np.array_equal(a_[k], b_[k])
+        assert np.array_equal(a_["obj"], b_["obj"], equal_nan=True)
+
+
+@pytest.mark.parametrize("klass,m,n,B,hint", [("S", 5, 5, 20000, 0), ("S", 6, 6, 3000, 0),
+                                             ("W", 12, 12, 2000, 0), ("R", 40, 40, 600, 0),
+                                             ("R", 60, 60, 300, 3), ("M", 40, 40, 200, 2),
+                                             ("L", 60, 60, 100, 4)])
+def test_kmax_hint_contract(klass, m, n, B, hint):
+    """lpb_options.kmax_hint (include/lpb.h): the solve is one launch sized for the promised
+    k; every LP that keeps the promise (#{b_i < 0} <= hint) is solved exactly as without the
+    hint (oracle parity), every LP that breaks it reports LPB_BAD_HINT (obj NaN, x NaN,
+    iters 0) instead of a wrong answer."""
+    A, b, c = lpgen.status_mix(B, m, n, 900 + m + hint)
+    g0 = lpgen.rng(77 + m)
+    want = g0.integers(0, hint + 3, size=B)  # per-LP count of negated rows: 0 .. hint + 2
+    for t in range(B):
+        rows = g0.permutation(m)[:want[t]]
+        b[t, rows] = -b[t, rows]
+    k = (b < 0).sum(axis=1)
+    ok = k <= hint
+    assert ok.any() and (~ok).any()
+    g = gpu_solve(A, b, c, kernel_class=klass, kmax_hint=hint)
+    assert g["launch"]["class"] == klass
+    assert np.all(g["status"][~ok] == 5)
+    assert np.all(np.isnan(g["obj"][~ok])) and np.all(g["iters"][~ok] == 0)
+    assert np.all(np.isnan(g["x"][~ok]))
+    idx = np.nonzero(ok)[0]
+    o = oracle.solve(A[idx], b[idx], c[idx])
+    compare(A, b, c, g, o, sample=idx)
+    if hint == 0 or klass in ("R", "W", "M", "L"):
+        assert g["launch"]["launches"] == 1  # no prepass, no deferred list
