@@ -508,9 +508,7 @@ __global__ void __launch_bounds__(NT) simplex_block_kernel(SimplexArgs a) {
       Cand ce{0.0, 0, -1};
       const bool rpc = a.rpc && !bland;
       const uint64_t pkey = rpc ? rpc_pivot_key(lpkey, it1 + it2) : 0ull;
-      // every warp scans ALL of this CTA's positions (cnt <= Q < 256: <= 8 per lane) and
-      // reduces them itself: the CTA-local winner without a block barrier
-      for (int j = lane; j < cnt; j += 32) {
+      for (int j = tid; j < cnt; j += NT) {
         const int var = s.nbvar[j];
         const double d = s.T[objrow * S + j];
         if (var != DEAD && d > a.eps_enter) {
@@ -518,7 +516,7 @@ __global__ void __launch_bounds__(NT) simplex_block_kernel(SimplexArgs a) {
           if (bland ? better<MIN_KEY>(cd, ce) : better<MAX_V>(cd, ce)) ce = cd;
         }
       }
-      ce = bland ? warp_reduce<MIN_KEY>(ce) : warp_reduce<MAX_V>(ce);
+      ce = bland ? block_reduce<MIN_KEY>(ce, s.wslots) : block_reduce<MAX_V>(ce, s.wslots);
       Cand cr{0.0, 0, -1};
       const int jc = ce.pos - g0;  // local column of the proposal
       if (ce.pos >= 0) {
