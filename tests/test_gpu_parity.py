@@ -370,3 +370,16 @@ def test_kmax_hint_contract(klass, m, n, B, hint):
     compare(A, b, c, g, o, sample=idx)
     if hint == 0 or klass in ("R", "W", "M", "L"):
         assert g["launch"]["launches"] == 1  # no prepass, no deferred list
+
+
+@pytest.mark.parametrize("seed,K", [(40, 3), (43, 3), (43, 2), (47, 3)])
+@pytest.mark.parametrize("klass", ["M", "L", "auto"])
+def test_numerical_status_parity(seed, K, klass):
+    """LPB_NUMERICAL (phase I without a ratio candidate: a rounding artifact, pinned in
+    tests/test_oracle_pins.py) is reproduced LP for LP on degenerate 100x100 batches with
+    small Bland thresholds, together with every other status, iteration count and bit."""
+    A, b, c = lpgen.degenerate(300, 100, 100, seed, negative_b=True)
+    o = oracle.solve(A, b, c, bland_after=K)
+    assert (o["status"] == oracle.NUMERICAL).any()
+    g = gpu_solve(A, b, c, kernel_class=klass, bland_after=K)
+    compare(A, b, c, g, o)

@@ -316,3 +316,39 @@ def test_residual_on_config_shapes():
     assert np.all(r["status"] == oracle.OPTIMAL)
     for k in range(0, 1000, 10):
         assert primal_residual(A[k], b[k], r["x"][k]) <= 1e-9
+
+
+# LPB_NUMERICAL (reading R2 / C6): phase I reporting "unbounded" is impossible in exact
+# arithmetic -- the phase-I objective -sum(artificials) is bounded above by 0 -- so the branch
+# fires only when fp64 rounding under an aggressive Bland threshold leaves an improving
+# phase-I column without a positive pivot candidate.  Pinned on seeded degenerate LPs where it
+# happens: the same LPs under the default threshold end with a certified status, and HiGHS
+# (presolve off, C-P17) finds them feasible or proves infeasibility -- never unbounded in
+# phase I.
+NUMERICAL_CASES = [(40, 3, 207), (43, 3, 147), (43, 2, 154), (47, 3, 81)]
+
+
+@pytest.mark.parametrize("seed,K,k", NUMERICAL_CASES)
+def test_numerical_status_is_a_rounding_artifact(seed, K, k):
+    linprog = pytest.importorskip("scipy.optimize").linprog
+    A, b, c = lpgen.degenerate(300, 100, 100, seed, negative_b=True)
+    A1, b1, c1 = A[k:k + 1], b[k:k + 1], c[k:k + 1]
+    o = oracle.solve(A1, b1, c1, bland_after=K)
+    assert o["status"][0] == oracle.NUMERICAL and o["iters"][0][1] == 0  # ended in phase I
+    assert np.isnan(o["obj"][0]) and np.all(np.isnan(o["x"][0]))
+    # another threshold (the default, else Bland after every degenerate pivot) solves the same
+    # LP to a certified outcome
+    for Kalt in (0, 1):
+        od = oracle.solve(A1, b1, c1, bland_after=Kalt, certs=True)
+        st = od["status"][0]
+        if st != oracle.NUMERICAL:
+            break
+    assert st in (oracle.OPTIMAL, oracle.INFEASIBLE, oracle.UNBOUNDED)
+    if st == oracle.OPTIMAL:
+        assert not check_optimal(A1[0], b1[0], c1[0], od["obj"][0], od["x"][0], od["y"][0])
+    elif st == oracle.INFEASIBLE:
+        assert not check_infeasible(A1[0], b1[0], od["y"][0])
+    h = linprog(-c1[0], A_ub=A1[0], b_ub=b1[0], bounds=(0, None), method="highs",
+                options={"presolve": False})
+    assert h.status in (0, 2, 3)  # optimal / infeasible / unbounded: a real LP status
+    assert (h.status == 2) == (st == oracle.INFEASIBLE)
