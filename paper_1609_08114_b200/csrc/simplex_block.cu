@@ -28,6 +28,7 @@
 #include <cfloat>
 #include <climits>
 
+#include "lpb_async.cuh"
 #include "lpb_fp64.cuh"
 #include "lpb_internal.cuh"
 #include "lpb_reduce.cuh"
@@ -113,6 +114,7 @@ struct Smem {
   Rec* rec;       // 2 x CL proposals (parity-buffered), written by every CTA of the cluster
   double* colC;   // 2 x CL x RC proposal columns (parity-buffered)
   Ctl* ctl;
+  uint64_t* xbar; // 2 mbarriers (by parity): the peers' proposals have landed (PUSH, CL > 1)
   double* rbuf;   // 2 x (n + kmax + 1): phase-II row replay (warm start, mode 2)
 };
 
@@ -355,11 +357,23 @@ __global__ void __launch_bounds__(NT) simplex_block_kernel(SimplexArgs a) {
   s.rec = reinterpret_cast<Rec*>(s.cslots + 2 * CL);
   s.colC = reinterpret_cast<double*>(s.rec + 2 * CL);
   s.ctl = reinterpret_cast<Ctl*>(s.colC + 2 * (PULL ? 1 : CL) * RC);
-  s.rbuf = reinterpret_cast<double*>(s.ctl + 1);  // allocated for mode 2 (warm start) only
+  s.xbar = reinterpret_cast<uint64_t*>(s.ctl + 1);
+  s.rbuf = reinterpret_cast<double*>(s.xbar + 2);  // allocated for mode 2 (warm start) only
+  // PUSH clusters exchange the per-pivot proposals with st.async into the peers' slots, each
+  // completing on the receiver's mbarrier of that parity: no cluster barrier (and no release
+  // fence over every outstanding memory operation) per pivot.
+  constexpr bool XASYNC = !PULL && CL > 1;
+  if (XASYNC && tid == 0) {
+    mbar_init(&s.xbar[0], 1);
+    mbar_init(&s.xbar[1], 1);
+  }
+  uint32_t xph = 0;  // bit q: parity of the next phase of xbar[q]
 
   // DSMEM may only be touched once every CTA of the cluster is running: one
-  // cluster barrier before the first remote ticket write (racecheck finding).
+  // cluster barrier before the first remote ticket write (racecheck finding); it also
+  // publishes the initialised mbarriers.
   if constexpr (CL > 1) cl.sync();
+  else if (XASYNC) __syncthreads();
 
   int par = 0;
   for (;;) {
@@ -539,22 +553,58 @@ __global__ void __launch_bounds__(NT) simplex_block_kernel(SimplexArgs a) {
       // barrier, which every reader has passed only once its pivot_local read is done.
       double* const myc = PULL ? s.colC + (size_t)pp * RC
                                : s.colC + (size_t)(pp * CL + cl.rank) * RC;
-      if (ce.pos >= 0)
-        for (int i = tid; i < nrow; i += NT) {
-          const double v = s.T[i * S + jc];
-          if constexpr (PULL) {
-            myc[i] = v;
-          } else {
+      if constexpr (XASYNC) {
+        // every CTA sends a column (column 0 when it has no candidate, then ignored), so
+        // each receiver expects exactly (CL - 1) columns + records
+        const int jcs = ce.pos >= 0 ? jc : 0;
+        if (tid == 0) mbar_arrive_expect(&s.xbar[pp], (CL - 1) * (nrow * 8 + (int)sizeof(Rec)));
+        uint32_t rb[CL], rc[CL];
 #pragma unroll
-            for (int q = 0; q < CL; ++q) cl.remote(myc, q)[i] = v;
-          }
+        for (int q = 0; q < CL; ++q) {
+          rb[q] = cluster_addr(myc, q);
+          rc[q] = cluster_addr(&s.xbar[pp], q);
         }
-      if (tid == 0) {
-        const Rec r{ce, cr.v, cr.pos, 0};
+        for (int i = tid; i < nrow; i += NT) {
+          const double v = s.T[i * S + jcs];
+          myc[i] = v;
+#pragma unroll
+          for (int q = 0; q < CL; ++q)
+            if (q != cl.rank) st_async_f64(rb[q] + 8u * i, v, rc[q]);
+        }
+        if (tid == 0) {
+          const Rec r{ce, cr.v, cr.pos, 0};
+          Rec* mine = s.rec + pp * CL + cl.rank;
+          *mine = r;
+          const uint4* w4 = reinterpret_cast<const uint4*>(&r);
+#pragma unroll
+          for (int q = 0; q < CL; ++q)
+            if (q != cl.rank) {
+              const uint32_t ra = cluster_addr(mine, q);
+              st_async_v4(ra, w4[0], rc[q]);
+              st_async_v4(ra + 16u, w4[1], rc[q]);
+            }
+        }
+        __syncthreads();  // this CTA's own slot
+        mbar_wait_cluster(&s.xbar[pp], (xph >> pp) & 1u);
+        xph ^= 1u << pp;
+      } else {
+        if (ce.pos >= 0)
+          for (int i = tid; i < nrow; i += NT) {
+            const double v = s.T[i * S + jc];
+            if constexpr (PULL) {
+              myc[i] = v;
+            } else {
+#pragma unroll
+              for (int q = 0; q < CL; ++q) cl.remote(myc, q)[i] = v;
+            }
+          }
+        if (tid == 0) {
+          const Rec r{ce, cr.v, cr.pos, 0};
 #pragma unroll 1
-        for (int q = 0; q < CL; ++q) *cl.remote(s.rec + pp * CL + cl.rank, q) = r;  // 32 B
+          for (int q = 0; q < CL; ++q) *cl.remote(s.rec + pp * CL + cl.rank, q) = r;  // 32 B
+        }
+        cl.sync();
       }
-      cl.sync();
       int win = 0;
       ce = s.rec[pp * CL].ce;
 #pragma unroll 4
@@ -695,7 +745,7 @@ static size_t smem_bytes(int cl, int m, int n, int kmax, bool pull, bool warm) {
   bytes = (bytes + 15) & ~size_t(15);
   const size_t ncol = pull ? 1 : (size_t)cl;  // proposal columns per parity (PUSH: cl)
   bytes += sizeof(Cand) * (2 * NW + 2 * cl) + sizeof(Rec) * 2 * cl +
-           sizeof(double) * 2 * ncol * (m + 2) + sizeof(Ctl);
+           sizeof(double) * 2 * ncol * (m + 2) + sizeof(Ctl) + 2 * sizeof(uint64_t);
   if (warm) bytes += sizeof(double) * 2 * ((size_t)n + kmax + 1);  // warm-start replay buffer
   return bytes;
 }
