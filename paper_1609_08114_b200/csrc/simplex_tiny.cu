@@ -154,18 +154,55 @@ __global__ void __launch_bounds__(128, LPB_TINY_MINB) simplex_tiny_kernel(Simple
         for (int j = 1; j < C; ++j) v = (e == j) ? T[i][j] : v;
         col[i] = v;
       }
-      int lkey = INT_MAX;
+      // Pass 1: approximate quotients rhs_i * (1/v_i) (MUFU reciprocal + one Newton step,
+      // relative error < 2^-40) find the smallest; the exact IEEE quotient of that row is
+      // the answer unless another candidate lies within the approximation's error of it (a
+      // near or exact tie, e.g. several zero ratios) or Bland's rule orders ties by basis
+      // key: then every candidate is divided exactly, as before.
+      bool val[C];
+      double qa[C];
+      double amin = 0.0;
 #pragma unroll
       for (int i = 0; i < C; ++i) {
-        const bool val = i < m && col[i] > a.eps_piv;
-        bool slow;
-        double rr = div_fast(rhs[i], val ? col[i] : 1.0, slow);
-        if (slow) rr = ddiv_slow(rhs[i], val ? col[i] : 1.0);
-        const int key = bland ? bkey[i] : i;
-        const bool take = val && (l < 0 || rr < theta || (rr == theta && key < lkey));
+        val[i] = i < m && col[i] > a.eps_piv;
+        const double v = val[i] ? col[i] : 1.0;
+        double r0;
+        asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r0) : "d"(v));
+        qa[i] = __dmul_rn(rhs[i], __fma_rn(__fma_rn(-v, r0, 1.0), r0, r0));
+        const bool take = val[i] && (l < 0 || qa[i] < amin);
+        amin = take ? qa[i] : amin;
         l = take ? i : l;
-        lkey = take ? key : lkey;
-        theta = take ? rr : theta;
+      }
+      constexpr double kDelta = 0x1p-30;
+      const double ub = amin + fabs(amin) * kDelta;
+      bool multi = bland;
+#pragma unroll
+      for (int i = 0; i < C; ++i)
+        multi |= val[i] && i != l && (qa[i] - fabs(qa[i]) * kDelta <= ub || qa[i] == amin);
+      if (!multi && l >= 0) {
+        double v = col[0], rv = rhs[0];
+#pragma unroll
+        for (int i = 1; i < C; ++i) {
+          v = (l == i) ? col[i] : v;
+          rv = (l == i) ? rhs[i] : rv;
+        }
+        bool slow;
+        theta = div_fast(rv, v, slow);
+        if (slow) theta = ddiv_slow(rv, v);
+      } else if (l >= 0) {
+        l = -1;
+        int lkey = INT_MAX;
+#pragma unroll
+        for (int i = 0; i < C; ++i) {
+          bool slow;
+          double rr = div_fast(rhs[i], val[i] ? col[i] : 1.0, slow);
+          if (slow) rr = ddiv_slow(rhs[i], val[i] ? col[i] : 1.0);
+          const int key = bland ? bkey[i] : i;
+          const bool take = val[i] && (l < 0 || rr < theta || (rr == theta && key < lkey));
+          l = take ? i : l;
+          lkey = take ? key : lkey;
+          theta = take ? rr : theta;
+        }
       }
       if (l < 0) st = ST_UNBOUNDED;
     }
