@@ -166,9 +166,7 @@ __global__ void __launch_bounds__(128, LPB_TINY_MINB) simplex_tiny_kernel(Simple
       for (int i = 0; i < C; ++i) {
         val[i] = i < m && col[i] > a.eps_piv;
         const double v = val[i] ? col[i] : 1.0;
-        double r0;
-        asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r0) : "d"(v));
-        qa[i] = __dmul_rn(rhs[i], __fma_rn(__fma_rn(-v, r0, 1.0), r0, r0));
+        qa[i] = __dmul_rn(rhs[i], recip_approx(v));
         const bool take = val[i] && (l < 0 || qa[i] < amin);
         amin = take ? qa[i] : amin;
         l = take ? i : l;

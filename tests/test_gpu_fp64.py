@@ -38,3 +38,28 @@ def test_div_fast_bit_exact():
     qn = q.cpu().numpy()
     assert np.array_equal(qn.view(np.int64), ref.view(np.int64))
     # out[1] counts operands outside the fast range (extreme exponents): they take __ddiv_rn
+
+
+def test_recip_approx_error_bound():
+    """The S kernel's ratio test orders rows by approximate quotients (recip_approx) and
+    treats rows within a relative 2^-30 of the minimum as ties that are divided exactly; the
+    approximation's own relative error must be far below that window for every divisor the
+    ratio test can meet (v > eps_piv = 1e-9, up to huge magnitudes)."""
+    import torch
+
+    from gpu_util import dev_lib
+    dlib = dev_lib()
+    dlib.lpb_selftest_rcp_approx.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64]
+    g = np.random.Generator(np.random.PCG64(11))
+    n = 2_000_000
+    v = np.ldexp(g.uniform(1.0, 2.0, n), g.integers(-30, 1000, n))
+    v[:100000] = g.uniform(1e-9, 100.0, 100000)
+    v[100000:100010] = [1e-9, 1.0, 2.0, 3.0, 0.1, 1e300, 1.5, 1.9999999999999998, 1.0000000000000002, 7.0]
+    vt = torch.from_numpy(v).cuda()
+    rt = torch.empty_like(vt)
+    assert dlib.lpb_selftest_rcp_approx(ctypes.c_void_p(vt.data_ptr()), ctypes.c_void_p(rt.data_ptr()),
+                                        ctypes.c_int64(n)) == 0
+    r = rt.cpu().numpy().astype(np.longdouble)
+    rel = np.abs(r * v.astype(np.longdouble) - 1.0)
+    assert np.all(np.isfinite(rel))
+    assert rel.max() < 2.0 ** -40, float(rel.max())
