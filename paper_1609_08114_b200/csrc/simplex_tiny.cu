@@ -155,7 +155,7 @@ __global__ void __launch_bounds__(128, LPB_TINY_MINB) simplex_tiny_kernel(Simple
         col[i] = v;
       }
       // Pass 1: approximate quotients rhs_i * (1/v_i) (MUFU reciprocal + one Newton step,
-      // relative error < 2^-40) find the smallest; the exact IEEE quotient of that row is
+      // relative error ~1e-12 < 2^-36) find the smallest; the exact IEEE quotient of that row is
       // the answer unless another candidate lies within the approximation's error of it (a
       // near or exact tie, e.g. several zero ratios) or Bland's rule orders ties by basis
       // key: then every candidate is divided exactly, as before.
