@@ -53,6 +53,40 @@ __global__ void __launch_bounds__(128, LPB_TINY_MINB) simplex_tiny_kernel(Simple
   int64_t lp = 0;
   bool have = false;
   uint64_t lpkey = 0ull;
+  // Step 1 (entering position) of the NEXT pivot; computed right after the build and right
+  // after each update, so that an LP whose last pivot leaves no candidate is extracted in
+  // the same loop iteration (an LP with p pivots takes max(p, 1) iterations, not p + 1).
+  int e = -1, ev = INT_MAX;
+  auto step1 = [&]() {
+    // LPC: max d, lowest variable on ties; Bland: lowest variable; RPC: largest
+    // counter-based score (include/lpb.h)
+    const bool bland = a.bland_K > 0 && stall >= a.bland_K;
+    const bool rpc = RPC && !bland;
+    const uint64_t pkey = rpc ? rpc_pivot_key(lpkey, it2) : 0ull;
+    e = -1;
+    ev = INT_MAX;
+    double best = 0.0;
+    uint64_t ub = 0ull;
+#pragma unroll
+    for (int j = 0; j < C; ++j) {
+      const int var = nbv[j];
+      const double dj = d[j];
+      const bool cand = var != DEADV && dj > a.eps_enter;
+      bool take;
+      if (rpc) {
+        const uint64_t u = rpc_score(pkey, var);
+        take = cand && (e < 0 || u > ub || (u == ub && var < ev));
+        ub = take ? u : ub;
+      } else if (bland) {
+        take = cand && var < ev;
+      } else {
+        take = cand && (e < 0 || dj > best || (dj == best && var < ev));
+      }
+      e = take ? j : e;
+      ev = take ? var : ev;
+      best = take ? dj : best;
+    }
+  };
   for (;;) {
     // ---- refill: the lanes without an LP take consecutive tickets ----
     {
@@ -107,37 +141,12 @@ __global__ void __launch_bounds__(128, LPB_TINY_MINB) simplex_tiny_kernel(Simple
       stall = 0;
       lpkey = RPC ? rpc_lp_key(a.rpc_seed, a.lp_base + lp) : 0ull;
       have = true;
+      step1();
     }
 
-    // ---- one pivot ----
+    // ---- one pivot; Step 1 was done at the build / the last update ----
     int st = -1;
     const bool bland = a.bland_K > 0 && stall >= a.bland_K;
-    const bool rpc = RPC && !bland;
-    // Step 1: entering position (LPC: max d, lowest variable on ties; Bland: lowest variable;
-    // RPC: largest counter-based score, include/lpb.h)
-    const uint64_t pkey = rpc ? rpc_pivot_key(lpkey, it2) : 0ull;
-    int e = -1, ev = INT_MAX;
-    double best = 0.0;
-    uint64_t ub = 0ull;
-#pragma unroll
-    for (int j = 0; j < C; ++j) {
-      const int var = nbv[j];
-      const double dj = d[j];
-      const bool cand = var != DEADV && dj > a.eps_enter;
-      bool take;
-      if (rpc) {
-        const uint64_t u = rpc_score(pkey, var);
-        take = cand && (e < 0 || u > ub || (u == ub && var < ev));
-        ub = take ? u : ub;
-      } else if (bland) {
-        take = cand && var < ev;
-      } else {
-        take = cand && (e < 0 || dj > best || (dj == best && var < ev));
-      }
-      e = take ? j : e;
-      ev = take ? var : ev;
-      best = take ? dj : best;
-    }
     double theta = 0.0;
     int l = -1;
     double col[C];
@@ -261,7 +270,10 @@ __global__ void __launch_bounds__(128, LPB_TINY_MINB) simplex_tiny_kernel(Simple
       for (int j = 0; j < C; ++j) nbv[j] = (e == j) ? leaving : nbv[j];
       ++it2;
       stall = (theta > 0.0) ? 0 : stall + 1;
-      continue;
+      step1();
+      if (e < 0) st = ST_OPTIMAL;
+      else if (it2 >= a.max_iter) st = ST_ITER_LIMIT;
+      if (st < 0) continue;
     }
 
     // ---- extract (R10) ----
