@@ -71,7 +71,7 @@ __global__ void __launch_bounds__(128, LPB_TINY_MINB) simplex_tiny_kernel(Simple
     for (int j = 0; j < C; ++j) {
       const int var = nbv[j];
       const double dj = d[j];
-      const bool cand = var != DEADV && dj > a.eps_enter;
+      const bool cand = dj > a.eps_enter;  // padding positions (DEADV) hold -inf forever
       bool take;
       if (rpc) {
         const uint64_t u = rpc_score(pkey, var);
@@ -180,12 +180,13 @@ __global__ void __launch_bounds__(128, LPB_TINY_MINB) simplex_tiny_kernel(Simple
         amin = take ? qa[i] : amin;
         l = take ? i : l;
       }
-      constexpr double kDelta = 0x1p-30;
-      const double ub = amin + fabs(amin) * kDelta;
+      // a row j can only tie with or beat row l exactly if qa_j <= amin + 4 * 2^-30 * |amin|
+      // (the approximation's relative error is below 2^-36; zero ratios are exact, and
+      // +-inf quotients compare equal to each other)
+      const double lim = __fma_rn(fabs(amin), 0x1p-28, amin);
       bool multi = bland;
 #pragma unroll
-      for (int i = 0; i < C; ++i)
-        multi |= val[i] && i != l && (qa[i] - fabs(qa[i]) * kDelta <= ub || qa[i] == amin);
+      for (int i = 0; i < C; ++i) multi |= val[i] && i != l && qa[i] <= lim;
       if (!multi && l >= 0) {
         double v = col[0], rv = rhs[0];
 #pragma unroll
