@@ -519,18 +519,29 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
       LPB_PROF_MARK(3)
       double theta = 0.0;
       double qrc = 1.0;
-      if (!drive) {  // Step 2c: every thread scans the NWARP warp partials (ascending warp)
-        Part q = sm.part[0];
+      if (!drive) {  // Step 2c: the NWARP warp partials
+        if constexpr (NWARP >= 4) {
+          // lanes < NWARP hold one partial each; the same (ratio, tie) argmin by REDUX
+          // (measured: cfg2 -0.6 %; with 2 warps the serial compare is shorter)
+          Part q = (lane < NWARP) ? sm.part[lane] : Part{0.0, INT_MAX, -1, 1.0};
+          const int ql = warp_argmin(q.idx >= 0, okey(q.v), ikey(q.tie));
+          if (ql < 0) { st = (phase == 2) ? ST_UNBOUNDED : ST_NUMERICAL; break; }
+          l = __shfl_sync(FULL, q.idx, ql);
+          theta = __shfl_sync(FULL, q.v, ql);
+          qrc = __shfl_sync(FULL, q.rc, ql);
+        } else {  // every thread scans the partials (ascending warp)
+          Part q = sm.part[0];
 #pragma unroll
-        for (int u = 1; u < NWARP; ++u) {
-          const Part o = sm.part[u];
-          // (ratio, tie) order of warp_argmin: IEEE compare (-0 == +0), then the smaller key
-          if (o.idx >= 0 && (q.idx < 0 || o.v < q.v || (o.v == q.v && o.tie < q.tie))) q = o;
+          for (int u = 1; u < NWARP; ++u) {
+            const Part o = sm.part[u];
+            // (ratio, tie) order of warp_argmin: IEEE compare (-0 == +0), then the smaller key
+            if (o.idx >= 0 && (q.idx < 0 || o.v < q.v || (o.v == q.v && o.tie < q.tie))) q = o;
+          }
+          if (q.idx < 0) { st = (phase == 2) ? ST_UNBOUNDED : ST_NUMERICAL; break; }
+          l = q.idx;
+          theta = q.v;
+          qrc = q.rc;
         }
-        if (q.idx < 0) { st = (phase == 2) ? ST_UNBOUNDED : ST_NUMERICAL; break; }
-        l = q.idx;
-        theta = q.v;
-        qrc = q.rc;
       }
 
       LPB_PROF_MARK(4)
@@ -577,16 +588,29 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
       {
         const int leaving = sm.leaving;
         double pv[BC];
-        bool slow_any = false;
+        double prr;
+        // the RPW thread-rows of a warp hold the same positions: each divides every RPW-th of
+        // the BC positions and the RHS (g = k*RPW + group), and the quotients travel by
+        // shuffle from the lane with the same tc in the owning group
+        constexpr int QN = (BC + 1 + RPW - 1) / RPW;
+        const int grp = lane / TC;
+        double q[QN];
+        bool sl_any = false;
 #pragma unroll
-        for (int b = 0; b < BC; ++b) {
+        for (int k = 0; k < QN; ++k) {
+          const int g = k * RPW + grp;
+          const double raw = (g < BC) ? sm.prow[tc + TC * (g < BC ? g : 0)] : rhs_l;
           bool sl;
-          pv[b] = div_with(sm.prow[tc + TC * b], pe, rpe, sl);
-          slow_any |= sl;
+          q[k] = div_with(raw, pe, rpe, sl);
+          sl_any |= sl && g <= BC;
         }
-        bool slr;
-        double prr = div_with(rhs_l, pe, rpe, slr);
-        if (slow_any || slr) {  // rare: outside div_with's fast range -> IEEE __ddiv_rn
+#pragma unroll
+        for (int b = 0; b <= BC; ++b) {
+          const double v = __shfl_sync(FULL, q[b / RPW], (lane % TC) + TC * (b % RPW));
+          if (b < BC) pv[b] = v;
+          else prr = v;
+        }
+        if (__any_sync(FULL, sl_any)) {  // rare: outside div_with's fast range -> IEEE __ddiv_rn
 #pragma unroll
           for (int b = 0; b < BC; ++b) pv[b] = ddiv_slow(sm.prow[tc + TC * b], pe);
           prr = ddiv_slow(rhs_l, pe);
