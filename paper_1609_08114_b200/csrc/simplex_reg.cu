@@ -671,6 +671,34 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
           bool bval = false;
           int bb = 0;
           unsigned bvar = 0xffffffffu;
+          if constexpr (!RPC) {
+            // the first maximum over b, then this thread's variable at it; an exact tie
+            // inside a thread (rare) redoes the scan with the variable-index rule
+#pragma unroll
+            for (int b = 0; b < BC; ++b) {
+              const double v = p1n ? d1[TWO ? b : 0] : d2[b];
+              const bool take = v > bv;
+              bv = take ? v : bv;
+              bb = take ? b : bb;
+            }
+            int neq = 0;
+#pragma unroll
+            for (int b = 0; b < BC; ++b) neq += ((p1n ? d1[TWO ? b : 0] : d2[b]) == bv);
+            bvar = (unsigned)sm.nbvar[tc + TC * bb];
+            if (__any_sync(FULL, neq > 1 && bv > a.eps_enter)) {
+              bv = neg_inf();
+              bvar = 0xffffffffu;
+#pragma unroll
+              for (int b = 0; b < BC; ++b) {
+                const double v = p1n ? d1[TWO ? b : 0] : d2[b];
+                const unsigned var = (unsigned)sm.nbvar[tc + TC * b];
+                const bool take = v > bv || (v == bv && var < bvar);
+                bv = take ? v : bv;
+                bb = take ? b : bb;
+                bvar = take ? var : bvar;
+              }
+            }
+          } else {
 #pragma unroll
           for (int b = 0; b < BC; ++b) {
             const double v = p1n ? d1[TWO ? b : 0] : d2[b];
@@ -688,6 +716,7 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
             }
             bb = take ? b : bb;
             bvar = take ? var : bvar;
+          }
           }
           const bool val = (RPC ? bval : bv > a.eps_enter) && (RPW == 1 || lane < TC);
           const unsigned long long key = RPC ? bu : okey(bv);
