@@ -1,4 +1,4 @@
-"""Small batches through every kernel (size classes S, W, R, T, M, L on 2/4/8/16-CTA
+"""Small batches through every kernel (size classes S, W, R, M, L on 2/4/8/16-CTA
 clusters, the phase-I warm start, hyperbox TMA-ring and plain kernels), for
 compute-sanitizer (memcheck / racecheck / synccheck / initcheck):
     compute-sanitizer --tool racecheck python scripts/sanitize.py"""
@@ -24,7 +24,7 @@ def run(A, b, c, **kw):
 
 A, b, c = lpgen.status_mix(64, 6, 6, 1, infeasible_start=True)
 # S: register kernel + deferred two-phase LPs in list mode; W: element layout + generic warps
-for kl in ("S", "W", "R", "T", "M", "L"):
+for kl in ("S", "W", "R", "M", "L"):
     st, li = run(A, b, c, kernel_class=kl)
     print(kl, li, np.bincount(st, minlength=5))
 A, b, c = lpgen.status_mix(20000, 5, 5, 7, infeasible_start=True)  # 128-thread S CTAs
