@@ -33,6 +33,7 @@
 #include "lpb_internal.cuh"
 #include "lpb_reduce.cuh"
 #include "lpb_rng.cuh"
+#include "lpb_tmem.cuh"
 
 namespace lpb {
 namespace {
@@ -80,6 +81,7 @@ struct RegSmem {
   uint64_t mbar;         // completes when the prefetched A of LP `lp` has landed
   int lp;
   int leaving;
+  uint32_t tmem;         // TMEM base address (TM layouts)
 };
 
 // Optional phase profiler, compiled in only with -DLPB_PROFILE (scripts/phase_prof.py builds
@@ -99,7 +101,11 @@ struct RegSmem {
 // AS > 0: each thread also owns AS more rows (i = tr + TR*(A+s)) kept in a thread-private
 // SMEM slice (double2 pairs of positions, thread-interleaved: conflict-free 128-bit accesses),
 // so that three LPs fit one SM (registers + SMEM) instead of two (registers only).
-template <int TR, int TC, int A, int AS, int BC, bool TWO, int MINB, bool RPC>
+// TM: the AS extra rows live in TENSOR MEMORY instead (lpb_tmem.cuh): thread tid owns TMEM
+// lane tid, row slot s at columns 16 s .. 16 s + 13 (BC doubles), reached with tcgen05.ld/st
+// from the whole warp at a warp-uniform column; no SMEM traffic and no prefetch buffer, so
+// three CTAs (LPs) share an SM: 2/3 of the tableau in registers, 1/3 in TMEM.
+template <int TR, int TC, int A, int AS, int BC, bool TWO, int MINB, bool RPC, bool TM = false>
 __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs a) {
   constexpr int AT = A + AS;  // rows per thread-row
   constexpr int NT = TR * TC, RCAP = TR * AT, CCAP = TC * BC, NWARP = NT / 32;
@@ -107,8 +113,15 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
   constexpr int BH = (BC + 1) / 2;  // double2 pairs per SMEM row
   static_assert(NT % 32 == 0 && 32 % TC == 0 && TR <= 32 && AT <= 32 && BC <= 32, "layout");
   static_assert(RPW * AT <= 32, "the warp's rows must fit its lanes");
+  static_assert(!TM || (!TWO && TR * TC == 128 && AS * 16 <= 128 && BC <= 8), "TMEM layout");
   __shared__ RegSmem<TR, TC, AT, BC> sm;
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  // TM layouts (128 registers): threadIdx.x through a volatile asm, so that the compiler
+  // cannot re-read it (S2R, ~20 cycles) at every use under register pressure; the derived
+  // indices are rebuilt from one register (measured: cfg2 -3.8 %; neutral elsewhere)
+  int tid_;
+  if constexpr (TM) asm volatile("mov.u32 %0, %%tid.x;" : "=r"(tid_));
+  else tid_ = threadIdx.x;
+  const int tid = tid_, lane = tid & 31, w = tid >> 5;
   const int tr = tid / TC, tc = tid - (tid / TC) * TC;
   // the row this lane serves in the warp-parallel ratio test
   const int rrow = (w * RPW + lane % RPW) + TR * (lane / RPW);
@@ -132,6 +145,14 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
     return Ts1[(size_t)((s_ * BH + (b_ >> 1)) * NT) * 2 + (b_ & 1)];
   };
   const bool pf = AS == 0 && a.prefetch != 0;
+  uint32_t tbase = 0;  // this thread's TMEM lane, column 0 (TM)
+  if constexpr (TM) {
+    if (w == 0) tm_alloc<128>(&sm.tmem);
+    tm_fence_before();
+    gsync<NT>();
+    tm_fence_after();
+    tbase = sm.tmem + ((uint32_t)(w * 32) << 16);
+  }
   const bool direct = a.ticket == nullptr;
   const uint32_t abytes = (uint32_t)((int64_t)m * n * 8);
   uint32_t mphase = 0;
@@ -227,6 +248,7 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
       const int i = tr + TR * (A + s_);
       const bool rowok = (i < m) && st < 0;
       const bool neg = rowok && sm.bkey[i] < 0;
+      uint32_t cell[16];
 #pragma unroll
       for (int b = 0; b < BC; ++b) {
         const int p = tc + TC * b;
@@ -239,9 +261,16 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
             v = (i == sm.negrows[p - n]) ? -1.0 : (neg ? -0.0 : 0.0);
           }
         }
-        ts(s_, b) = v;
+        if constexpr (TM) tm_split(v, cell[2 * b], cell[2 * b + 1]);
+        else ts(s_, b) = v;
+      }
+      if constexpr (TM) {
+#pragma unroll
+        for (int k = 2 * BC; k < 16; ++k) cell[k] = 0u;
+        tm_st16(tbase + 16 * s_, cell);
       }
     }
+    if constexpr (TM) tm_wait_st();
     // padding positions (and, later, dead artificial positions) hold -inf in the objective
     // replicas: never a Step-1 candidate, and fma(f, p, -inf) keeps them -inf
 #pragma unroll
@@ -471,12 +500,27 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
     break;
         switch (be) { LPB_CASES(LPB_PUB) default: break; }
 #undef LPB_PUB
+        if constexpr (!TM) {
 #pragma unroll
-        for (int s_ = 0; s_ < AS; ++s_) {  // SMEM rows: dynamic position index
-          double& t = ts(s_, be);
-          colE[tr + TR * (A + s_)] = t;
-          t = 0.0;
+          for (int s_ = 0; s_ < AS; ++s_) {  // SMEM rows: dynamic position index
+            double& t = ts(s_, be);
+            colE[tr + TR * (A + s_)] = t;
+            t = 0.0;
+          }
         }
+      }
+      if constexpr (TM) {  // TMEM rows: the whole warp loads column be, the owners publish it
+        uint32_t lo[AS > 0 ? AS : 1], hi[AS > 0 ? AS : 1];
+#pragma unroll
+        for (int s_ = 0; s_ < AS; ++s_) tm_ld2(tbase + 16 * s_ + 2 * be, lo[s_], hi[s_]);
+        tm_wait_ld();
+        const bool own = tc == etc;
+#pragma unroll
+        for (int s_ = 0; s_ < AS; ++s_) {
+          if (own) colE[tr + TR * (A + s_)] = tm_d(lo[s_], hi[s_]);
+          tm_st2(tbase + 16 * s_ + 2 * be, own ? 0u : lo[s_], own ? 0u : hi[s_]);
+        }
+        tm_wait_st();  // the pivot-row load below may read these columns
       }
       __syncwarp();
       LPB_PROF_MARK(1)
@@ -571,13 +615,30 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
     break;
         switch (al) { LPB_CASES(LPB_PROW) default: break; }
 #undef LPB_PROW
-        if (AS > 0 && al >= A) {  // pivot row in SMEM
+        if (!TM && AS > 0 && al >= A) {  // pivot row in SMEM
           const int s_ = al - A;
 #pragma unroll
           for (int b = 0; b < BC; ++b) {
             sm.prow[tc + TC * b] = (tc + TC * b == e) ? 1.0 : ts(s_, b);
             ts(s_, b) = 0.0;
           }
+        }
+      }
+      if constexpr (TM) {
+        if (al >= A) {  // pivot row in TMEM (warp-uniform): whole-warp load, owners publish
+          const int s_ = al - A;
+          uint32_t cell[16];
+          tm_ld16(tbase + 16 * s_, cell);
+          tm_wait_ld();
+          const bool own = tr == ltr;
+#pragma unroll
+          for (int b = 0; b < BC; ++b) {
+            if (own) sm.prow[tc + TC * b] = (tc + TC * b == e) ? 1.0 : tm_d(cell[2 * b], cell[2 * b + 1]);
+            cell[2 * b] = own ? 0u : cell[2 * b];
+            cell[2 * b + 1] = own ? 0u : cell[2 * b + 1];
+          }
+          tm_st16(tbase + 16 * s_, cell);
+          tm_wait_st();
         }
       }
       const double rpe = drive ? recip_of(pe) : qrc;  // the winning ratio lane's reciprocal
@@ -639,8 +700,23 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
 #pragma unroll
           for (int b = 0; b < BC; ++b) T[ai][b] = __fma_rn(fi, pv[b], T[ai][b]);
         }
+        if constexpr (TM) {  // TMEM rows: load, fma, store one slot at a time
 #pragma unroll
-        for (int s_ = 0; s_ < AS; ++s_) {  // SMEM rows, two positions per 128-bit access
+          for (int s_ = 0; s_ < AS; ++s_) {
+            const double fi = sm.fcol[par][tr + TR * (A + s_)];
+            uint32_t cell[16];
+            tm_ld16(tbase + 16 * s_, cell);
+            tm_wait_ld();
+#pragma unroll
+            for (int b = 0; b < BC; ++b)
+              tm_split(__fma_rn(fi, pv[b], tm_d(cell[2 * b], cell[2 * b + 1])), cell[2 * b],
+                       cell[2 * b + 1]);
+            tm_st16(tbase + 16 * s_, cell);
+          }
+          tm_wait_st();
+        }
+#pragma unroll
+        for (int s_ = 0; s_ < (TM ? 0 : AS); ++s_) {  // SMEM rows, two positions per 128-bit access
           const double fi = sm.fcol[par][tr + TR * (A + s_)];
 #pragma unroll
           for (int h = 0; h < BH; ++h) {
@@ -776,6 +852,12 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
     }
     gsync<NT>();
   }
+  if constexpr (TM) {
+    tm_fence_before();
+    gsync<NT>();
+    tm_fence_after();
+    if (w == 0) tm_dealloc<128>(sm.tmem);
+  }
 #ifdef LPB_PROFILE
   if (prof_on && lane == 0)
     for (int q = 0; q < 12; ++q)
@@ -801,11 +883,19 @@ struct RegCfg {
   X(6, 8, 16, 13, 0, 7, false, 2)       \
   X(4, 16, 16, 7, 0, 7, false, 1)       \
   X(5, 16, 16, 7, 0, 7, true, 1)
+// TMEM layouts (TM = true): A register rows + AS rows in tensor memory.  Layout 15 replaces
+// layout 6 (type-1 LPs up to 104 x 112, cfg2): 5 of each thread's 13 rows in registers, 8 in
+// TMEM (8 x 16 columns), 128 registers, FOUR CTAs (LPs) per SM instead of two.  Measured on
+// cfg2: 4 LPs/SM 19.7 ms (then 19.0 with the tid register) vs 20.4 ms for layout 6; 3 LPs/SM
+// with 8 or 5 register rows: 21.4 / 23.4 ms.
+#define LPB_REG_TM_CONFIGS(X)           \
+  X(15, 8, 16, 5, 8, 7, false, 4)
 
-template <int TR, int TC, int A, int AS, int BC, bool TWO, int MINB, bool RPC>
+template <int TR, int TC, int A, int AS, int BC, bool TWO, int MINB, bool RPC, bool TM = false>
 cudaError_t launch_one(const SimplexArgs& a, int grid_override, cudaStream_t s, int* ctas) {
-  auto kern = simplex_reg_kernel<TR, TC, A, AS, BC, TWO, MINB, RPC>;
-  const size_t dsm = AS > 0 ? (size_t)AS * ((BC + 1) / 2) * TR * TC * 16
+  auto kern = simplex_reg_kernel<TR, TC, A, AS, BC, TWO, MINB, RPC, TM>;
+  const size_t dsm = TM ? 0
+                   : AS > 0 ? (size_t)AS * ((BC + 1) / 2) * TR * TC * 16
                             : (a.prefetch ? (size_t)a.m * a.n * 8 : 0);
   // attribute + occupancy queries are host round trips: cache them per (device, smem size)
   static LaunchMemo memo;
@@ -816,6 +906,9 @@ cudaError_t launch_one(const SimplexArgs& a, int grid_override, cudaStream_t s, 
     return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, kern, TR * TC, dsm);
   });
   if (em != cudaSuccess) return em;
+  // TMEM layouts: the occupancy query reports 1 CTA/SM for tcgen05 kernels; MINB CTAs are
+  // co-resident (registers) and their TMEM columns (MINB x 128 <= 512) fit
+  if (TM) per_sm = MINB;
   int64_t grid = (int64_t)(per_sm < 1 ? 1 : per_sm) * device_sm_count();
   SimplexArgs d = a;
   if (a.batch <= grid && grid_override <= 0) {
@@ -840,6 +933,11 @@ static const RegCfg kCfgs[] = {
     LPB_REG_CONFIGS(X)
 #undef X
 };
+static const RegCfg kTmCfgs[] = {
+#define X(id, TR, TC, A, AS, BC, TWO, MINB) {TR * (A + AS), TC * BC, TWO ? 1 : 0, id},
+    LPB_REG_TM_CONFIGS(X)
+#undef X
+};
 
 static int pick_cfg(int m, int n, int kmax) {
 #ifdef LPB_DEV_HOOKS
@@ -848,11 +946,15 @@ static int pick_cfg(int m, int n, int kmax) {
     const int id = atoi(f);
     for (const RegCfg& c : kCfgs)
       if (c.id == id && m <= c.rcap && n + kmax <= c.ccap && (kmax == 0 || c.two)) return id;
+    for (const RegCfg& c : kTmCfgs)
+      if (c.id == id && m <= c.rcap && n + kmax <= c.ccap && (kmax == 0 || c.two)) return id;
   }
 #endif
   for (const RegCfg& c : kCfgs) {
     if (m > c.rcap || n + kmax > c.ccap) continue;
     if (kmax > 0 && !c.two) continue;
+    // layout 6's sizes run on the TMEM layout 15 (same capacity, 4 LPs/SM instead of 2)
+    if (c.id == 6 && !dev_flag("LPB_NO_TMEM")) return 15;
     return c.id;
   }
   return -1;
@@ -870,6 +972,12 @@ cudaError_t launch_simplex_reg(const SimplexArgs& a, int grid_override, cudaStre
     return a.rpc ? launch_one<TR, TC, A, AS, BC, TWO, MINB, true>(a, grid_override, s, ctas_out) \
                  : launch_one<TR, TC, A, AS, BC, TWO, MINB, false>(a, grid_override, s, ctas_out);
     LPB_REG_CONFIGS(X)
+#undef X
+#define X(id, TR, TC, A, AS, BC, TWO, MINB) \
+  case id:                                                                        \
+    return a.rpc ? launch_one<TR, TC, A, AS, BC, TWO, MINB, true, true>(a, grid_override, s, ctas_out) \
+                 : launch_one<TR, TC, A, AS, BC, TWO, MINB, false, true>(a, grid_override, s, ctas_out);
+    LPB_REG_TM_CONFIGS(X)
 #undef X
     default: return cudaErrorInvalidValue;
   }
