@@ -113,7 +113,9 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
   constexpr int BH = (BC + 1) / 2;  // double2 pairs per SMEM row
   static_assert(NT % 32 == 0 && 32 % TC == 0 && TR <= 32 && AT <= 32 && BC <= 32, "layout");
   static_assert(RPW * AT <= 32, "the warp's rows must fit its lanes");
-  static_assert(!TM || (!TWO && TR * TC == 128 && AS * 16 <= 128 && BC <= 8), "TMEM layout");
+  static_assert(!TM || (!TWO && (TR * TC == 128 || TR * TC == 64) && AS * 16 <= 128 && BC <= 8),
+                "TMEM layout");
+  constexpr int TMCOLS = AS * 16 <= 32 ? 32 : AS * 16 <= 64 ? 64 : 128;  // power of two
   __shared__ RegSmem<TR, TC, AT, BC> sm;
   // TM layouts (128 registers): threadIdx.x through a volatile asm, so that the compiler
   // cannot re-read it (S2R, ~20 cycles) at every use under register pressure; the derived
@@ -147,7 +149,7 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
   const bool pf = AS == 0 && a.prefetch != 0;
   uint32_t tbase = 0;  // this thread's TMEM lane, column 0 (TM)
   if constexpr (TM) {
-    if (w == 0) tm_alloc<128>(&sm.tmem);
+    if (w == 0) tm_alloc<TMCOLS>(&sm.tmem);
     tm_fence_before();
     gsync<NT>();
     tm_fence_after();
@@ -856,7 +858,7 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
     tm_fence_before();
     gsync<NT>();
     tm_fence_after();
-    if (w == 0) tm_dealloc<128>(sm.tmem);
+    if (w == 0) tm_dealloc<TMCOLS>(sm.tmem);
   }
 #ifdef LPB_PROFILE
   if (prof_on && lane == 0)
@@ -887,9 +889,12 @@ struct RegCfg {
 // layout 6 (type-1 LPs up to 104 x 112, cfg2): 5 of each thread's 13 rows in registers, 8 in
 // TMEM (8 x 16 columns), 128 registers, FOUR CTAs (LPs) per SM instead of two.  Measured on
 // cfg2: 4 LPs/SM 19.7 ms (then 19.0 with the tid register) vs 20.4 ms for layout 6; 3 LPs/SM
-// with 8 or 5 register rows: 21.4 / 23.4 ms.
+// with 8 or 5 register rows: 21.4 / 23.4 ms.  Layout 17 replaces layout 8 (up to 56 x 56,
+// cfg10): 3 + 4 rows, 64-thread CTAs with 64 TMEM columns each, EIGHT LPs per SM instead of
+// four (TMEM's 512 columns are the limit): cfg10 3.47 -> 2.95 ms.
 #define LPB_REG_TM_CONFIGS(X)           \
-  X(15, 8, 16, 5, 8, 7, false, 4)
+  X(15, 8, 16, 5, 8, 7, false, 4)       \
+  X(17, 8, 8, 3, 4, 7, false, 8)
 
 template <int TR, int TC, int A, int AS, int BC, bool TWO, int MINB, bool RPC, bool TM = false>
 cudaError_t launch_one(const SimplexArgs& a, int grid_override, cudaStream_t s, int* ctas) {
@@ -953,8 +958,10 @@ static int pick_cfg(int m, int n, int kmax) {
   for (const RegCfg& c : kCfgs) {
     if (m > c.rcap || n + kmax > c.ccap) continue;
     if (kmax > 0 && !c.two) continue;
-    // layout 6's sizes run on the TMEM layout 15 (same capacity, 4 LPs/SM instead of 2)
+    // layout 6's sizes run on the TMEM layout 15 (same capacity, 4 LPs/SM instead of 2),
+    // layout 8's on layout 17 (same capacity, 8 LPs/SM instead of 4)
     if (c.id == 6 && !dev_flag("LPB_NO_TMEM")) return 15;
+    if (c.id == 8 && !dev_flag("LPB_NO_TMEM")) return 17;
     return c.id;
   }
   return -1;
