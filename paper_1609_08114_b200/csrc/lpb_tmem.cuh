@@ -20,6 +20,15 @@ __device__ __forceinline__ void tm_alloc(uint32_t* dst) {
                    smem_u32(dst)), "n"(NCOL));
   asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
 }
+// Runtime column count (a power of two >= 32).
+__device__ __forceinline__ void tm_alloc_n(uint32_t* dst, uint32_t ncol) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                   smem_u32(dst)), "r"(ncol));
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+}
+__device__ __forceinline__ void tm_dealloc_n(uint32_t taddr, uint32_t ncol) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(taddr), "r"(ncol));
+}
 template <int NCOL>
 __device__ __forceinline__ void tm_dealloc(uint32_t taddr) {
   asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(taddr), "n"(NCOL));

@@ -33,6 +33,7 @@
 #include "lpb_internal.cuh"
 #include "lpb_reduce.cuh"
 #include "lpb_rng.cuh"
+#include "lpb_tmem.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -328,9 +329,216 @@ __device__ __forceinline__ int compact_live(const Smem& s, int S, int cnt, int n
   return tot;
 }
 
+// ---- TMR variants: the constraint rows live in TENSOR MEMORY during the pivot loop ----
+// The L class is bound by SMEM bandwidth in its rank-1 update (16 B of SMEM traffic per
+// element, 128 B/clk/SM).  TMEM (128 lanes x 512 columns x 32 bit per SM) has its own
+// datapath (scripts/ubench/tmem_bw.cu: ~155 B/clk/SM read plus as much written), so the TMR
+// variants keep constraint row r in TMEM lane r % 128, row slot r / 128, position j of the
+// CTA's range at columns slot * sc + 2j, 2j + 1 (one fp64 per column pair).  Warp w reaches
+// lanes 32 (w % 4) .. + 31 (the 32x32b shapes), so the 8 warps of a CTA form two halves
+// (h = w / 4) over the same lanes: half h updates the 8-position chunks c = h, h + 2, ... of
+// every row of its lanes, and serves the row slots s = h, h + 2, ... in the ratio test.  The
+// objective rows (Step 1) stay in SMEM.  The SMEM rows are still the storage of record for
+// the build, the phase switch (drive-out + compaction) and the extraction: the rows are
+// copied TMEM <-> SMEM at those points (once or twice per LP), and the pivot loop in between
+// never touches the SMEM copies of the constraint rows.
+constexpr int TM_NS = 4;     // row slots (m <= 512)
+// row slots a TMR variant is compiled for (register arrays): 2-CTA clusters m <= 256, 4-CTA
+// m <= 384, larger clusters m <= 512
+__host__ __device__ constexpr int tm_ns_max(int cl) { return cl <= 2 ? 2 : cl <= 4 ? 3 : 4; }
+constexpr int TM_COLS = 512; // the whole TMEM of the SM: TMR launches run 1 CTA per SM
+
+struct TmRows {
+  uint32_t tb;  // TMEM address of this warp's lane quarter, column 0
+  int ns, sc;   // row slots in use, columns per slot (16 per 8-position chunk)
+  int q, h;     // lane quarter (w % 4), half (w / 4)
+};
+
+__host__ __device__ __forceinline__ int tm_slot_cols(int Q) { return 16 * ((Q + 1 + 7) / 8); }
+__host__ __device__ __forceinline__ int tm_slots(int m) { return (m + 127) / 128; }
+
+// Every TMEM write of this thread has landed, and a barrier orders it before the other
+// threads' TMEM accesses (and theirs before ours).
+__device__ __forceinline__ void tm_sync() {
+  tm_wait_st();
+  tm_fence_before();
+  __syncthreads();
+  tm_fence_after();
+}
+
+// SMEM rows [0, m) -> TMEM (nch chunks of 8 positions); ends with tm_sync().
+__device__ __forceinline__ void tm_rows_from_smem(const Smem& s, const TmRows& t, int S, int m,
+                                                  int nch) {
+  const int lane = threadIdx.x & 31;
+  for (int sl = 0; sl < t.ns; ++sl) {
+    if (128 * sl + 32 * t.q >= m) break;  // warp-uniform: no row of this warp
+    const int r = 128 * sl + 32 * t.q + lane;
+    const double* row = s.T + (size_t)(r < m ? r : 0) * S;
+    for (int c = t.h; c < nch; c += 2) {
+      uint32_t v[16];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int j = 8 * c + k;
+        tm_split((r < m && j < S) ? row[j] : 0.0, v[2 * k], v[2 * k + 1]);
+      }
+      tm_st16(t.tb + sl * t.sc + 16 * c, v);
+    }
+  }
+  tm_sync();
+}
+
+// TMEM rows [0, m) -> SMEM; ends with a barrier.
+__device__ __forceinline__ void tm_rows_to_smem(const Smem& s, const TmRows& t, int S, int m,
+                                                int nch) {
+  const int lane = threadIdx.x & 31;
+  for (int sl = 0; sl < t.ns; ++sl) {
+    if (128 * sl + 32 * t.q >= m) break;
+    const int r = 128 * sl + 32 * t.q + lane;
+    double* row = s.T + (size_t)(r < m ? r : 0) * S;
+    for (int c = t.h; c < nch; c += 2) {
+      uint32_t v[16];
+      tm_ld16(t.tb + sl * t.sc + 16 * c, v);
+      tm_wait_ld();
+      if (r < m) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int j = 8 * c + k;
+          if (j < S) row[j] = tm_d(v[2 * k], v[2 * k + 1]);
+        }
+      }
+    }
+  }
+  tm_fence_before();
+  __syncthreads();
+  tm_fence_after();
+}
+
+// Step 3 of the TMR variants (same arithmetic as pivot_local): row l (< m) is fetched from
+// TMEM into its SMEM row by the two warps of its lane quarter (the owner lane stores, every
+// lane writes back, the owner zeros), then the divisions by PE run as in pivot_local, column
+// jloc is zeroed in TMEM (owner CTA), and the update runs chunk by chunk over the TMEM rows
+// (the 8 pivot-row quotients of a chunk are SMEM broadcasts) and row by row over the SMEM
+// objective rows [m, nrow).
+template <int NSX>
+__device__ __forceinline__ void pivot_local_tm(const Smem& s, const TmRows& t, const double* colE,
+                                               int S, int Wa, int m, int nrow, int l, bool own,
+                                               int jloc, int ent_var, const RecRow& rec) {
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int nch = (Wa + 7) >> 3;
+  if (t.q == ((l >> 5) & 3)) {  // the pivot row's lane quarter (warp-uniform)
+    const int sl = l >> 7;
+    const bool ol = lane == (l & 31);
+    constexpr int FB = 1;  // chunks in flight per wait (measured: 4 is no faster)
+    for (int c0 = t.h; c0 < nch; c0 += 2 * FB) {
+      uint32_t v[FB][16];
+#pragma unroll
+      for (int u = 0; u < FB; ++u)
+        if (c0 + 2 * u < nch) tm_ld16(t.tb + sl * t.sc + 16 * (c0 + 2 * u), v[u]);
+      tm_wait_ld();
+#pragma unroll
+      for (int u = 0; u < FB; ++u) {
+        const int c = c0 + 2 * u;
+        if (c < nch) {
+          if (ol) {  // 128-bit stores (S is even: pairs never straddle the row end)
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const int j = 8 * c + 2 * k;
+              if (j < S)
+                *reinterpret_cast<double2*>(s.T + l * S + j) =
+                    make_double2(tm_d(v[u][4 * k], v[u][4 * k + 1]),
+                                 tm_d(v[u][4 * k + 2], v[u][4 * k + 3]));
+            }
+          }
+#pragma unroll
+          for (int k = 0; k < 16; ++k) v[u][k] = ol ? 0u : v[u][k];
+          tm_st16(t.tb + sl * t.sc + 16 * c, v[u]);
+        }
+      }
+    }
+  }
+  if (own && t.h == ((jloc >> 3) & 1))  // the swapped column starts from 0 (as pivot_local)
+    for (int sl = 0; sl < t.ns; ++sl)
+      if (128 * sl + 32 * t.q < m) tm_st2(t.tb + sl * t.sc + 2 * jloc, 0u, 0u);
+  tm_sync();
+  const double pe = colE[l];
+  const double rpe = recip_of(pe);
+  for (int j = tid; j < Wa; j += NT) {
+    const bool sw = own && j == jloc;
+    const double num = sw ? 1.0 : s.T[l * S + j];
+    bool slow;
+    double q = div_with(num, pe, rpe, slow);
+    if (slow) q = ddiv_slow(num, pe);
+    s.prow[j] = q;
+    if (rec.row) {
+      if (j < Wa - 1) rec.row[rec.g0 + j] = q;
+      else if (rec.rank0) rec.row[rec.npos] = q;
+    }
+  }
+  for (int i = tid; i < nrow; i += NT) {
+    s.fcol[i] = (i == l) ? 1.0 : -colE[i];
+    if (own && i >= m) s.T[i * S + jloc] = 0.0;
+  }
+  if (tid == 0) {
+    const int leaving = s.bkey[l];
+    s.bkey[l] = ent_var;
+    if (own) s.nbvar[jloc] = leaving < 0 ? DEAD : leaving;
+    if (Wa & 1) s.prow[Wa] = 0.0;
+  }
+  __syncthreads();
+  // objective rows (SMEM): lanes walk 128-bit column pairs
+  {
+    const int Wa2 = (Wa + 1) >> 1, S2 = S >> 1;
+    const double2* prow2 = reinterpret_cast<const double2*>(s.prow);
+    double2* T2 = reinterpret_cast<double2*>(s.T);
+    for (int i = m + w; i < nrow; i += NW) {
+      const double f = s.fcol[i];
+      for (int j = lane; j < Wa2; j += 32) {
+        const double2 p = prow2[j];
+        double2 v = T2[i * S2 + j];
+        v.x = __fma_rn(f, p.x, v.x);
+        v.y = __fma_rn(f, p.y, v.y);
+        T2[i * S2 + j] = v;
+      }
+    }
+  }
+  // constraint rows (TMEM): chunk c = h, h + 2, ...; the chunk's 8 quotients are loaded once
+  // and applied to every row slot of the lane
+  // chunk by chunk: the chunk's 8 quotients are loaded once and applied to every row slot of
+  // the lane (measured: batching several TMEM loads per wait is slower, cfg3 +10..20 %)
+  double f[NSX];
+#pragma unroll
+  for (int sl = 0; sl < NSX; ++sl) {
+    const int r = 128 * sl + 32 * t.q + lane;
+    f[sl] = (sl < t.ns && r < m) ? s.fcol[r] : 0.0;
+  }
+  const double2* prow2 = reinterpret_cast<const double2*>(s.prow);
+  for (int c = t.h; c < nch; c += 2) {
+    double2 p[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) p[k] = prow2[4 * c + k];
+#pragma unroll
+    for (int sl = 0; sl < NSX; ++sl) {
+      if (sl < t.ns && 128 * sl + 32 * t.q < m) {  // warp-uniform
+        uint32_t v[16];
+        const uint32_t ad = t.tb + sl * t.sc + 16 * c;
+        tm_ld16(ad, v);
+        tm_wait_ld();
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          tm_split(__fma_rn(f[sl], p[k].x, tm_d(v[4 * k], v[4 * k + 1])), v[4 * k], v[4 * k + 1]);
+          tm_split(__fma_rn(f[sl], p[k].y, tm_d(v[4 * k + 2], v[4 * k + 3])), v[4 * k + 2],
+                   v[4 * k + 3]);
+        }
+        tm_st16(ad, v);
+      }
+    }
+  }
+  tm_sync();
+}
+
 // PULL (proposal columns read over DSMEM after the barrier) is used for CL >= 8, and for
 // CL = 2/4 whenever its smaller SMEM footprint fits more CTAs per SM than PUSH (launch_cl).
-template <int CL, bool PULL>
+template <int CL, bool PULL, bool TMR>
 __global__ void __launch_bounds__(NT) simplex_block_kernel(SimplexArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const Cluster<CL> cl;
@@ -372,8 +580,17 @@ __global__ void __launch_bounds__(NT) simplex_block_kernel(SimplexArgs a) {
   // DSMEM may only be touched once every CTA of the cluster is running: one
   // cluster barrier before the first remote ticket write (racecheck finding); it also
   // publishes the initialised mbarriers.
+  TmRows tm{0u, tm_slots(m), tm_slot_cols(Q), w & 3, w >> 2};
+  if constexpr (TMR) {
+    if (w == 0) tm_alloc_n(reinterpret_cast<uint32_t*>(&s.ctl->pad), TM_COLS);
+    tm_fence_before();
+  }
   if constexpr (CL > 1) cl.sync();
-  else if (XASYNC) __syncthreads();
+  else if (XASYNC || TMR) __syncthreads();
+  if constexpr (TMR) {
+    tm_fence_after();
+    tm.tb = (uint32_t)s.ctl->pad + ((uint32_t)(32 * tm.q) << 16);
+  }
 
   int par = 0;
   for (;;) {
@@ -422,6 +639,7 @@ __global__ void __launch_bounds__(NT) simplex_block_kernel(SimplexArgs a) {
     __syncthreads();
 
     int st = -1, it1 = 0, it2 = 0;
+    bool tm_live = false;  // TMR: the constraint rows are in TMEM (not their SMEM copies)
     const uint64_t lpkey = a.rpc ? rpc_lp_key(a.rpc_seed, a.lp_base + lp) : 0ull;
     int cnt = max(0, min(Q, n + k - cl.rank * Q));  // live local positions
     int Wa = cnt + 1;                               // + RHS at local column cnt
@@ -469,6 +687,10 @@ __global__ void __launch_bounds__(NT) simplex_block_kernel(SimplexArgs a) {
         __syncthreads();
         cnt = compact_live(s, S, cnt, m + 1);  // phase II from here on: drop dead positions
         Wa = cnt + 1;
+        if constexpr (TMR) {
+          tm_rows_from_smem(s, tm, S, m, (Wa + 7) >> 3);
+          tm_live = true;
+        }
       }
     } else if (st < 0) {
       for (int i = w; i < m; i += NW) {
@@ -504,6 +726,10 @@ __global__ void __launch_bounds__(NT) simplex_block_kernel(SimplexArgs a) {
         }
       }
       __syncthreads();
+      if constexpr (TMR) {
+          tm_rows_from_smem(s, tm, S, m, (Wa + 7) >> 3);
+          tm_live = true;
+        }
     }
 
     // ---- Steps 1-3 loop, two phases ----
@@ -533,7 +759,32 @@ __global__ void __launch_bounds__(NT) simplex_block_kernel(SimplexArgs a) {
       ce = bland ? block_reduce<MIN_KEY>(ce, s.wslots) : block_reduce<MAX_V>(ce, s.wslots);
       Cand cr{0.0, 0, -1};
       const int jc = ce.pos - g0;  // local column of the proposal
-      if (ce.pos >= 0) {
+      const int jcs = ce.pos >= 0 ? jc : 0;  // the column sent (ignored without a candidate)
+      double cv[TMR ? TM_NS : 1];  // TMR: column jcs of this thread's TMEM rows
+      if constexpr (TMR) {
+#pragma unroll
+        for (int sl = 0; sl < TM_NS; ++sl) {
+          cv[sl] = 0.0;
+          if (sl < tm.ns && (sl & 1) == tm.h && 128 * sl + 32 * tm.q < m) {  // warp-uniform
+            uint32_t a0, a1, b0, b1;
+            tm_ld2(tm.tb + sl * tm.sc + 2 * jcs, a0, a1);
+            tm_ld2(tm.tb + sl * tm.sc + 2 * cnt, b0, b1);
+            tm_wait_ld();
+            const int i = 128 * sl + 32 * tm.q + lane;
+            const double ai = tm_d(a0, a1);
+            cv[sl] = ai;
+            if (ce.pos >= 0 && i < m && ai > a.eps_piv) {
+              const double ri = tm_d(b0, b1);
+              bool slow;
+              double r = div_fast(ri, ai, slow);
+              if (slow) r = ddiv_slow(ri, ai);
+              const Cand cc{r, bland ? s.bkey[i] : i, i};
+              if (better<MIN_V>(cc, cr)) cr = cc;
+            }
+          }
+        }
+        tm_fence_before();  // these loads precede the update's stores (after the barriers)
+      } else if (ce.pos >= 0) {
         for (int i = tid; i < m; i += NT) {
           const double ai = s.T[i * S + jc];
           if (ai > a.eps_piv) {
@@ -556,7 +807,6 @@ __global__ void __launch_bounds__(NT) simplex_block_kernel(SimplexArgs a) {
       if constexpr (XASYNC) {
         // every CTA sends a column (column 0 when it has no candidate, then ignored), so
         // each receiver expects exactly (CL - 1) columns + records
-        const int jcs = ce.pos >= 0 ? jc : 0;
         if (tid == 0) mbar_arrive_expect(&s.xbar[pp], (CL - 1) * (nrow * 8 + (int)sizeof(Rec)));
         uint32_t rb[CL], rc[CL];
 #pragma unroll
@@ -564,7 +814,19 @@ __global__ void __launch_bounds__(NT) simplex_block_kernel(SimplexArgs a) {
           rb[q] = cluster_addr(myc, q);
           rc[q] = cluster_addr(&s.xbar[pp], q);
         }
-        for (int i = tid; i < nrow; i += NT) {
+        if constexpr (TMR) {
+#pragma unroll
+          for (int sl = 0; sl < TM_NS; ++sl) {
+            const int i = 128 * sl + 32 * tm.q + lane;
+            if (sl < tm.ns && (sl & 1) == tm.h && i < m) {
+              myc[i] = cv[sl];
+#pragma unroll
+              for (int q = 0; q < CL; ++q)
+                if (q != cl.rank) st_async_f64(rb[q] + 8u * i, cv[sl], rc[q]);
+            }
+          }
+        }
+        for (int i = (TMR ? m : 0) + tid; i < nrow; i += NT) {
           const double v = s.T[i * S + jcs];
           myc[i] = v;
 #pragma unroll
@@ -588,8 +850,22 @@ __global__ void __launch_bounds__(NT) simplex_block_kernel(SimplexArgs a) {
         mbar_wait_cluster(&s.xbar[pp], (xph >> pp) & 1u);
         xph ^= 1u << pp;
       } else {
+        if (TMR && ce.pos >= 0) {
+#pragma unroll
+          for (int sl = 0; sl < TM_NS; ++sl) {
+            const int i = 128 * sl + 32 * tm.q + lane;
+            if (sl < tm.ns && (sl & 1) == tm.h && i < m) {
+              if constexpr (PULL) {
+                myc[i] = cv[sl];
+              } else {
+#pragma unroll
+                for (int q = 0; q < CL; ++q) cl.remote(myc, q)[i] = cv[sl];
+              }
+            }
+          }
+        }
         if (ce.pos >= 0)
-          for (int i = tid; i < nrow; i += NT) {
+          for (int i = (TMR ? m : 0) + tid; i < nrow; i += NT) {
             const double v = s.T[i * S + jc];
             if constexpr (PULL) {
               myc[i] = v;
@@ -618,6 +894,10 @@ __global__ void __launch_bounds__(NT) simplex_block_kernel(SimplexArgs a) {
       if (ce.pos < 0) {
         if (phase == 2) { st = ST_OPTIMAL; break; }
         // phase switch (R8, R9): infeasibility test, drive artificials out, drop phase-I row
+        if (TMR && tm_live) {  // the SMEM path from here
+          tm_rows_to_smem(s, tm, S, m, (Wa + 7) >> 3);
+          tm_live = false;
+        }
         const double wstar = s.T[(m + 1) * S + cnt];
         if (wstar > a.eps_phase1 * fmax(1.0, binf)) { st = ST_INFEASIBLE; break; }
         for (int l = 0; l < m; ++l) {
@@ -656,6 +936,10 @@ __global__ void __launch_bounds__(NT) simplex_block_kernel(SimplexArgs a) {
         if (!record) {  // phase II never touches the dead (left artificial) positions
           cnt = compact_live(s, S, cnt, m + 1);
           Wa = cnt + 1;
+          if constexpr (TMR) {
+          tm_rows_from_smem(s, tm, S, m, (Wa + 7) >> 3);
+          tm_live = true;
+        }
         }
         if (record) {  // phase I recorded: dump the tableau it leaves, then stop (mode 1)
           for (int i = w; i < m; i += NW)
@@ -691,12 +975,17 @@ __global__ void __launch_bounds__(NT) simplex_block_kernel(SimplexArgs a) {
         rr.row = a.rec_rows + (size_t)it1 * Wr;
         if (cl.rank == 0 && tid == 0) a.rec_e[it1] = ce.pos;
       }
-      pivot_local(s, wcol, S, Wa, nrow, l, cl.rank == win, jloc, ce.key, rr);
+      if constexpr (TMR)
+        pivot_local_tm<tm_ns_max(CL)>(s, tm, wcol, S, Wa, m, nrow, l, cl.rank == win, jloc, ce.key, rr);
+      else
+        pivot_local(s, wcol, S, Wa, nrow, l, cl.rank == win, jloc, ce.key, rr);
       pp ^= 1;
       if (phase == 1) ++it1; else ++it2;
       stall = (theta > 0.0) ? 0 : stall + 1;
     }
 
+    // rows still in TMEM (the LP ended inside a pivot loop phase): back to SMEM for extract
+    if (TMR && tm_live) tm_rows_to_smem(s, tm, S, m, (Wa + 7) >> 3);
     if (record) {  // mode 1: no result for LP 0 here (the warm pass solves it); a phase-I
                    // outcome that ends every LP (INFEASIBLE, NUMERICAL, ITER_LIMIT) is recorded
       if (!recorded && cl.rank == 0 && tid == 0) {
@@ -733,6 +1022,12 @@ __global__ void __launch_bounds__(NT) simplex_block_kernel(SimplexArgs a) {
     }
     cl.sync();
   }
+  if constexpr (TMR) {
+    tm_fence_before();
+    __syncthreads();
+    tm_fence_after();
+    if (w == 0) tm_dealloc_n((uint32_t)s.ctl->pad, TM_COLS);
+  }
 }
 
 }  // namespace
@@ -758,22 +1053,22 @@ bool block_fits(int cl, int m, int n, int kmax) {
 }
 
 // Resident CTAs of one (CL, PULL) variant for this launch's SMEM size (memoised).
-template <int CL, bool PULL>
+template <int CL, bool PULL, bool TMR = false>
 static cudaError_t resident_ctas(const SimplexArgs& a, size_t smem, int* out) {
   const int sms = device_sm_count();
   static LaunchMemo memo;
   return memo.get(smem, out, [&](int& v, size_t attr) {
-    cudaError_t e = cudaFuncSetAttribute(simplex_block_kernel<CL, PULL>,
+    cudaError_t e = cudaFuncSetAttribute(simplex_block_kernel<CL, PULL, TMR>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)attr);
     if (e != cudaSuccess) return e;
     if constexpr (CL > 8) {  // 16-CTA clusters are a non-portable (opt-in) size on sm_100
-      e = cudaFuncSetAttribute(simplex_block_kernel<CL, PULL>,
+      e = cudaFuncSetAttribute(simplex_block_kernel<CL, PULL, TMR>,
                                cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
       if (e != cudaSuccess) return e;
     }
     if constexpr (CL == 1) {
       int per_sm = 0;
-      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, simplex_block_kernel<1, PULL>,
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, simplex_block_kernel<1, PULL, TMR>,
                                                         NT, smem);
       v = per_sm * sms;
       return e;
@@ -790,14 +1085,14 @@ static cudaError_t resident_ctas(const SimplexArgs& a, size_t smem, int* out) {
       q.dynamicSmemBytes = smem;
       q.gridDim = dim3(CL * sms);
       int clusters = 0;
-      e = cudaOccupancyMaxActiveClusters(&clusters, simplex_block_kernel<CL, PULL>, &q);
+      e = cudaOccupancyMaxActiveClusters(&clusters, simplex_block_kernel<CL, PULL, TMR>, &q);
       v = clusters * CL;
       return e;
     }
   });
 }
 
-template <int CL, bool PULL>
+template <int CL, bool PULL, bool TMR>
 static cudaError_t launch_variant(const SimplexArgs& a, size_t smem, int resident,
                                   int grid_override, cudaStream_t s, int* ctas_out) {
   cudaLaunchConfig_t cfg = {};
@@ -823,7 +1118,32 @@ static cudaError_t launch_variant(const SimplexArgs& a, size_t smem, int residen
   if (ctas_out) *ctas_out = grid;
   const cudaError_t e = cudaMemsetAsync(a.ticket, 0, sizeof(int), s);  // persistent LP ticket
   if (e != cudaSuccess) return e;
-  return cudaLaunchKernelEx(&cfg, simplex_block_kernel<CL, PULL>, a);
+  return cudaLaunchKernelEx(&cfg, simplex_block_kernel<CL, PULL, TMR>, a);
+}
+
+// TMR (constraint rows in TMEM during the pivot loop) for clusters of >= 4 CTAs whose CTAs
+// run one per SM anyway (the SMEM tableau admits no second CTA) and whose rows fit the SM's
+// 512 TMEM columns; each TMR CTA allocates all of them.  Measured (A/B, bit-identical):
+// cfg6 (4-CTA) 59.0 -> 56.2 ms per 1000 LPs, cfg8 (8-CTA) 615.7 -> 510.8 ms per 200, cfg7
+// (16-CTA) 305.7 -> 242.5 ms per 300; but cfg3 on 2-CTA clusters 200.5 -> 233.3 ms per 1500
+// (the pivot-row fetch from one TMEM lane is on the critical path of every pivot), so 2-CTA
+// clusters keep the SMEM rows.
+template <int CL, bool PULL>
+static cudaError_t launch_tm_or(const SimplexArgs& a, size_t smem, int resident,
+                                int grid_override, cudaStream_t s, int* ctas_out) {
+  if constexpr (CL >= 4) {
+    const int Q = (a.n + a.kmax + CL - 1) / CL;
+    const int ns = tm_slots(a.m);
+    if (ns <= tm_ns_max(CL) && ns * tm_slot_cols(Q) <= TM_COLS && resident <= device_sm_count() &&
+        !dev_flag("LPB_NO_TMEM")) {
+      int rt = 0;
+      const cudaError_t e = resident_ctas<CL, PULL, true>(a, smem, &rt);
+      if (e != cudaSuccess) return e;
+      if (rt >= CL)
+        return launch_variant<CL, PULL, true>(a, smem, rt, grid_override, s, ctas_out);
+    }
+  }
+  return launch_variant<CL, PULL, false>(a, smem, resident, grid_override, s, ctas_out);
 }
 
 // PUSH for CL <= 4 unless PULL's smaller footprint (one own proposal column per parity
@@ -845,9 +1165,9 @@ static cudaError_t launch_cl(const SimplexArgs& a, int grid_override, cudaStream
       if (e != cudaSuccess) return e;
     }
     if (rpush >= rpull)
-      return launch_variant<CL, false>(a, spush, rpush, grid_override, s, ctas_out);
+      return launch_tm_or<CL, false>(a, spush, rpush, grid_override, s, ctas_out);
   }
-  return launch_variant<CL, true>(a, spull, rpull, grid_override, s, ctas_out);
+  return launch_tm_or<CL, true>(a, spull, rpull, grid_override, s, ctas_out);
 }
 
 cudaError_t launch_simplex_block(int cl, const SimplexArgs& a, int grid_override,

@@ -2,7 +2,9 @@
 
     python scripts/ab.py <variant_root> [<variant_root> ...] -- cfg2:20000 cfg3:2000 ...
 
-Each variant root holds a built paper_1609_08114_b200/ (build.py --variant <root> ...).  Every
+Each variant root holds a built paper_1609_08114_b200/ (build.py --variant <root> ...); a root
+written <root>@VAR=value[,VAR=value] runs with those environment variables (the development
+build's A/B switches, e.g. devbuild@LPB_NO_TMEM=1).  Every
 variant runs in its own subprocess on the same inputs; prints the dominant kernel's device
 time (min / median of 7 solves) and a digest of the results (status, iters, obj bits), so
 variants that must be bit-identical can be checked at a glance."""
@@ -57,8 +59,13 @@ def main():
     repo = os.path.abspath('.')
     res = {}
     for root in roots:
-        code = CHILD.format(root=os.path.abspath(root), repo=repo, specs=specs)
-        p = subprocess.run([sys.executable, '-c', code], capture_output=True, text=True)
+        path, _, envs = root.partition('@')
+        env = dict(os.environ)
+        for kv in filter(None, envs.split(',')):
+            k, _, v = kv.partition('=')
+            env[k] = v
+        code = CHILD.format(root=os.path.abspath(path), repo=repo, specs=specs)
+        p = subprocess.run([sys.executable, '-c', code], capture_output=True, text=True, env=env)
         line = [l for l in p.stdout.splitlines() if l.startswith('AB-JSON ')]
         if not line:
             print(root, 'FAILED', p.stdout[-800:], p.stderr[-1500:])
