@@ -59,6 +59,42 @@ __device__ __forceinline__ void tm_st16(uint32_t addr, const uint32_t (&v)[16]) 
         "r"(v[14]), "r"(v[15])
       : "memory");
 }
+// 8 / 4 consecutive columns (4 / 2 doubles).
+__device__ __forceinline__ void tm_ld8(uint32_t addr, uint32_t* v) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
+                 "=r"(v[6]), "=r"(v[7])
+               : "r"(addr));
+}
+__device__ __forceinline__ void tm_st8(uint32_t addr, const uint32_t* v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};\n"
+               ::"r"(addr), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]),
+                 "r"(v[6]), "r"(v[7])
+               : "memory");
+}
+__device__ __forceinline__ void tm_ld4(uint32_t addr, uint32_t* v) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];\n"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
+               : "r"(addr));
+}
+__device__ __forceinline__ void tm_st4(uint32_t addr, const uint32_t* v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};\n"
+               ::"r"(addr), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3])
+               : "memory");
+}
+// 14 consecutive columns (7 doubles) as x8 + x4 + x2.
+__device__ __forceinline__ void tm_ld2(uint32_t addr, uint32_t& lo, uint32_t& hi);
+__device__ __forceinline__ void tm_st2(uint32_t addr, uint32_t lo, uint32_t hi);
+__device__ __forceinline__ void tm_ld14(uint32_t addr, uint32_t (&v)[14]) {
+  tm_ld8(addr, v);
+  tm_ld4(addr + 8, v + 8);
+  tm_ld2(addr + 12, v[12], v[13]);
+}
+__device__ __forceinline__ void tm_st14(uint32_t addr, const uint32_t (&v)[14]) {
+  tm_st8(addr, v);
+  tm_st4(addr + 8, v + 8);
+  tm_st2(addr + 12, v[12], v[13]);
+}
 // 2 consecutive columns (one double).
 __device__ __forceinline__ void tm_ld2(uint32_t addr, uint32_t& lo, uint32_t& hi) {
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];\n" : "=r"(lo), "=r"(hi) : "r"(addr));

@@ -113,7 +113,7 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
   constexpr int BH = (BC + 1) / 2;  // double2 pairs per SMEM row
   static_assert(NT % 32 == 0 && 32 % TC == 0 && TR <= 32 && AT <= 32 && BC <= 32, "layout");
   static_assert(RPW * AT <= 32, "the warp's rows must fit its lanes");
-  static_assert(!TM || (!TWO && (TR * TC == 128 || TR * TC == 64) && AS * 16 <= 128 && BC <= 8),
+  static_assert(!TM || (!TWO && (TR * TC == 128 || TR * TC == 64) && AS * 16 <= 128 && BC == 7),
                 "TMEM layout");
   constexpr int TMCOLS = AS * 16 <= 32 ? 32 : AS * 16 <= 64 ? 64 : 128;  // power of two
   __shared__ RegSmem<TR, TC, AT, BC> sm;
@@ -250,7 +250,7 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
       const int i = tr + TR * (A + s_);
       const bool rowok = (i < m) && st < 0;
       const bool neg = rowok && sm.bkey[i] < 0;
-      uint32_t cell[16];
+      uint32_t cell[TM ? 2 * BC : 1];
 #pragma unroll
       for (int b = 0; b < BC; ++b) {
         const int p = tc + TC * b;
@@ -267,9 +267,7 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
         else ts(s_, b) = v;
       }
       if constexpr (TM) {
-#pragma unroll
-        for (int k = 2 * BC; k < 16; ++k) cell[k] = 0u;
-        tm_st16(tbase + 16 * s_, cell);
+        tm_st14(tbase + 16 * s_, cell);
       }
     }
     if constexpr (TM) tm_wait_st();
@@ -629,8 +627,8 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
       if constexpr (TM) {
         if (al >= A) {  // pivot row in TMEM (warp-uniform): whole-warp load, owners publish
           const int s_ = al - A;
-          uint32_t cell[16];
-          tm_ld16(tbase + 16 * s_, cell);
+          uint32_t cell[14];
+          tm_ld14(tbase + 16 * s_, cell);
           tm_wait_ld();
           const bool own = tr == ltr;
 #pragma unroll
@@ -639,7 +637,7 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
             cell[2 * b] = own ? 0u : cell[2 * b];
             cell[2 * b + 1] = own ? 0u : cell[2 * b + 1];
           }
-          tm_st16(tbase + 16 * s_, cell);
+          tm_st14(tbase + 16 * s_, cell);
           tm_wait_st();
         }
       }
@@ -706,14 +704,17 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
 #pragma unroll
           for (int s_ = 0; s_ < AS; ++s_) {
             const double fi = sm.fcol[par][tr + TR * (A + s_)];
-            uint32_t cell[16];
-            tm_ld16(tbase + 16 * s_, cell);
+// the slot's 2 BC = 14 columns as x8 + x4 + x2 accesses: with x16 tuples ptxas loads
+            // each slot into a second tuple and copies it (16 moves per slot) and spills
+            // (316 bytes); measured: see DESIGN.md §9
+            uint32_t cell[14];
+            tm_ld14(tbase + 16 * s_, cell);
             tm_wait_ld();
 #pragma unroll
             for (int b = 0; b < BC; ++b)
               tm_split(__fma_rn(fi, pv[b], tm_d(cell[2 * b], cell[2 * b + 1])), cell[2 * b],
                        cell[2 * b + 1]);
-            tm_st16(tbase + 16 * s_, cell);
+            tm_st14(tbase + 16 * s_, cell);
           }
           tm_wait_st();
         }
