@@ -7,6 +7,8 @@ mkdir -p $OUT
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $OUT/gpu.txt
 timeout 1500 python -m pytest tests -m gpu -q > $OUT/pytest_gpu.txt 2>&1
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.txt 2>&1
+# the whole cfg3 batch against the oracle (~6 min of oracle time on the box's cores)
+LPB_SLOW=1 timeout 1500 python -m pytest tests/test_gpu_configs.py -k cfg3_full -s -q > $OUT/cfg3_full.txt 2>&1
 for cf in cfg2 cfg5; do  # with the n_chunks = 1 (no overlap) e2e control
   timeout 900 python bench.py --config $cf --e2e-chunks1 > $OUT/bench_$cf.json 2> $OUT/bench_$cf.err
 done
