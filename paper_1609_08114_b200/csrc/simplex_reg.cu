@@ -113,9 +113,13 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
   constexpr int BH = (BC + 1) / 2;  // double2 pairs per SMEM row
   static_assert(NT % 32 == 0 && 32 % TC == 0 && TR <= 32 && AT <= 32 && BC <= 32, "layout");
   static_assert(RPW * AT <= 32, "the warp's rows must fit its lanes");
-  static_assert(!TM || (!TWO && (TR * TC == 128 || TR * TC == 64) && AS * 16 <= 128 && BC == 7),
+  // TMEM row slot stride: 16 columns, or 14 (exactly BC = 7 doubles: column offsets need no
+  // alignment, scripts/ubench/tmem_align.cu) when 16-column slots would not fit 128 columns
+  // (4 register + 9 TMEM rows for cfg2's sizes: measured 6 % slower than layout 15)
+  constexpr int SLOT = AS * 16 <= 128 ? 16 : 14;
+  static_assert(!TM || (!TWO && (TR * TC == 128 || TR * TC == 64) && AS * SLOT <= 128 && BC == 7),
                 "TMEM layout");
-  constexpr int TMCOLS = AS * 16 <= 32 ? 32 : AS * 16 <= 64 ? 64 : 128;  // power of two
+  constexpr int TMCOLS = AS * SLOT <= 32 ? 32 : AS * SLOT <= 64 ? 64 : 128;  // power of two
   __shared__ RegSmem<TR, TC, AT, BC> sm;
   // TM layouts (128 registers): threadIdx.x through a volatile asm, so that the compiler
   // cannot re-read it (S2R, ~20 cycles) at every use under register pressure; the derived
@@ -267,7 +271,7 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
         else ts(s_, b) = v;
       }
       if constexpr (TM) {
-        tm_st14(tbase + 16 * s_, cell);
+        tm_st14(tbase + SLOT * s_, cell);
       }
     }
     if constexpr (TM) tm_wait_st();
@@ -512,13 +516,13 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
       if constexpr (TM) {  // TMEM rows: the whole warp loads column be, the owners publish it
         uint32_t lo[AS > 0 ? AS : 1], hi[AS > 0 ? AS : 1];
 #pragma unroll
-        for (int s_ = 0; s_ < AS; ++s_) tm_ld2(tbase + 16 * s_ + 2 * be, lo[s_], hi[s_]);
+        for (int s_ = 0; s_ < AS; ++s_) tm_ld2(tbase + SLOT * s_ + 2 * be, lo[s_], hi[s_]);
         tm_wait_ld();
         const bool own = tc == etc;
 #pragma unroll
         for (int s_ = 0; s_ < AS; ++s_) {
           if (own) colE[tr + TR * (A + s_)] = tm_d(lo[s_], hi[s_]);
-          tm_st2(tbase + 16 * s_ + 2 * be, own ? 0u : lo[s_], own ? 0u : hi[s_]);
+          tm_st2(tbase + SLOT * s_ + 2 * be, own ? 0u : lo[s_], own ? 0u : hi[s_]);
         }
         tm_wait_st();  // the pivot-row load below may read these columns
       }
@@ -628,7 +632,7 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
         if (al >= A) {  // pivot row in TMEM (warp-uniform): whole-warp load, owners publish
           const int s_ = al - A;
           uint32_t cell[14];
-          tm_ld14(tbase + 16 * s_, cell);
+          tm_ld14(tbase + SLOT * s_, cell);
           tm_wait_ld();
           const bool own = tr == ltr;
 #pragma unroll
@@ -637,7 +641,7 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
             cell[2 * b] = own ? 0u : cell[2 * b];
             cell[2 * b + 1] = own ? 0u : cell[2 * b + 1];
           }
-          tm_st14(tbase + 16 * s_, cell);
+          tm_st14(tbase + SLOT * s_, cell);
           tm_wait_st();
         }
       }
@@ -701,20 +705,21 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
           for (int b = 0; b < BC; ++b) T[ai][b] = __fma_rn(fi, pv[b], T[ai][b]);
         }
         if constexpr (TM) {  // TMEM rows: load, fma, store one slot at a time
+          // each slot's 2 BC = 14 columns as x8 + x4 + x2 accesses: with x16 tuples ptxas loads
+          // each slot into a second tuple and copies it (16 moves per slot) and spills (316
+          // bytes).  Measured slower: the next slot's load issued before this
+          // slot's fmas (2 or 3 rotating buffers: +12 %, spills), 4 + 9 rows in 14-column slots
 #pragma unroll
           for (int s_ = 0; s_ < AS; ++s_) {
             const double fi = sm.fcol[par][tr + TR * (A + s_)];
-// the slot's 2 BC = 14 columns as x8 + x4 + x2 accesses: with x16 tuples ptxas loads
-            // each slot into a second tuple and copies it (16 moves per slot) and spills
-            // (316 bytes); measured: see DESIGN.md §9
             uint32_t cell[14];
-            tm_ld14(tbase + 16 * s_, cell);
+            tm_ld14(tbase + SLOT * s_, cell);
             tm_wait_ld();
 #pragma unroll
             for (int b = 0; b < BC; ++b)
               tm_split(__fma_rn(fi, pv[b], tm_d(cell[2 * b], cell[2 * b + 1])), cell[2 * b],
                        cell[2 * b + 1]);
-            tm_st14(tbase + 16 * s_, cell);
+            tm_st14(tbase + SLOT * s_, cell);
           }
           tm_wait_st();
         }
