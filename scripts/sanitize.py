@@ -1,5 +1,6 @@
-"""Small batches through every kernel (size classes S, W, R, M, L on 2/4/8/16-CTA
-clusters, the phase-I warm start, hyperbox TMA-ring and plain kernels), for
+"""Small batches through every kernel (size classes S, W, R (incl. the TMEM layouts), M, L on
+2/4/8/16-CTA clusters (incl. the TMR variants), the phase-I warm start, hyperbox TMA-ring and
+plain kernels), for
 compute-sanitizer (memcheck / racecheck / synccheck / initcheck):
     compute-sanitizer --tool racecheck python scripts/sanitize.py"""
 import sys
@@ -46,6 +47,12 @@ print("R 100x100", li, np.bincount(st, minlength=5))
 A, b, c = lpgen.signed_bounded(8, 20, 20, 5)
 st, li = run(A, b, c, pivot_rule="RPC", rpc_seed=3)
 print("RPC", li, np.bincount(st, minlength=5))
+# tensor-memory paths: R layouts 15 (cfg2 sizes) and 17 (cfg10), L-class TMR variants on
+# 4-, 8- (two-phase: phase-switch copies) and 16-CTA clusters
+for name, B in (("cfg2", 4), ("cfg10", 8), ("cfg6", 3), ("cfg8", 2), ("cfg7", 1)):
+    A, b, c = lpgen.make_config(name, B)
+    st, li = run(A, b, c)
+    print("TMEM", name, li, np.bincount(st, minlength=5))
 lo, hi, dirs = lpgen.hyperbox(256 * 8 * 3 + 17, 5, 6)
 h = lpb.hyperbox(lo, hi, torch.from_numpy(dirs).cuda())
 print("H tma", h["status"].sum().item())
