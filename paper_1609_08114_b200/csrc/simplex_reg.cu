@@ -316,6 +316,11 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
       const int t = direct ? (int)a.batch : atomicAdd(a.ticket, 1);
       sm.lp = t;
       if (pf && t < a.batch) bulk_load(abuf, a.A + (int64_t)t * a.sA, abytes, &sm.mbar);
+      // layouts without the SMEM prefetch buffer (TMEM / SMEM rows): the next LP's A is
+      // bulk-prefetched into L2 instead, so its build reads hit L2 rather than HBM (ncu
+      // r02f: 19 % of cfg2's stall samples were the build's A loads; cfg2 -3.4 %, cfg10 -6.8 %)
+      if (AS > 0 && a.prefetch && t < a.batch)
+        bulk_prefetch_l2(a.A + (int64_t)t * a.sA, abytes);
     }
 
     // ---- Steps 1-3, two phases ----
