@@ -229,44 +229,65 @@ __global__ void __launch_bounds__(TR * TC, MINB) simplex_reg_kernel(SimplexArgs 
       sm.nbvar[p] = (p < n) ? p : (p < npos ? n + sm.negrows[p - n] : DEADV);
     for (int i = m + tid; i < RCAP; i += NT) sm.rhs[i] = 0.0;
 
+    // a tableau element of the build: row i (negated when b_i < 0), position p (R7)
+    auto elem = [&](int i, bool rowok, bool neg, int p) -> double {
+      double v = 0.0;
+      if (rowok && p < npos) {
+        if (p < n) {
+          v = Ak[i * n + p];
+          v = neg ? -v : v;
+        } else {
+          v = (i == sm.negrows[p - n]) ? -1.0 : (neg ? -0.0 : 0.0);
+        }
+      }
+      return v;
+    };
+    if constexpr (TM) {
+      // TMEM rows first, while the register rows are not live yet: the loads of G row slots
+      // are in flight together (one slot at a time exposed an L2 round trip per slot; cfg2
+      // -0.7 %, G = 8 spills)
+      constexpr int G = 4;
+#pragma unroll
+      for (int s0 = 0; s0 < AS; s0 += G) {
+        double vv[G][BC];
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          if (s0 + g < AS) {
+            const int i = tr + TR * (A + s0 + g);
+            const bool rowok = (i < m) && st < 0;
+            const bool neg = rowok && sm.bkey[i] < 0;
+#pragma unroll
+            for (int b = 0; b < BC; ++b) vv[g][b] = elem(i, rowok, neg, tc + TC * b);
+          }
+        }
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          if (s0 + g < AS) {
+            uint32_t cell[2 * BC];
+#pragma unroll
+            for (int b = 0; b < BC; ++b) tm_split(vv[g][b], cell[2 * b], cell[2 * b + 1]);
+            tm_st14(tbase + SLOT * (s0 + g), cell);
+          }
+        }
+      }
+    }
 #pragma unroll
     for (int ai = 0; ai < A; ++ai) {
       const int i = tr + TR * ai;
       const bool rowok = (i < m) && st < 0;
       const bool neg = rowok && sm.bkey[i] < 0;
 #pragma unroll
-      for (int b = 0; b < BC; ++b) {
-        const int p = tc + TC * b;
-        double v = 0.0;
-        if (rowok && p < npos) {
-          if (p < n) {
-            v = Ak[i * n + p];
-            v = neg ? -v : v;
-          } else {
-            v = (i == sm.negrows[p - n]) ? -1.0 : (neg ? -0.0 : 0.0);
-          }
-        }
-        T[ai][b] = v;
-      }
+      for (int b = 0; b < BC; ++b) T[ai][b] = elem(i, rowok, neg, tc + TC * b);
     }
 #pragma unroll
-    for (int s_ = 0; s_ < AS; ++s_) {
+    for (int s_ = 0; s_ < (TM ? 0 : AS); ++s_) {  // SMEM rows (non-TM layouts with AS > 0)
       const int i = tr + TR * (A + s_);
       const bool rowok = (i < m) && st < 0;
       const bool neg = rowok && sm.bkey[i] < 0;
       uint32_t cell[TM ? 2 * BC : 1];
 #pragma unroll
       for (int b = 0; b < BC; ++b) {
-        const int p = tc + TC * b;
-        double v = 0.0;
-        if (rowok && p < npos) {
-          if (p < n) {
-            v = Ak[i * n + p];
-            v = neg ? -v : v;
-          } else {
-            v = (i == sm.negrows[p - n]) ? -1.0 : (neg ? -0.0 : 0.0);
-          }
-        }
+        const double v = elem(i, rowok, neg, tc + TC * b);
         if constexpr (TM) tm_split(v, cell[2 * b], cell[2 * b + 1]);
         else ts(s_, b) = v;
       }
