@@ -61,6 +61,9 @@ struct lpb_ctx {
   int* d_kmax = nullptr;
   int* d_defer = nullptr;      // S class register kernel: deferred (two-phase) LPs, [batch]
   int* d_defer_cnt = nullptr;  // one counter per chunk
+  // L class hybrid TMR layout: per-chunk global scratch for rows 0..127 (allocated on use)
+  double* d_tmscr[64] = {};
+  size_t tmscr_n[64] = {};
   int* h_kmax = nullptr;    // pinned
   std::vector<cudaStream_t> chunk_streams;
   std::vector<cudaEvent_t> chunk_done;
@@ -234,6 +237,7 @@ extern "C" int lpb_destroy(lpb_ctx* c) {
   cudaFree(c->d_kmax);
   cudaFree(c->d_defer);
   cudaFree(c->d_defer_cnt);
+  for (double* p : c->d_tmscr) cudaFree(p);
   cudaFree(c->rec_rows);
   cudaFree(c->rec_T);
   cudaFree(c->rec_ints);
@@ -308,6 +312,8 @@ static void fill_args(const lpb_ctx* c, SimplexArgs& a, int64_t lp0, int64_t cnt
   a.lp_base = c->opt.lp_index_base + lp0;
   a.defer_list = nullptr;
   a.defer_cnt = nullptr;
+  a.tm_hyb = 0;
+  a.tm_scr = nullptr;
   // bulk-copy prefetch needs every LP's A to start 16-byte aligned and be a multiple of 16
   // bytes (m*n even), and to fit SMEM next to the register layouts' small SMEM state
   const int64_t bytes = (int64_t)m * n * 8;
@@ -392,6 +398,20 @@ static int run_general(lpb_ctx* c, cudaStream_t s, int64_t lp0, int64_t cnt, con
   } else if (klass == CLASS_R) {
     LPB_CUDA(c, launch_simplex_reg(a, c->opt.grid_ctas, s, &ctas));
   } else {
+    if (klass == CLASS_L && cl == 2) {  // hybrid TMR layout: the chunk's row-0..127 scratch
+      const size_t need = block_hyb_scratch_doubles(c->m, c->n, kmax);
+      const int slot = (int)(ticket - c->d_ticket);
+      if (need > 0 && slot >= 0 && slot < 64) {
+        if (c->tmscr_n[slot] < need) {
+          cudaFree(c->d_tmscr[slot]);
+          c->d_tmscr[slot] = nullptr;
+          c->tmscr_n[slot] = 0;
+          LPB_CUDA(c, cudaMalloc(&c->d_tmscr[slot], sizeof(double) * need));
+          c->tmscr_n[slot] = need;
+        }
+        a.tm_scr = c->d_tmscr[slot];
+      }
+    }
     // Shared constraints with an infeasible slack basis (LPB_SHARED_AB, k > 0): phase I
     // depends on A and b only, so it is solved once (mode 1, LP 0) and every LP starts at
     // phase II from that record (mode 2).  Under RPC the phase-I path

@@ -60,6 +60,11 @@ struct SimplexArgs {
   // (list mode when defer_cnt != nullptr).
   int* defer_list;     // [batch] launch-relative LP indices
   int* defer_cnt;      // number of entries, zeroed before the register kernel
+  // L class, hybrid TMR layout (2-CTA clusters at 2 CTAs per SM): constraint rows 0..127 in
+  // TMEM during the pivot loop, their storage of record in tm_scr (per CTA: 128 x S doubles,
+  // CTA b at tm_scr + b * 128 * S) instead of SMEM
+  int tm_hyb;
+  double* tm_scr;
 };
 
 struct HyperboxArgs {
@@ -76,6 +81,7 @@ struct HyperboxArgs {
 // ---- M / L classes: one LP per CTA (cl = 1) or per cl-CTA cluster, tableau in SMEM ----
 size_t block_smem_bytes(int cl, int m, int n, int kmax);
 bool block_fits(int cl, int m, int n, int kmax);
+size_t block_hyb_scratch_doubles(int m, int n, int kmax);  // 0: no hybrid TMR layout
 cudaError_t launch_simplex_block(int cl, const SimplexArgs& a, int grid_override,
                                  cudaStream_t s, int* ctas_out);
 

@@ -102,10 +102,19 @@ struct Ctl {
 __host__ __device__ __forceinline__ int row_stride(int Q) { return 2 * (((Q + 2) >> 1) | 1); }
 
 struct Smem {
+  // Tableau row i: SMEM row i - h0 for i >= h0; rows below h0 (hybrid TMR variants only) keep
+  // their storage of record in a per-CTA global (L2-resident) scratch gT (the pivot loop holds
+  // them in TMEM)
+  __device__ __forceinline__ double* row(int i) const {
+    return i < h0 ? gT + (size_t)i * S : T + (size_t)(i - h0) * S;
+  }
+  int h0 = 0, S = 0;
+  double* gT = nullptr;
   double* T;      // rows x S
   double* colE;   // pivot column (all rows), filled by the owner CTA
   double* fcol;   // update multipliers: -colE_i, +1 for the pivot row
   double* prow;   // new pivot row (local columns)
+  double* lraw;   // TMR: raw pivot row fetched from TMEM (S doubles)
   int* nbvar;     // local position -> variable index (or DEAD)
   int* bkey;      // row -> key of its basic variable (>= 0 real, < 0 artificial)
   int* negrows;   // ascending list of rows with b_i < 0
@@ -209,7 +218,7 @@ __device__ __forceinline__ void pivot_local(const Smem& s, const double* colE, i
   const double rpe = recip_of(pe);
   for (int j = tid; j < Wa; j += NT) {
     const bool sw = own && j == jloc;
-    double* tl = s.T + l * S + j;
+    double* tl = s.row(l) + j;
     const double num = sw ? 1.0 : *tl;
     bool slow;
     double q = div_with(num, pe, rpe, slow);
@@ -223,7 +232,7 @@ __device__ __forceinline__ void pivot_local(const Smem& s, const double* colE, i
   }
   for (int i = tid; i < nrow; i += NT) {
     s.fcol[i] = (i == l) ? 1.0 : -colE[i];
-    if (own) s.T[i * S + jloc] = 0.0;
+    if (own) s.row(i)[jloc] = 0.0;
   }
   if (tid == 0) {
     const int leaving = s.bkey[l];
@@ -242,11 +251,10 @@ __device__ __forceinline__ void pivot_local(const Smem& s, const double* colE, i
     const int j = lane + 32 * c;
     pr[c] = (j < Wa2) ? prow2[j] : make_double2(0.0, 0.0);
   }
-  double2* T2 = reinterpret_cast<double2*>(s.T);
   if (Wa2 <= 64) {  // the common case: two chunks
     for (int i = w; i < nrow; i += NW) {
       const double f = s.fcol[i];
-      double2* row = T2 + i * S2 + lane;
+      double2* row = reinterpret_cast<double2*>(s.row(i)) + lane;
       if (lane < Wa2) {
         double2 v0 = row[0];
         v0.x = __fma_rn(f, pr[0].x, v0.x);
@@ -263,7 +271,7 @@ __device__ __forceinline__ void pivot_local(const Smem& s, const double* colE, i
   } else {
     for (int i = w; i < nrow; i += NW) {
       const double f = s.fcol[i];
-      double2* row = T2 + i * S2 + lane;
+      double2* row = reinterpret_cast<double2*>(s.row(i)) + lane;
 #pragma unroll
       for (int c = 0; c < MAXC; ++c) {
         if (lane + 32 * c < Wa2) {
@@ -317,12 +325,12 @@ __device__ __forceinline__ int compact_live(const Smem& s, int S, int cnt, int n
     for (int c = 0; c < CH; ++c) {
       const int jj = lane + 32 * c;
       dst[c] = jj <= cnt ? map[jj] : -1;
-      v[c] = dst[c] >= 0 ? s.T[i * S + jj] : 0.0;
+      v[c] = dst[c] >= 0 ? s.row(i)[jj] : 0.0;
     }
     __syncwarp();
 #pragma unroll
     for (int c = 0; c < CH; ++c)
-      if (dst[c] >= 0) s.T[i * S + dst[c]] = v[c];
+      if (dst[c] >= 0) s.row(i)[dst[c]] = v[c];
     __syncwarp();
   }
   __syncthreads();
@@ -352,6 +360,7 @@ struct TmRows {
   uint32_t tb;  // TMEM address of this warp's lane quarter, column 0
   int ns, sc;   // row slots in use, columns per slot (16 per 8-position chunk)
   int q, h;     // lane quarter (w % 4), half (w / 4)
+  int mt;       // rows [0, mt) live in TMEM (m, or 128 in the hybrid layout); the rest in SMEM
 };
 
 __host__ __device__ __forceinline__ int tm_slot_cols(int Q) { return 16 * ((Q + 1 + 7) / 8); }
@@ -367,13 +376,13 @@ __device__ __forceinline__ void tm_sync() {
 }
 
 // SMEM rows [0, m) -> TMEM (nch chunks of 8 positions); ends with tm_sync().
-__device__ __forceinline__ void tm_rows_from_smem(const Smem& s, const TmRows& t, int S, int m,
+__device__ __forceinline__ void tm_rows_from_smem(const Smem& s, const TmRows& t, int S, int,
                                                   int nch) {
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, m = t.mt;
   for (int sl = 0; sl < t.ns; ++sl) {
     if (128 * sl + 32 * t.q >= m) break;  // warp-uniform: no row of this warp
     const int r = 128 * sl + 32 * t.q + lane;
-    const double* row = s.T + (size_t)(r < m ? r : 0) * S;
+    const double* row = s.row(r < m ? r : 0);
     for (int c = t.h; c < nch; c += 2) {
       uint32_t v[16];
 #pragma unroll
@@ -388,13 +397,13 @@ __device__ __forceinline__ void tm_rows_from_smem(const Smem& s, const TmRows& t
 }
 
 // TMEM rows [0, m) -> SMEM; ends with a barrier.
-__device__ __forceinline__ void tm_rows_to_smem(const Smem& s, const TmRows& t, int S, int m,
+__device__ __forceinline__ void tm_rows_to_smem(const Smem& s, const TmRows& t, int S, int,
                                                 int nch) {
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, m = t.mt;
   for (int sl = 0; sl < t.ns; ++sl) {
     if (128 * sl + 32 * t.q >= m) break;
     const int r = 128 * sl + 32 * t.q + lane;
-    double* row = s.T + (size_t)(r < m ? r : 0) * S;
+    double* row = s.row(r < m ? r : 0);
     for (int c = t.h; c < nch; c += 2) {
       uint32_t v[16];
       tm_ld16(t.tb + sl * t.sc + 16 * c, v);
@@ -419,13 +428,15 @@ __device__ __forceinline__ void tm_rows_to_smem(const Smem& s, const TmRows& t, 
 // jloc is zeroed in TMEM (owner CTA), and the update runs chunk by chunk over the TMEM rows
 // (the 8 pivot-row quotients of a chunk are SMEM broadcasts) and row by row over the SMEM
 // objective rows [m, nrow).
-template <int NSX>
+template <int NSX, bool HYB>
 __device__ __forceinline__ void pivot_local_tm(const Smem& s, const TmRows& t, const double* colE,
                                                int S, int Wa, int m, int nrow, int l, bool own,
                                                int jloc, int ent_var, const RecRow& rec) {
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int nch = (Wa + 7) >> 3;
-  if (t.q == ((l >> 5) & 3)) {  // the pivot row's lane quarter (warp-uniform)
+  const int mt = HYB ? t.mt : m;
+  const bool ltm = !HYB || l < mt;  // row l in TMEM (else an SMEM row of the hybrid layout)
+  if (ltm && t.q == ((l >> 5) & 3)) {  // the pivot row's lane quarter (warp-uniform)
     const int sl = l >> 7;
     const bool ol = lane == (l & 31);
     constexpr int FB = 1;  // chunks in flight per wait (measured: 4 is no faster)
@@ -444,7 +455,7 @@ __device__ __forceinline__ void pivot_local_tm(const Smem& s, const TmRows& t, c
             for (int k = 0; k < 4; ++k) {
               const int j = 8 * c + 2 * k;
               if (j < S)
-                *reinterpret_cast<double2*>(s.T + l * S + j) =
+                *reinterpret_cast<double2*>(s.lraw + j) =
                     make_double2(tm_d(v[u][4 * k], v[u][4 * k + 1]),
                                  tm_d(v[u][4 * k + 2], v[u][4 * k + 3]));
             }
@@ -458,13 +469,15 @@ __device__ __forceinline__ void pivot_local_tm(const Smem& s, const TmRows& t, c
   }
   if (own && t.h == ((jloc >> 3) & 1))  // the swapped column starts from 0 (as pivot_local)
     for (int sl = 0; sl < t.ns; ++sl)
-      if (128 * sl + 32 * t.q < m) tm_st2(t.tb + sl * t.sc + 2 * jloc, 0u, 0u);
+      if (128 * sl + 32 * t.q < mt) tm_st2(t.tb + sl * t.sc + 2 * jloc, 0u, 0u);
   tm_sync();
+  double* const lrow = ltm ? s.lraw : s.row(l);
   const double pe = colE[l];
   const double rpe = recip_of(pe);
   for (int j = tid; j < Wa; j += NT) {
     const bool sw = own && j == jloc;
-    const double num = sw ? 1.0 : s.T[l * S + j];
+    const double num = sw ? 1.0 : lrow[j];
+    if (!ltm) lrow[j] = 0.0;  // an SMEM row l starts from 0 (fcol_l = 1), as in pivot_local
     bool slow;
     double q = div_with(num, pe, rpe, slow);
     if (slow) q = ddiv_slow(num, pe);
@@ -476,7 +489,7 @@ __device__ __forceinline__ void pivot_local_tm(const Smem& s, const TmRows& t, c
   }
   for (int i = tid; i < nrow; i += NT) {
     s.fcol[i] = (i == l) ? 1.0 : -colE[i];
-    if (own && i >= m) s.T[i * S + jloc] = 0.0;
+    if (own && i >= mt) s.row(i)[jloc] = 0.0;
   }
   if (tid == 0) {
     const int leaving = s.bkey[l];
@@ -487,17 +500,17 @@ __device__ __forceinline__ void pivot_local_tm(const Smem& s, const TmRows& t, c
   __syncthreads();
   // objective rows (SMEM): lanes walk 128-bit column pairs
   {
-    const int Wa2 = (Wa + 1) >> 1, S2 = S >> 1;
+    const int Wa2 = (Wa + 1) >> 1;
     const double2* prow2 = reinterpret_cast<const double2*>(s.prow);
-    double2* T2 = reinterpret_cast<double2*>(s.T);
-    for (int i = m + w; i < nrow; i += NW) {
+    for (int i = mt + w; i < nrow; i += NW) {  // SMEM rows: the objective rows (+ hybrid rows)
       const double f = s.fcol[i];
+      double2* T2 = reinterpret_cast<double2*>(s.row(i));
       for (int j = lane; j < Wa2; j += 32) {
         const double2 p = prow2[j];
-        double2 v = T2[i * S2 + j];
+        double2 v = T2[j];
         v.x = __fma_rn(f, p.x, v.x);
         v.y = __fma_rn(f, p.y, v.y);
-        T2[i * S2 + j] = v;
+        T2[j] = v;
       }
     }
   }
@@ -509,7 +522,7 @@ __device__ __forceinline__ void pivot_local_tm(const Smem& s, const TmRows& t, c
 #pragma unroll
   for (int sl = 0; sl < NSX; ++sl) {
     const int r = 128 * sl + 32 * t.q + lane;
-    f[sl] = (sl < t.ns && r < m) ? s.fcol[r] : 0.0;
+    f[sl] = (sl < t.ns && r < mt) ? s.fcol[r] : 0.0;
   }
   const double2* prow2 = reinterpret_cast<const double2*>(s.prow);
   for (int c = t.h; c < nch; c += 2) {
@@ -518,7 +531,7 @@ __device__ __forceinline__ void pivot_local_tm(const Smem& s, const TmRows& t, c
     for (int k = 0; k < 4; ++k) p[k] = prow2[4 * c + k];
 #pragma unroll
     for (int sl = 0; sl < NSX; ++sl) {
-      if (sl < t.ns && 128 * sl + 32 * t.q < m) {  // warp-uniform
+      if (sl < t.ns && 128 * sl + 32 * t.q < mt) {  // warp-uniform
         uint32_t v[16];
         const uint32_t ad = t.tb + sl * t.sc + 16 * c;
         tm_ld16(ad, v);
@@ -539,7 +552,7 @@ __device__ __forceinline__ void pivot_local_tm(const Smem& s, const TmRows& t, c
 // PULL (proposal columns read over DSMEM after the barrier) is used for CL >= 8, and for
 // CL = 2/4 whenever its smaller SMEM footprint fits more CTAs per SM than PUSH (launch_cl).
 template <int CL, bool PULL, bool TMR>
-__global__ void __launch_bounds__(NT) simplex_block_kernel(SimplexArgs a) {
+__device__ __forceinline__ void simplex_block_body(const SimplexArgs& a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const Cluster<CL> cl;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
@@ -548,12 +561,19 @@ __global__ void __launch_bounds__(NT) simplex_block_kernel(SimplexArgs a) {
   const int S = row_stride(Q);  // even (128-bit rows), S/2 odd (spread column reads)
   const int RC = m + 2;
 
+  // hybrid TMR layout: rows 0..127 live in TMEM during the pivot loop and in the CTA's global
+  // scratch otherwise; SMEM holds rows 128.. only
+  const bool hyb = TMR && CL == 2 && a.tm_hyb != 0;
   Smem s;
+  s.S = S;
+  s.h0 = hyb ? 128 : 0;
+  s.gT = hyb ? a.tm_scr + (size_t)blockIdx.x * 128 * S : nullptr;
   s.T = reinterpret_cast<double*>(smem_raw);
-  s.colE = s.T + (size_t)RC * S;
+  s.colE = s.T + (size_t)(RC - s.h0) * S;
   s.fcol = s.colE + RC;
   s.prow = s.fcol + RC;
-  s.nbvar = reinterpret_cast<int*>(s.prow + S);
+  s.lraw = s.prow + S;
+  s.nbvar = reinterpret_cast<int*>(s.lraw + S);
   s.bkey = s.nbvar + (Q + 1);
   // negrows is needed only while the LP is built, before colE is first written: alias
   s.negrows = reinterpret_cast<int*>(s.colE);
@@ -580,9 +600,10 @@ __global__ void __launch_bounds__(NT) simplex_block_kernel(SimplexArgs a) {
   // DSMEM may only be touched once every CTA of the cluster is running: one
   // cluster barrier before the first remote ticket write (racecheck finding); it also
   // publishes the initialised mbarriers.
-  TmRows tm{0u, tm_slots(m), tm_slot_cols(Q), w & 3, w >> 2};
+  TmRows tm{0u, hyb ? 1 : tm_slots(m), tm_slot_cols(Q), w & 3, w >> 2, hyb ? (m < 128 ? m : 128) : m};
+  const uint32_t tmcols = hyb ? TM_COLS / 2 : TM_COLS;  // hybrid: two CTAs share the SM's TMEM
   if constexpr (TMR) {
-    if (w == 0) tm_alloc_n(reinterpret_cast<uint32_t*>(&s.ctl->pad), TM_COLS);
+    if (w == 0) tm_alloc_n(reinterpret_cast<uint32_t*>(&s.ctl->pad), tmcols);
     tm_fence_before();
   }
   if constexpr (CL > 1) cl.sync();
@@ -664,7 +685,7 @@ __global__ void __launch_bounds__(NT) simplex_block_kernel(SimplexArgs a) {
         phase = 2;
         for (int i = w; i < m; i += NW)
           for (int j = lane; j < Wp; j += 32)
-            s.T[i * S + j] = (j < cnt) ? a.rec_T[(size_t)i * Wr + g0 + j]
+            s.row(i)[j] = (j < cnt) ? a.rec_T[(size_t)i * Wr + g0 + j]
                                        : (j == cnt ? a.rec_T[(size_t)i * Wr + npos] : 0.0);
         for (int j = tid; j < cnt; j += NT) s.nbvar[j] = a.rec_nbvar[g0 + j];
         for (int i = tid; i < m; i += NT) s.bkey[i] = a.rec_bkey[i];
@@ -683,7 +704,7 @@ __global__ void __launch_bounds__(NT) simplex_block_kernel(SimplexArgs a) {
           __syncthreads();
         }
         for (int j = tid; j < Wp; j += NT)
-          s.T[m * S + j] = (j < cnt) ? cur[g0 + j] : (j == cnt ? cur[npos] : 0.0);
+          s.row(m)[j] = (j < cnt) ? cur[g0 + j] : (j == cnt ? cur[npos] : 0.0);
         __syncthreads();
         cnt = compact_live(s, S, cnt, m + 1);  // phase II from here on: drop dead positions
         Wa = cnt + 1;
@@ -709,20 +730,20 @@ __global__ void __launch_bounds__(NT) simplex_block_kernel(SimplexArgs a) {
           } else {
             v = (i == s.negrows[gp - n]) ? -1.0 : (neg ? -0.0 : 0.0);
           }
-          s.T[i * S + j] = v;
+          s.row(i)[j] = v;
         }
       }
       for (int j = tid; j < Wp; j += NT) {
         const int gp = g0 + j;
-        s.T[m * S + j] = (j < cnt && gp < n) ? __ldg(ck + gp) : 0.0;
+        s.row(m)[j] = (j < cnt && gp < n) ? __ldg(ck + gp) : 0.0;
         if (j < cnt) s.nbvar[j] = gp < n ? gp : n + s.negrows[gp - n];
       }
       __syncthreads();
       if (k > 0) {  // phase-I row: ascending-row sums of the negated rows (R7)
         for (int j = tid; j < Wp; j += NT) {
           double acc = 0.0;
-          for (int t = 0; t < k; ++t) acc = __dadd_rn(acc, s.T[s.negrows[t] * S + j]);
-          s.T[(m + 1) * S + j] = acc;
+          for (int t = 0; t < k; ++t) acc = __dadd_rn(acc, s.row(s.negrows[t])[j]);
+          s.row(m + 1)[j] = acc;
         }
       }
       __syncthreads();
@@ -750,7 +771,7 @@ __global__ void __launch_bounds__(NT) simplex_block_kernel(SimplexArgs a) {
       const uint64_t pkey = rpc ? rpc_pivot_key(lpkey, it1 + it2) : 0ull;
       for (int j = tid; j < cnt; j += NT) {
         const int var = s.nbvar[j];
-        const double d = s.T[objrow * S + j];
+        const double d = s.row(objrow)[j];
         if (var != DEAD && d > a.eps_enter) {
           const Cand cd{rpc ? (double)rpc_score(pkey, var) : d, var, g0 + j};
           if (bland ? better<MIN_KEY>(cd, ce) : better<MAX_V>(cd, ce)) ce = cd;
@@ -765,7 +786,7 @@ __global__ void __launch_bounds__(NT) simplex_block_kernel(SimplexArgs a) {
 #pragma unroll
         for (int sl = 0; sl < TM_NS; ++sl) {
           cv[sl] = 0.0;
-          if (sl < tm.ns && (sl & 1) == tm.h && 128 * sl + 32 * tm.q < m) {  // warp-uniform
+          if (sl < tm.ns && (sl & 1) == tm.h && 128 * sl + 32 * tm.q < tm.mt) {  // warp-uniform
             uint32_t a0, a1, b0, b1;
             tm_ld2(tm.tb + sl * tm.sc + 2 * jcs, a0, a1);
             tm_ld2(tm.tb + sl * tm.sc + 2 * cnt, b0, b1);
@@ -773,7 +794,7 @@ __global__ void __launch_bounds__(NT) simplex_block_kernel(SimplexArgs a) {
             const int i = 128 * sl + 32 * tm.q + lane;
             const double ai = tm_d(a0, a1);
             cv[sl] = ai;
-            if (ce.pos >= 0 && i < m && ai > a.eps_piv) {
+            if (ce.pos >= 0 && i < tm.mt && ai > a.eps_piv) {
               const double ri = tm_d(b0, b1);
               bool slow;
               double r = div_fast(ri, ai, slow);
@@ -784,13 +805,14 @@ __global__ void __launch_bounds__(NT) simplex_block_kernel(SimplexArgs a) {
           }
         }
         tm_fence_before();  // these loads precede the update's stores (after the barriers)
-      } else if (ce.pos >= 0) {
-        for (int i = tid; i < m; i += NT) {
-          const double ai = s.T[i * S + jc];
+      }
+      if (ce.pos >= 0) {  // SMEM constraint rows (all of them, or the hybrid's rows 128..)
+        for (int i = (TMR ? tm.mt : 0) + tid; i < m; i += NT) {
+          const double ai = s.row(i)[jc];
           if (ai > a.eps_piv) {
             bool slow;
-            double r = div_fast(s.T[i * S + cnt], ai, slow);
-            if (slow) r = ddiv_slow(s.T[i * S + cnt], ai);
+            double r = div_fast(s.row(i)[cnt], ai, slow);
+            if (slow) r = ddiv_slow(s.row(i)[cnt], ai);
             const Cand cc{r, bland ? s.bkey[i] : i, i};
             if (better<MIN_V>(cc, cr)) cr = cc;
           }
@@ -818,7 +840,7 @@ __global__ void __launch_bounds__(NT) simplex_block_kernel(SimplexArgs a) {
 #pragma unroll
           for (int sl = 0; sl < TM_NS; ++sl) {
             const int i = 128 * sl + 32 * tm.q + lane;
-            if (sl < tm.ns && (sl & 1) == tm.h && i < m) {
+            if (sl < tm.ns && (sl & 1) == tm.h && i < tm.mt) {
               myc[i] = cv[sl];
 #pragma unroll
               for (int q = 0; q < CL; ++q)
@@ -826,8 +848,8 @@ __global__ void __launch_bounds__(NT) simplex_block_kernel(SimplexArgs a) {
             }
           }
         }
-        for (int i = (TMR ? m : 0) + tid; i < nrow; i += NT) {
-          const double v = s.T[i * S + jcs];
+        for (int i = (TMR ? tm.mt : 0) + tid; i < nrow; i += NT) {
+          const double v = s.row(i)[jcs];
           myc[i] = v;
 #pragma unroll
           for (int q = 0; q < CL; ++q)
@@ -854,7 +876,7 @@ __global__ void __launch_bounds__(NT) simplex_block_kernel(SimplexArgs a) {
 #pragma unroll
           for (int sl = 0; sl < TM_NS; ++sl) {
             const int i = 128 * sl + 32 * tm.q + lane;
-            if (sl < tm.ns && (sl & 1) == tm.h && i < m) {
+            if (sl < tm.ns && (sl & 1) == tm.h && i < tm.mt) {
               if constexpr (PULL) {
                 myc[i] = cv[sl];
               } else {
@@ -865,8 +887,8 @@ __global__ void __launch_bounds__(NT) simplex_block_kernel(SimplexArgs a) {
           }
         }
         if (ce.pos >= 0)
-          for (int i = (TMR ? m : 0) + tid; i < nrow; i += NT) {
-            const double v = s.T[i * S + jc];
+          for (int i = (TMR ? tm.mt : 0) + tid; i < nrow; i += NT) {
+            const double v = s.row(i)[jc];
             if constexpr (PULL) {
               myc[i] = v;
             } else {
@@ -898,14 +920,14 @@ __global__ void __launch_bounds__(NT) simplex_block_kernel(SimplexArgs a) {
           tm_rows_to_smem(s, tm, S, m, (Wa + 7) >> 3);
           tm_live = false;
         }
-        const double wstar = s.T[(m + 1) * S + cnt];
+        const double wstar = s.row(m + 1)[cnt];
         if (wstar > a.eps_phase1 * fmax(1.0, binf)) { st = ST_INFEASIBLE; break; }
         for (int l = 0; l < m; ++l) {
           if (s.bkey[l] >= 0) continue;
           Cand cd{0.0, 0, -1};
           for (int j = tid; j < cnt; j += NT) {
             const int var = s.nbvar[j];
-            const double v = fabs(s.T[l * S + j]);
+            const double v = fabs(s.row(l)[j]);
             if (var != DEAD && v > a.eps_piv) {
               const Cand cc{v, var, g0 + j};
               if (better<MAX_V>(cc, cd)) cd = cc;
@@ -916,7 +938,7 @@ __global__ void __launch_bounds__(NT) simplex_block_kernel(SimplexArgs a) {
           const int owner = cd.pos / Q, jloc = cd.pos - owner * Q;
           if (cl.rank == owner) {
             for (int i = tid; i < m + 2; i += NT) {
-              const double v = s.T[i * S + jloc];
+              const double v = s.row(i)[jloc];
 #pragma unroll 1
               for (int q = 0; q < CL; ++q) cl.remote(s.colE, q)[i] = v;
             }
@@ -944,8 +966,8 @@ __global__ void __launch_bounds__(NT) simplex_block_kernel(SimplexArgs a) {
         if (record) {  // phase I recorded: dump the tableau it leaves, then stop (mode 1)
           for (int i = w; i < m; i += NW)
             for (int j = lane; j < Wa; j += 32) {
-              if (j < cnt) a.rec_T[(size_t)i * Wr + g0 + j] = s.T[i * S + j];
-              else if (cl.rank == 0) a.rec_T[(size_t)i * Wr + npos] = s.T[i * S + cnt];
+              if (j < cnt) a.rec_T[(size_t)i * Wr + g0 + j] = s.row(i)[j];
+              else if (cl.rank == 0) a.rec_T[(size_t)i * Wr + npos] = s.row(i)[cnt];
             }
           for (int j = tid; j < cnt; j += NT) a.rec_nbvar[g0 + j] = s.nbvar[j];
           if (cl.rank == 0) {
@@ -976,7 +998,7 @@ __global__ void __launch_bounds__(NT) simplex_block_kernel(SimplexArgs a) {
         if (cl.rank == 0 && tid == 0) a.rec_e[it1] = ce.pos;
       }
       if constexpr (TMR)
-        pivot_local_tm<tm_ns_max(CL)>(s, tm, wcol, S, Wa, m, nrow, l, cl.rank == win, jloc, ce.key, rr);
+        pivot_local_tm<tm_ns_max(CL), CL == 2>(s, tm, wcol, S, Wa, m, nrow, l, cl.rank == win, jloc, ce.key, rr);
       else
         pivot_local(s, wcol, S, Wa, nrow, l, cl.rank == win, jloc, ce.key, rr);
       pp ^= 1;
@@ -1003,7 +1025,7 @@ __global__ void __launch_bounds__(NT) simplex_block_kernel(SimplexArgs a) {
         a.status[lp] = st;
         a.iters[2 * lp] = it1;
         a.iters[2 * lp + 1] = it2;
-        a.obj[lp] = (st == ST_OPTIMAL) ? -s.T[m * S + cnt]
+        a.obj[lp] = (st == ST_OPTIMAL) ? -s.row(m)[cnt]
                   : (st == ST_UNBOUNDED) ? __longlong_as_double(0x7ff0000000000000ll)
                   : (st == ST_INFEASIBLE) ? __longlong_as_double(0xfff0000000000000ll)
                                           : __longlong_as_double(0x7ff8000000000000ll);
@@ -1016,7 +1038,7 @@ __global__ void __launch_bounds__(NT) simplex_block_kernel(SimplexArgs a) {
         if (st == ST_OPTIMAL)
           for (int i = tid; i < m; i += NT) {
             const int key = s.bkey[i];
-            if (key >= 0 && key < n) xk[key] = s.T[i * S + cnt];
+            if (key >= 0 && key < n) xk[key] = s.row(i)[cnt];
           }
       }
     }
@@ -1026,16 +1048,33 @@ __global__ void __launch_bounds__(NT) simplex_block_kernel(SimplexArgs a) {
     tm_fence_before();
     __syncthreads();
     tm_fence_after();
-    if (w == 0) tm_dealloc_n((uint32_t)s.ctl->pad, TM_COLS);
+    if (w == 0) tm_dealloc_n((uint32_t)s.ctl->pad, tmcols);
   }
+}
+
+// The kernels: the hybrid TMR variant (2-CTA clusters, two CTAs per SM) is compiled for 128
+// registers; every other variant keeps the default register heuristics of __launch_bounds__(NT).
+template <int CL, bool PULL, bool TMR>
+__global__ void __launch_bounds__(NT) simplex_block_kernel(SimplexArgs a) {
+  simplex_block_body<CL, PULL, TMR>(a);
+}
+template <bool PULL>
+__global__ void __launch_bounds__(NT, 2) simplex_block_hyb_kernel(SimplexArgs a) {
+  simplex_block_body<2, PULL, true>(a);
+}
+template <int CL, bool PULL, bool TMR>
+constexpr void (*block_kernel())(SimplexArgs) {
+  if constexpr (CL == 2 && TMR) return simplex_block_hyb_kernel<PULL>;
+  else return simplex_block_kernel<CL, PULL, TMR>;
 }
 
 }  // namespace
 
-static size_t smem_bytes(int cl, int m, int n, int kmax, bool pull, bool warm) {
+static size_t smem_bytes(int cl, int m, int n, int kmax, bool pull, bool warm, int h0 = 0) {
   const int Q = (n + kmax + cl - 1) / cl;
   const int S = row_stride(Q);
-  size_t bytes = sizeof(double) * ((size_t)(m + 2) * S + 2 * (size_t)(m + 2) + S);
+  // SMEM rows (all m + 2, or rows h0.. of the hybrid TMR layout), colE, fcol, prow, lraw
+  size_t bytes = sizeof(double) * ((size_t)(m + 2 - h0) * S + 2 * (size_t)(m + 2) + 2 * (size_t)S);
   bytes += sizeof(int) * ((size_t)(Q + 1) + (size_t)m + NW);  // nbvar, bkey, wcount
   bytes = (bytes + 15) & ~size_t(15);
   const size_t ncol = pull ? 1 : (size_t)cl;  // proposal columns per parity (PUSH: cl)
@@ -1047,6 +1086,28 @@ static size_t smem_bytes(int cl, int m, int n, int kmax, bool pull, bool warm) {
 size_t block_smem_bytes(int cl, int m, int n, int kmax) {
   return smem_bytes(cl, m, n, kmax, cl >= 8, true);
 }
+// Hybrid TMR layout (2-CTA clusters, two CTAs per SM): eligible when rows 0..127 fit one TMEM
+// slot of <= 256 columns and the remaining SMEM footprint admits exactly two CTAs per SM (more
+// would let a third CTA wait on the SM's TMEM).  Returns the global scratch one launch needs
+// (doubles: 128 rows x S per CTA, <= 2 CTAs per SM), 0 when not eligible.
+static bool hyb_eligible(int m, int n, int kmax, bool pull, bool warm, size_t* smem_out) {
+  if (m <= 128 || dev_flag("LPB_NO_TMEM") || dev_flag("LPB_NO_HYB")) return false;
+  const int Q = (n + kmax + 1) / 2;
+  if (tm_slot_cols(Q) > TM_COLS / 2) return false;
+  const size_t sm = smem_bytes(2, m, n, kmax, pull, warm, 128);
+  if (smem_out) *smem_out = sm;
+  return 2 * (sm + 1024) <= 227 * 1024 && 3 * (sm + 1024) > 228 * 1024;
+}
+size_t block_hyb_scratch_doubles(int m, int n, int kmax) {
+  const int Q = (n + kmax + 1) / 2;
+  if (!hyb_eligible(m, n, kmax, false, true, nullptr) &&
+      !hyb_eligible(m, n, kmax, true, true, nullptr) &&
+      !hyb_eligible(m, n, kmax, false, false, nullptr) &&
+      !hyb_eligible(m, n, kmax, true, false, nullptr))
+    return 0;
+  return (size_t)2 * device_sm_count() * 128 * row_stride(Q);
+}
+
 bool block_fits(int cl, int m, int n, int kmax) {
   const int Q = (n + kmax + cl - 1) / cl;  // pivot_local keeps <= 8 columns per lane
   return Q + 1 <= 256 && smem_bytes(cl, m, n, kmax, true, true) <= 227 * 1024;
@@ -1058,17 +1119,17 @@ static cudaError_t resident_ctas(const SimplexArgs& a, size_t smem, int* out) {
   const int sms = device_sm_count();
   static LaunchMemo memo;
   return memo.get(smem, out, [&](int& v, size_t attr) {
-    cudaError_t e = cudaFuncSetAttribute(simplex_block_kernel<CL, PULL, TMR>,
+    cudaError_t e = cudaFuncSetAttribute(block_kernel<CL, PULL, TMR>(),
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)attr);
     if (e != cudaSuccess) return e;
     if constexpr (CL > 8) {  // 16-CTA clusters are a non-portable (opt-in) size on sm_100
-      e = cudaFuncSetAttribute(simplex_block_kernel<CL, PULL, TMR>,
+      e = cudaFuncSetAttribute(block_kernel<CL, PULL, TMR>(),
                                cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
       if (e != cudaSuccess) return e;
     }
     if constexpr (CL == 1) {
       int per_sm = 0;
-      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, simplex_block_kernel<1, PULL, TMR>,
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, block_kernel<1, PULL, TMR>(),
                                                         NT, smem);
       v = per_sm * sms;
       return e;
@@ -1085,7 +1146,7 @@ static cudaError_t resident_ctas(const SimplexArgs& a, size_t smem, int* out) {
       q.dynamicSmemBytes = smem;
       q.gridDim = dim3(CL * sms);
       int clusters = 0;
-      e = cudaOccupancyMaxActiveClusters(&clusters, simplex_block_kernel<CL, PULL, TMR>, &q);
+      e = cudaOccupancyMaxActiveClusters(&clusters, block_kernel<CL, PULL, TMR>(), &q);
       v = clusters * CL;
       return e;
     }
@@ -1118,7 +1179,7 @@ static cudaError_t launch_variant(const SimplexArgs& a, size_t smem, int residen
   if (ctas_out) *ctas_out = grid;
   const cudaError_t e = cudaMemsetAsync(a.ticket, 0, sizeof(int), s);  // persistent LP ticket
   if (e != cudaSuccess) return e;
-  return cudaLaunchKernelEx(&cfg, simplex_block_kernel<CL, PULL, TMR>, a);
+  return cudaLaunchKernelEx(&cfg, block_kernel<CL, PULL, TMR>(), a);
 }
 
 // TMR (constraint rows in TMEM during the pivot loop) for clusters of >= 4 CTAs whose CTAs
@@ -1131,6 +1192,28 @@ static cudaError_t launch_variant(const SimplexArgs& a, size_t smem, int residen
 template <int CL, bool PULL>
 static cudaError_t launch_tm_or(const SimplexArgs& a, size_t smem, int resident,
                                 int grid_override, cudaStream_t s, int* ctas_out) {
+  if constexpr (CL == 2) {  // hybrid TMR: two CTAs (LPs) per SM instead of one
+    size_t sh = 0;
+    const int sms = device_sm_count();
+    if (a.tm_scr && hyb_eligible(a.m, a.n, a.kmax, PULL, a.mode == 2, &sh) &&
+        (grid_override <= 0 || grid_override * CL <= 2 * sms)) {
+      // the occupancy API counts one CTA per SM for kernels that use tcgen05; SMEM (checked by
+      // hyb_eligible), registers (<= 128 by the launch bounds) and TMEM (256 columns each)
+      // admit two, so the resident count is set here (after raising the SMEM attribute)
+      int rt = 0;
+      const cudaError_t e = resident_ctas<CL, PULL, true>(a, sh, &rt);
+      if (e != cudaSuccess) return e;
+      cudaFuncAttributes fa{};
+      const cudaError_t e2 = cudaFuncGetAttributes(&fa, block_kernel<CL, PULL, true>());
+      if (e2 != cudaSuccess) return e2;
+      rt = 2 * sms;
+      if (fa.numRegs <= 128 && rt > resident) {
+        SimplexArgs d = a;
+        d.tm_hyb = 1;
+        return launch_variant<CL, PULL, true>(d, sh, rt, grid_override, s, ctas_out);
+      }
+    }
+  }
   if constexpr (CL >= 4) {
     const int Q = (a.n + a.kmax + CL - 1) / CL;
     const int ns = tm_slots(a.m);
