@@ -351,6 +351,10 @@ __device__ __forceinline__ int compact_live(const Smem& s, int S, int cnt, int n
 // copied TMEM <-> SMEM at those points (once or twice per LP), and the pivot loop in between
 // never touches the SMEM copies of the constraint rows.
 constexpr int TM_NS = 4;     // row slots (m <= 512)
+#ifndef LPB_HYB_MT
+#define LPB_HYB_MT 128
+#endif
+constexpr int HYB_MT = LPB_HYB_MT;  // hybrid layout: constraint rows [0, HYB_MT) in TMEM
 // row slots a TMR variant is compiled for (register arrays): 2-CTA clusters m <= 256, 4-CTA
 // m <= 384, larger clusters m <= 512
 __host__ __device__ constexpr int tm_ns_max(int cl) { return cl <= 2 ? 2 : cl <= 4 ? 3 : 4; }
@@ -566,8 +570,8 @@ __device__ __forceinline__ void simplex_block_body(const SimplexArgs& a) {
   const bool hyb = TMR && CL == 2 && a.tm_hyb != 0;
   Smem s;
   s.S = S;
-  s.h0 = hyb ? 128 : 0;
-  s.gT = hyb ? a.tm_scr + (size_t)blockIdx.x * 128 * S : nullptr;
+  s.h0 = hyb ? HYB_MT : 0;
+  s.gT = hyb ? a.tm_scr + (size_t)blockIdx.x * HYB_MT * S : nullptr;
   s.T = reinterpret_cast<double*>(smem_raw);
   s.colE = s.T + (size_t)(RC - s.h0) * S;
   s.fcol = s.colE + RC;
@@ -600,7 +604,7 @@ __device__ __forceinline__ void simplex_block_body(const SimplexArgs& a) {
   // DSMEM may only be touched once every CTA of the cluster is running: one
   // cluster barrier before the first remote ticket write (racecheck finding); it also
   // publishes the initialised mbarriers.
-  TmRows tm{0u, hyb ? 1 : tm_slots(m), tm_slot_cols(Q), w & 3, w >> 2, hyb ? (m < 128 ? m : 128) : m};
+  TmRows tm{0u, hyb ? 1 : tm_slots(m), tm_slot_cols(Q), w & 3, w >> 2, hyb ? (m < HYB_MT ? m : HYB_MT) : m};
   const uint32_t tmcols = hyb ? TM_COLS / 2 : TM_COLS;  // hybrid: two CTAs share the SM's TMEM
   if constexpr (TMR) {
     if (w == 0) tm_alloc_n(reinterpret_cast<uint32_t*>(&s.ctl->pad), tmcols);
@@ -1091,10 +1095,10 @@ size_t block_smem_bytes(int cl, int m, int n, int kmax) {
 // would let a third CTA wait on the SM's TMEM).  Returns the global scratch one launch needs
 // (doubles: 128 rows x S per CTA, <= 2 CTAs per SM), 0 when not eligible.
 static bool hyb_eligible(int m, int n, int kmax, bool pull, bool warm, size_t* smem_out) {
-  if (m <= 128 || dev_flag("LPB_NO_TMEM") || dev_flag("LPB_NO_HYB")) return false;
+  if (m <= HYB_MT || dev_flag("LPB_NO_TMEM") || dev_flag("LPB_NO_HYB")) return false;
   const int Q = (n + kmax + 1) / 2;
   if (tm_slot_cols(Q) > TM_COLS / 2) return false;
-  const size_t sm = smem_bytes(2, m, n, kmax, pull, warm, 128);
+  const size_t sm = smem_bytes(2, m, n, kmax, pull, warm, HYB_MT);
   if (smem_out) *smem_out = sm;
   return 2 * (sm + 1024) <= 227 * 1024 && 3 * (sm + 1024) > 228 * 1024;
 }
@@ -1105,7 +1109,7 @@ size_t block_hyb_scratch_doubles(int m, int n, int kmax) {
       !hyb_eligible(m, n, kmax, false, false, nullptr) &&
       !hyb_eligible(m, n, kmax, true, false, nullptr))
     return 0;
-  return (size_t)2 * device_sm_count() * 128 * row_stride(Q);
+  return (size_t)2 * device_sm_count() * HYB_MT * row_stride(Q);
 }
 
 bool block_fits(int cl, int m, int n, int kmax) {
