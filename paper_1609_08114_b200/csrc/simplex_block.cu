@@ -810,8 +810,13 @@ __device__ __forceinline__ void simplex_block_body(const SimplexArgs& a) {
         }
         tm_fence_before();  // these loads precede the update's stores (after the barriers)
       }
-      if (ce.pos >= 0) {  // SMEM constraint rows (all of them, or the hybrid's rows 128..)
-        for (int i = (TMR ? tm.mt : 0) + tid; i < m; i += NT) {
+      // SMEM constraint rows (all of them, or the hybrid's rows 128..): in the hybrid layout the
+      // half-0 warps serve the TMEM slot above, so the half-1 warps take these rows
+      // (measured: cfg3 -1.4 %, and -1.6 % more for the column publish below)
+      const int st0 = hyb ? tid - NT / 2 : tid;
+      const int sstep = hyb ? NT / 2 : NT;
+      if (ce.pos >= 0 && st0 >= 0) {
+        for (int i = (TMR ? tm.mt : 0) + st0; i < m; i += sstep) {
           const double ai = s.row(i)[jc];
           if (ai > a.eps_piv) {
             bool slow;
@@ -852,7 +857,7 @@ __device__ __forceinline__ void simplex_block_body(const SimplexArgs& a) {
             }
           }
         }
-        for (int i = (TMR ? tm.mt : 0) + tid; i < nrow; i += NT) {
+        for (int i = (TMR ? tm.mt : 0) + st0; st0 >= 0 && i < nrow; i += sstep) {
           const double v = s.row(i)[jcs];
           myc[i] = v;
 #pragma unroll
